@@ -1,0 +1,467 @@
+#!/usr/bin/env python
+"""DART loss-pass benchmark (BASELINE.json metric):
+"loss fwd+bwd logit-tokens/s at V=152064 bf16, % of HBM peak, 1/2/4/8 GPU".
+
+One step = one whole pass over one batch: fwd sweep (all rows) -> C1
+all-gather of step entropies (N > 1) -> select -> bwd sweep (kept rows read +
+written, masked rows written as zeros) -> C2 stats all-reduce (N > 1).
+
+Usage:  python bench.py [--gpus N] [--steps K] [--warmup W] [--config single]
+        python bench.py --impl reference ...   (the float64 CPU oracle arm)
+For N > 1 launch with torchrun (one rank per GPU, NCCL).  Weak scaling: every
+rank owns its own 8-task batch of the config (global G = 8 N).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+PEAKS_PATH = os.path.join(ROOT, "MEASURED_PEAKS.json")
+FALLBACK_HBM = 6650.0  # GB/s, /opt/skills/guides/B200_PROFILING.md fallback
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+def hbm_peak():
+    try:
+        with open(PEAKS_PATH) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return FALLBACK_HBM, "fallback (B200_PROFILING.md)"
+
+
+# ------------------------------------------------------------------ clocks
+class ClockSampler:
+    FIELDS = "clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown," \
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown," \
+             "clocks_event_reasons.sw_power_cap,power.draw"
+
+    def __init__(self, index):
+        self.index = index
+        self.p = None
+
+    def start(self):
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                                       "--format=csv,noheader,nounits", "-lms", "50"],
+                                      stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.p = None
+
+    def stop(self):
+        if self.p is None:
+            return None
+        time.sleep(0.06)
+        self.p.terminate()
+        try:
+            out, _ = self.p.communicate(timeout=5)
+        except Exception:
+            self.p.kill()
+            out, _ = self.p.communicate()
+        rows = []
+        for line in out.strip().splitlines():
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) < 8:
+                continue
+            try:
+                rows.append(parts)
+            except Exception:
+                pass
+        if not rows:
+            return None
+        sm = [float(r[0]) for r in rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[3 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(rows)}
+
+
+# ------------------------------------------------------------------ setup
+def dist_setup(args):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    else:
+        if torch.cuda.is_available():
+            torch.cuda.set_device(0)
+    return world, rank, local
+
+
+def global_layout(per_rank_layout, world):
+    """Weak scaling: concatenate `world` copies of the per-rank layout
+    (rewards re-drawn per rank by the caller)."""
+    from paper_2509_23866_b200 import synth
+    L = per_rank_layout
+    tg, tr, tso, sto, fk = [], [], [0], [0], []
+    for r in range(world):
+        tg.append(L.traj_group + r * L.G)
+        tr.append(L.traj_reward)
+        tso.extend((L.traj_step_off[1:] + r * L.S).tolist())
+        sto.extend((L.step_tok_off[1:] + r * L.T).tolist())
+        fk.append(L.step_fork)
+    return synth.Layout(G=L.G * world, traj_group=np.concatenate(tg).astype(np.int32),
+                        traj_reward=np.concatenate(tr).astype(np.float32),
+                        traj_step_off=np.asarray(tso, dtype=np.int64),
+                        step_tok_off=np.asarray(sto, dtype=np.int64), step_fork=np.concatenate(fk))
+
+
+CONFIG_DESC = {
+    "single": "single GPU: 8 tasks x 8 rollouts x 15 steps x 64 tokens (T=61440), V=152064 bf16",
+    "single_ragged": "8 tasks x 8 rollouts, ragged 1-15 steps x 64 tokens, V=152064 bf16",
+    "mid": "2 tasks x 4 rollouts, ragged, V=152064 bf16 (parity size)",
+}
+
+
+# ------------------------------------------------------------------ our arm
+def run_dart(args):
+    from paper_2509_23866_b200 import build as B
+    if int(os.environ.get("RANK", "0")) == 0:
+        B.build()
+    world, rank, local = dist_setup(args)
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+    from paper_2509_23866_b200 import dart, synth
+    dev = torch.device("cuda", torch.cuda.current_device())
+    layout_r, V, dtype, _ = synth.config_layout(args.config, seed=args.seed)
+    glayout = global_layout(layout_r, world)
+    shards = []
+    for r in range(world):
+        shards.append(dart.Shard(r * layout_r.N_traj, (r + 1) * layout_r.N_traj, r * layout_r.S,
+                                 (r + 1) * layout_r.S, r * layout_r.T, (r + 1) * layout_r.T))
+    me = shards[rank]
+    cfg = dart.Config(entropy_q=args.q, beta_kl=args.beta, zero_fill_masked=0 if args.compact else 1,
+                      select_rule=dart.SEL_OFF if args.q <= 0 else dart.SEL_FLOOR)
+    t0 = time.time()
+    batch = synth.make_batch(args.config, seed=args.seed * 1000 + rank, device=dev, layout=layout_r, V=V,
+                             dtype=dtype)
+    torch.cuda.synchronize()
+    log(f"[rank {rank}] generated {layout_r.T} x {V} {dtype} logits in {time.time() - t0:.1f}s")
+    group = None
+    if world > 1:
+        import torch.distributed as dist
+        group = dist.group.WORLD
+    dl = dart.DartLoss(glayout, me, V, cfg, dev, logits_dtype=dtype, grad_dtype=torch.bfloat16,
+                       group=group, world_shards=shards)
+    inputs = (batch.logits, batch.target, batch.logp_old, batch.logp_rollout, batch.logp_ref)
+
+    stream = torch.cuda.current_stream()
+
+    def step():
+        dl.run(*inputs)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    dl.status.zero_()
+    dl.launches = 0
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+    torch.cuda.synchronize()
+
+    fwd_ms, bwd_ms = [], []
+    ev_pairs = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(args.steps)]
+    clk = ClockSampler(local)
+    clk.start()
+    time.sleep(0.15)
+    start = torch.cuda.Event(enable_timing=True)
+    end = torch.cuda.Event(enable_timing=True)
+    start.record(stream)
+    for k in range(args.steps):
+        step()
+    end.record(stream)
+    torch.cuda.synchronize()
+    clocks = clk.stop()
+    dart.set_timing_events()
+    elapsed_ms = start.elapsed_time(end)
+    launches = dl.launches
+    dl.check_status()
+
+    # per-kernel timing pass (same work; the library records the events on its
+    # stream immediately around the two sweep kernels)
+    for k in range(args.steps):
+        for x in ev_pairs[k]:
+            x.record(stream)          # creates the event handles
+    torch.cuda.synchronize()
+    for k in range(args.steps):
+        dart.set_timing_events(*ev_pairs[k])
+        step()
+    torch.cuda.synchronize()
+    dart.set_timing_events()
+    for k in range(args.steps):
+        e = ev_pairs[k]
+        fwd_ms.append(e[0].elapsed_time(e[1]))
+        bwd_ms.append(e[2].elapsed_time(e[3]))
+
+    ms = elapsed_ms / args.steps
+    if world > 1:
+        import torch.distributed as dist
+        t = torch.tensor([ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    T_tot = glayout.T
+    value = T_tot / (ms * 1e-3)
+
+    # algorithmic bytes: fwd 2V per row (+ 24 B of per-token
+    # I/O); bwd 4V per kept row (2V read + 2V write), 2V per masked row
+    # (write only; 0 with --compact)
+    keep = dl.keep.cpu().numpy()
+    n = np.diff(glayout.step_tok_off)
+    kept_tok_loc = int(n[me.step_begin:me.step_end][keep[me.step_begin:me.step_end].astype(bool)].sum())
+    masked_tok_loc = me.T_loc - kept_tok_loc
+    es = 2
+    fwd_bytes = me.T_loc * (es * V + 24)
+    bwd_bytes = kept_tok_loc * (2 * es * V) + (0 if args.compact else masked_tok_loc * es * V)
+    fwd_avg, bwd_avg = statistics.mean(fwd_ms), statistics.mean(bwd_ms)
+    peak, peak_src = hbm_peak()
+    fwd_gbs = fwd_bytes / (fwd_avg * 1e-3) / 1e9
+    bwd_gbs = bwd_bytes / (bwd_avg * 1e-3) / 1e9
+    dom = ("bwd_sweep", bwd_gbs, bwd_bytes, bwd_avg) if bwd_avg >= fwd_avg else ("fwd_sweep", fwd_gbs, fwd_bytes, fwd_avg)
+    step_bytes = fwd_bytes + bwd_bytes
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(tpath):
+        try:
+            with open(tpath) as f:
+                tj = json.load(f)
+            traffic = tj.get(dom[0], {}).get("dram_bytes_per_launch")
+        except Exception:
+            traffic = None
+
+    # ---- e2e through the public API with host buffers (pinned), rank-local
+    e2e = None
+    if not args.no_e2e:
+        e2e = run_e2e(args, dl, batch, stream, world)
+
+    # ---- CPU oracle baseline (rank 0, N == 1 only)
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        cpu = cpu_baseline(args, batch, cfg)
+
+    if rank == 0:
+        line = {
+            "metric": "loss fwd+bwd logit-tokens/s at V=152064 bf16, % of HBM peak, 1/2/4/8 GPU",
+            "value": value, "unit": "logit-tokens/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "bf16", "data": "synthetic (seeded; DESIGN.md §5 recipe)",
+            "config": {"workload": args.config, "desc": CONFIG_DESC.get(args.config, args.config),
+                       "global_tokens": T_tot, "tokens_per_gpu": me.T_loc, "V": V,
+                       "groups": glayout.G, "steps_total": glayout.S, "entropy_q": args.q, "beta_kl": args.beta,
+                       "is_cap": cfg.is_cap, "dlogits": "compact" if args.compact else "dense (masked rows zero)",
+                       "kept_token_frac": kept_tok_loc / max(me.T_loc, 1),
+                       "l2": "inputs larger than L2 (%.1f GB logits + %.1f GB dlogits per GPU >> 126 MB)" % (
+                           me.T_loc * V * es / 1e9, me.T_loc * V * es / 1e9),
+                       "parallelism": f"dp{world} (trajectory-sharded)"},
+            "roofline": {"bound": "hbm", "kernel": dom[0], "achieved": dom[1], "peak": peak,
+                         "peak_source": peak_src, "unit": "GB/s", "frac": dom[1] / peak,
+                         "traffic": traffic, "algorithmic_bytes_per_launch": dom[2],
+                         "avg_launch_ms": dom[3]},
+            "kernels": {"fwd_sweep": {"avg_ms": fwd_avg, "GBps": fwd_gbs, "frac": fwd_gbs / peak,
+                                      "bytes": fwd_bytes},
+                        "bwd_sweep": {"avg_ms": bwd_avg, "GBps": bwd_gbs, "frac": bwd_gbs / peak,
+                                      "bytes": bwd_bytes},
+                        "step_GBps": step_bytes / (ms * 1e-3) / 1e9,
+                        "step_frac": step_bytes / (ms * 1e-3) / 1e9 / peak},
+            "gpu_launches": launches,
+            "clocks": clocks,
+            "e2e": e2e,
+            "cpu_baseline": cpu,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def run_e2e(args, dl, batch, stream, world):
+    """Same pass through the public API with the step's inputs copied from
+    pinned host memory each step and the loss read back to the host."""
+    from paper_2509_23866_b200 import dart  # noqa: F401
+    host = [t.cpu().pin_memory() for t in (batch.logits, batch.target, batch.logp_old, batch.logp_rollout,
+                                           batch.logp_ref)]
+    dev_bufs = [torch.empty_like(t, device=batch.logits.device) for t in host]
+    loss_h = torch.empty(len(dl.stats), dtype=torch.float64).pin_memory()
+    h2d = sum(t.numel() * t.element_size() for t in host)
+    d2h = loss_h.numel() * loss_h.element_size()
+    steps = max(1, min(args.steps, args.e2e_steps))
+
+    def one():
+        for d, h in zip(dev_bufs, host):
+            d.copy_(h, non_blocking=True)
+        dl.run(*dev_bufs)
+        loss_h.copy_(dl.stats, non_blocking=True)
+
+    one()
+    torch.cuda.synchronize()
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+    s = torch.cuda.Event(enable_timing=True)
+    e = torch.cuda.Event(enable_timing=True)
+    s.record(stream)
+    for _ in range(steps):
+        one()
+    e.record(stream)
+    torch.cuda.synchronize()
+    _ = float(loss_h[0])
+    ms = s.elapsed_time(e) / steps
+    if world > 1:
+        import torch.distributed as dist
+        t = torch.tensor([ms], dtype=torch.float64, device=batch.logits.device)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    value = dl.layout.T / (ms * 1e-3)
+    del host, dev_bufs
+    return {"value": value, "unit": "logit-tokens/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+            "steps": steps, "ms_per_step": ms}
+
+
+# ------------------------------------------------------------------ oracle arms
+def oracle_sample(batch, n_traj=None, max_tokens=1024):
+    """A bounded sample of the workload: the first group's first trajectories,
+    truncated to whole steps totalling <= max_tokens tokens."""
+    from paper_2509_23866_b200 import synth
+    L = batch.layout
+    steps, toks = 0, 0
+    tso, sto = L.traj_step_off, L.step_tok_off
+    lens = []
+    i = 0
+    while i < L.N_traj and L.traj_group[i] == L.traj_group[0]:
+        li = 0
+        for s in range(tso[i], tso[i + 1]):
+            ns = int(sto[s + 1] - sto[s])
+            if toks + ns > max_tokens:
+                break
+            li += 1
+            toks += ns
+        if li == 0:
+            break
+        lens.append(li)
+        i += 1
+    # rebuild a 1-group layout with these trajectory lengths (rows taken in order)
+    rows = []
+    tso2, sto2 = [0], [0]
+    for j, li in enumerate(lens):
+        for s in range(tso[j], tso[j] + li):
+            rows.extend(range(int(sto[s]), int(sto[s + 1])))
+            sto2.append(sto2[-1] + int(sto[s + 1] - sto[s]))
+        tso2.append(tso2[-1] + li)
+    lay = synth.Layout(G=1, traj_group=np.zeros(len(lens), np.int32), traj_reward=L.traj_reward[:len(lens)],
+                       traj_step_off=np.asarray(tso2, np.int64), step_tok_off=np.asarray(sto2, np.int64),
+                       step_fork=np.zeros(len(sto2) - 1, bool))
+    rows_t = torch.as_tensor(rows, device=batch.logits.device)
+    d = dict(G=1, traj_group=lay.traj_group, traj_reward=lay.traj_reward.astype(np.float64),
+             traj_step_off=lay.traj_step_off, step_tok_off=lay.step_tok_off,
+             target=batch.target[rows_t].cpu().numpy().astype(np.int64),
+             logp_old=batch.logp_old[rows_t].cpu().numpy().astype(np.float64),
+             logp_rollout=batch.logp_rollout[rows_t].cpu().numpy().astype(np.float64),
+             logp_ref=batch.logp_ref[rows_t].cpu().numpy().astype(np.float64),
+             logits=batch.logits[rows_t].float().cpu().numpy())
+    return d, len(rows), len(lens), len(sto2) - 1
+
+
+def cpu_baseline(args, batch, cfg):
+    from oracle import dart_oracle as O
+    d, ntok, ntraj, nstep = oracle_sample(batch, max_tokens=args.cpu_tokens)
+    t0 = time.time()
+    O.loss_pass(d, cfg.as_f32())
+    dt = time.time() - t0
+    return {"value": ntok / dt, "unit": "logit-tokens/s", "cores": 1, "kind": "oracle",
+            "sample": f"{ntok} tokens ({ntraj} trajectories x whole steps of task 0, V={batch.V}); "
+                      f"full fwd+select+bwd incl. dlogits, float64 NumPy, single thread",
+            "seconds": dt}
+
+
+def run_reference(args):
+    """--impl reference: the float64 CPU oracle on the same config, each step a
+    bounded sample of the workload."""
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    from oracle import dart_oracle as O
+    from paper_2509_23866_b200 import dart, synth
+    layout_r, V, dtype, _ = synth.config_layout(args.config, seed=args.seed)
+    # generate only the sample's rows on the CPU (identical recipe)
+    batch = synth.make_batch(args.config, seed=args.seed * 1000, device="cpu", layout=_first_traj_layout(layout_r),
+                             V=V, dtype=dtype)
+    cfg = dart.Config(entropy_q=args.q, beta_kl=args.beta)
+    d, ntok, ntraj, nstep = oracle_sample(batch, max_tokens=args.cpu_tokens)
+    for _ in range(args.warmup):
+        O.loss_pass(d, cfg.as_f32())
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        O.loss_pass(d, cfg.as_f32())
+    dt = (time.perf_counter() - t0) / args.steps
+    value = ntok / dt
+    line = {"impl": "reference", "metric": "loss fwd+bwd logit-tokens/s at V=152064 bf16, % of HBM peak, 1/2/4/8 GPU",
+            "value": value, "unit": "logit-tokens/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": dt * 1e3, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "f64", "data": "synthetic (seeded; DESIGN.md §5 recipe)",
+            "config": {"workload": args.config, "desc": CONFIG_DESC.get(args.config, args.config),
+                       "sample_tokens": ntok},
+            "cpu_baseline": {"value": value, "unit": "logit-tokens/s", "cores": 1, "kind": "oracle",
+                             "sample": f"{ntok} tokens of {args.config} ({ntraj} trajectories of task 0), "
+                                       f"float64 NumPy oracle, single thread, per step"},
+            "e2e": {"value": value, "unit": "logit-tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def _first_traj_layout(L):
+    """The first task group of layout L (the oracle sample is drawn from it)."""
+    from paper_2509_23866_b200 import synth
+    nt = int(np.sum(L.traj_group == L.traj_group[0]))
+    tso = L.traj_step_off[:nt + 1]
+    S = int(tso[-1])
+    sto = L.step_tok_off[:S + 1]
+    return synth.Layout(G=1, traj_group=L.traj_group[:nt], traj_reward=L.traj_reward[:nt], traj_step_off=tso,
+                        step_tok_off=sto, step_fork=L.step_fork[:S])
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="dart", choices=["dart", "reference"])
+    ap.add_argument("--config", default="single")
+    ap.add_argument("--seed", type=int, default=0)
+    ap.add_argument("--q", type=float, default=0.2)
+    ap.add_argument("--beta", type=float, default=0.1)
+    ap.add_argument("--compact", action="store_true", help="do not zero-fill masked rows")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--cpu-tokens", type=int, default=1024)
+    args = ap.parse_args()
+    if args.warmup < 3:
+        log("warning: --warmup < 3 violates the timing rules; using 3")
+        args.warmup = 3
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_dart(args)
+
+
+if __name__ == "__main__":
+    main()

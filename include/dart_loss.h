@@ -1,0 +1,239 @@
+/*
+ * dart_loss.h -- C ABI of the B200-native DART policy-loss pass.
+ *
+ * DART (arXiv 2509.23866), trainer hot path: for every token row of the
+ * policy's output logits, a fused log-softmax gives the target log-prob and
+ * the entropy (Eq. 1 pi_theta(a|h,s); PAPER.md:238 H_{t,i});
+ * step entropies are averaged and the high-entropy steps of
+ * each task's step group kept; advantages are
+ * group-normalised over the step group D; the
+ * token-level truncated IS weight min(pi_old^Train / pi_old^Rollout, C)
+ * multiplies the clipped surrogate (Eq. 1,
+ * PAPER.md:252-264 Eq. 2) and the optional k3 KL term; the pass returns the
+ * loss L = -J_HE (to minimise) and dL/dlogits in bf16 (or fp32).
+ *
+ * Readings where the paper is silent/ambiguous: DESIGN.md §3.
+ *
+ * One pass = three calls on the same stream and the same workspace:
+ *     dart_loss_fwd      (advantages, fused sweep over all local rows,
+ *                         per-step entropy / loss sums)
+ *     [caller: all-gather the per-rank step entropies; a no-op at 1 rank]
+ *     dart_select_steps  (per-group order-statistic threshold, keep mask,
+ *                         global normaliser; identical on every rank)
+ *     dart_loss_bwd      (local loss partial + statistics, gradient sweep:
+ *                         kept rows read+write, masked rows write zeros)
+ *     [caller: all-reduce(SUM) the dart_stats partials]
+ *
+ * Conventions (all entry points):
+ *  - Pointers in the structs are DEVICE pointers unless marked "host".  The
+ *    structs themselves are host memory, read during the call only.
+ *  - Ownership: the caller allocates every buffer, including the workspace
+ *    (size from dart_workspace_size).  The library never allocates, frees,
+ *    retains a pointer past the call, or synchronises; every call is
+ *    asynchronous on `stream` (a cudaStream_t; NULL = legacy default stream).
+ *  - Errors: host-checkable problems return synchronously WITHOUT launching
+ *    (DART_ERR_INVALID_ARG / DART_ERR_UNSUPPORTED / DART_ERR_WORKSPACE);
+ *    a failed launch returns DART_ERR_CUDA.  Data errors found on the device
+ *    OR bits into *status (DART_STATUS_* below); the caller checks it after
+ *    the stream synchronises.  Outputs are unspecified when a bit is set.
+ *  - Determinism: bitwise deterministic for fixed inputs and device; no
+ *    floating-point atomics.  Per-row reductions use a canonical order that
+ *    does not depend on how rows are distributed, so sharding a batch over
+ *    ranks reproduces the single-rank bits (tests/test_virtual_ranks.py).
+ *  - Layout: logits row t (local) starts at logits + t*ld elements; rows must
+ *    be 16-byte aligned (base 16 B aligned, ld*sizeof(elem) % 16 == 0).
+ */
+#ifndef DART_LOSS_H
+#define DART_LOSS_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define DART_ABI_VERSION 1
+
+typedef enum {
+  DART_OK = 0,
+  DART_ERR_INVALID_ARG = 1,   /* NULL / misaligned pointer, bad size or config value */
+  DART_ERR_UNSUPPORTED = 2,   /* dtype or mode not supported */
+  DART_ERR_CUDA = 3,          /* kernel launch / CUDA runtime failure */
+  DART_ERR_WORKSPACE = 4      /* ws_bytes < dart_workspace_size(...) or ws NULL */
+} dart_status;
+
+typedef enum { DART_BF16 = 0, DART_F32 = 1 } dart_dtype;
+
+/* Normalisation of E over D (token aggregation unstated). */
+typedef enum {
+  DART_NORM_TOKEN_MEAN_KEPT = 0, /* L = sum_{kept tokens} ell / N_keep_tok   (default, DAPO-style) */
+  DART_NORM_STEP_MEAN_KEPT = 1,  /* L = (1/N_keep_step) sum_{kept s} (1/n_s) sum_{t in s} ell */
+  DART_NORM_TOKEN_MEAN_ALL = 2,  /* L = sum_{kept tokens} ell / T_global */
+  DART_NORM_STEP_MEAN_ALL = 3,   /* L = (1/S_global) sum_{kept s} (1/n_s) sum_{t in s} ell */
+  DART_NORM_SUM = 4              /* L = sum_{kept tokens} ell */
+} dart_norm_mode;
+
+/* Threshold tau_g over the n_g ascending-sorted step entropies s[] of group g
+ * ("at least larger than 20% steps", 264 tau_D^{0.2}). */
+typedef enum {
+  DART_SEL_FLOOR = 0,  /* tau = s[floor(q*n)]            (default; keeps >= ceil((1-q)n)) */
+  DART_SEL_CEIL = 1,   /* tau = s[min(ceil(q*n), n-1)] */
+  DART_SEL_LINEAR = 2, /* tau = s[lo] + f*(s[lo+1]-s[lo]), pos = q*(n-1)  (torch.quantile) */
+  DART_SEL_OFF = 3     /* keep every step of a valid group */
+} dart_select_rule;
+/* q*n and q*(n-1) are evaluated in float64 from the float32 value of entropy_q. */
+
+/* Device status bits (OR-accumulated into *status). */
+#define DART_STATUS_NONFINITE_LOGIT (1u << 0) /* NaN or +inf logit in a row */
+#define DART_STATUS_TARGET_RANGE    (1u << 1) /* target outside [0, V) */
+#define DART_STATUS_ROW_ALL_NEGINF  (1u << 2) /* every logit of a row is -inf */
+#define DART_STATUS_NONFINITE_LOGP  (1u << 3) /* non-finite logp_old / logp_rollout / logp_ref */
+#define DART_STATUS_EMPTY           (1u << 4) /* a step with 0 tokens or a trajectory with 0 steps */
+#define DART_STATUS_BAD_CSR         (1u << 5) /* decreasing offsets, traj_group decreasing or out of
+                                                 [0,G), or the local shard not aligned to steps */
+#define DART_STATUS_TARGET_NEGINF   (1u << 6) /* the target's logit is -inf (log-prob -inf) */
+
+/* Hyper-parameters (host struct).  Paper values: PAPER.md:575-578. */
+typedef struct {
+  float eps_low;          /* 0.2   clip lower bound 1-eps_low,  in (0,1)            */
+  float eps_high;         /* 0.28  clip upper bound 1+eps_high, in (0,1)            */
+  float is_cap;           /* C = 1 truncation of the IS weight, > 0                 */
+  float beta_kl;          /* 0.1   k3-KL coefficient, >= 0; 0 => logp_ref may be NULL */
+  float entropy_q;        /* 0.2   drop quantile, in [0,1)                           */
+  float inv_temperature;  /* 1.0   logits are scaled by this before the softmax, (0, 1e6] */
+  float adv_eps;          /* 0.0 (paper).  > 0: A = (R-mean)/(std+adv_eps) and sigma=0
+                             groups are kept with A = 0 (a verl-style flag)          */
+  int32_t norm_mode;      /* dart_norm_mode   */
+  int32_t select_rule;    /* dart_select_rule */
+  int32_t zero_fill_masked; /* 1: dense dlogits (masked rows written as zeros);
+                               0: masked rows are left untouched                   */
+} dart_cfg;
+
+/* GLOBAL batch metadata, replicated on every rank (device pointers). */
+typedef struct {
+  int64_t G;        /* task groups (step groups D) */
+  int64_t N_traj;   /* trajectories */
+  int64_t S;        /* steps */
+  int64_t T;        /* tokens = step_tok_off[S] */
+  const int32_t* traj_group;     /* [N_traj] group id in [0,G), non-decreasing */
+  const float* traj_reward;      /* [N_traj] R_i (in [0,1]) */
+  const int64_t* traj_step_off;  /* [N_traj+1] steps of traj i: [off[i], off[i+1]), >= 1 each */
+  const int64_t* step_tok_off;   /* [S+1] global tokens of step s, >= 1 each */
+} dart_meta;
+
+/* The LOCAL shard: a contiguous range of whole trajectories. */
+typedef struct {
+  const void* logits;      /* [T_loc, ld] elements of logits_dtype */
+  int32_t logits_dtype;    /* dart_dtype */
+  int64_t T_loc;           /* local token rows (>= 0) */
+  int64_t V;               /* vocabulary size (>= 1) */
+  int64_t ld;              /* row pitch in elements, >= V */
+  int64_t tok_begin;       /* global token index of local row 0 (= step_tok_off[step_begin]) */
+  int64_t step_begin;      /* global step index of local step 0 */
+  int64_t S_loc;           /* local steps */
+  const int32_t* target;       /* [T_loc] sampled token y_t in [0,V) */
+  const float* logp_old;       /* [T_loc] log pi_old^Train(y_t)   (stop-grad input) */
+  const float* logp_rollout;   /* [T_loc] log pi_old^Rollout(y_t) (recorded by the rollout engine) */
+  const float* logp_ref;       /* [T_loc] log pi_ref(y_t), or NULL when beta_kl == 0 */
+} dart_batch;
+
+/* Forward outputs (caller-allocated device buffers). */
+typedef struct {
+  float* lse;           /* [T_loc] log-sum-exp of z*inv_temperature (natural log) */
+  float* logp;          /* [T_loc] log pi_theta(y_t) */
+  float* tok_entropy;   /* [T_loc] H_t (nats) */
+  float* ell;           /* [T_loc] per-token loss term -w*min(rA, clip(r)A) + beta*k3 */
+  float* dell;          /* [T_loc] d ell / d logp */
+  float* step_entropy;  /* [S_loc] mean token entropy of each local step */
+  double* step_ell;     /* [S_loc] sum of ell over each local step's tokens */
+  float* adv;           /* [N_traj] advantage per trajectory (global) */
+  uint8_t* group_ok;    /* [G] 1 iff sigma_R > 0 (or adv_eps > 0) */
+  uint32_t* status;     /* [1] DART_STATUS_* bits, OR-accumulated (caller zeroes it) */
+} dart_fwd_out;
+
+/* Normaliser, written by dart_select_steps (device struct). */
+typedef struct {
+  int64_t n_keep_tok;   /* global kept tokens */
+  int64_t n_keep_step;  /* global kept steps */
+  int64_t n_tok;        /* global tokens T */
+  int64_t n_step;       /* global steps S */
+  double inv_norm;      /* 1/N for the mode (0 if N == 0); per-step 1/n_s applied in bwd */
+} dart_norm;
+
+/* Local partial sums, written by dart_loss_bwd (device struct).  All-reduce
+ * (SUM) over ranks; loss is already normalised (sum over ranks = L). */
+typedef struct {
+  double loss;
+  double n_tok;        /* local tokens */
+  double n_kept_tok;   /* local kept tokens */
+  double n_kept_step;  /* local kept steps */
+  double sum_clip;     /* kept tokens whose clipped branch is the min (no ratio gradient) */
+  double sum_trunc;    /* kept tokens with pi_old/pi_rollout >= C */
+  double sum_w;        /* sum of IS weights over kept tokens */
+  double sum_adv;      /* sum of A over kept tokens */
+  double sum_adv2;     /* sum of A^2 over kept tokens */
+  double sum_H;        /* sum of token entropies over all local tokens */
+  double sum_kl;       /* sum of k3 KL over kept tokens */
+} dart_stats;
+
+/* Bytes of workspace the three calls need for this shard (host-only, no launch). */
+size_t dart_workspace_size(const dart_batch* batch, const dart_meta* meta, const dart_cfg* cfg);
+
+/* Forward: advantages (all G groups), metadata checks, the fused sweep over
+ * all T_loc rows (one read of each logit row), per-step reductions.
+ * `out` fields are all required.  Workspace contents carry to select/bwd. */
+dart_status dart_loss_fwd(const dart_batch* batch, const dart_meta* meta, const dart_cfg* cfg,
+                          const dart_fwd_out* out, void* workspace, size_t ws_bytes, void* stream);
+
+/* Selection over the GLOBAL step entropies.
+ * step_entropy_gathered: [world * S_pad] floats, rank r's S_loc_r step
+ *   entropies at [r*S_pad, r*S_pad + S_loc_r) (the layout of an all-gather of
+ *   per-rank buffers padded to S_pad); for world == 1 pass the fwd's
+ *   step_entropy with S_pad = S.
+ * rank_step_off: [world+1] device int64, rank r owns global steps
+ *   [rank_step_off[r], rank_step_off[r+1]); rank_step_off[world] == S.
+ * Writes keep [S] (uint8), tau [G] (float; NaN for empty groups) and *norm. */
+dart_status dart_select_steps(const float* step_entropy_gathered, const int64_t* rank_step_off,
+                              int32_t world, int64_t S_pad, const dart_meta* meta,
+                              const dart_cfg* cfg, const uint8_t* group_ok, uint8_t* keep,
+                              float* tau, dart_norm* norm, void* workspace, size_t ws_bytes,
+                              void* stream);
+
+/* Backward: local loss partial + statistics into *stats, then dL/dlogits for
+ * the local rows: kept rows re-read once and written once, masked rows
+ * written as zeros (zero_fill_masked=1) or skipped.  dlogits: [T_loc, ldg]
+ * of grad_dtype, 16-byte aligned rows. */
+dart_status dart_loss_bwd(const dart_batch* batch, const dart_meta* meta, const dart_cfg* cfg,
+                          const dart_fwd_out* fwd, const uint8_t* keep, const dart_norm* norm,
+                          void* dlogits, int32_t grad_dtype, int64_t ldg, dart_stats* stats,
+                          void* workspace, size_t ws_bytes, void* stream);
+
+/* Single-rank convenience: fwd + select (world = 1) + bwd on one stream. */
+dart_status dart_loss_pass(const dart_batch* batch, const dart_meta* meta, const dart_cfg* cfg,
+                           const dart_fwd_out* fwd, uint8_t* keep, float* tau, dart_norm* norm,
+                           void* dlogits, int32_t grad_dtype, int64_t ldg, dart_stats* stats,
+                           void* workspace, size_t ws_bytes, void* stream);
+
+/* Static description of a status code (never NULL). */
+const char* dart_status_str(dart_status s);
+
+/* ABI version (DART_ABI_VERSION) -- lets bindings check they match. */
+int32_t dart_abi_version(void);
+
+/* Number of kernel launches the most recent successful fwd / select / bwd
+ * call on this host thread issued (for the bench's gpu_launches count). */
+int32_t dart_last_launch_count(void);
+
+/* Profiling hook (host thread-local): when set, the next fwd / bwd calls
+ * record these cudaEvent_t handles on their stream immediately before and
+ * after the sweep kernel (K1 resp. K4), so the caller can time the hot
+ * kernels alone with CUDA events.  Pass NULLs to disable.  Events are owned
+ * by the caller. */
+void dart_set_timing_events(void* fwd_sweep_begin, void* fwd_sweep_end, void* bwd_sweep_begin,
+                            void* bwd_sweep_end);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* DART_LOSS_H */

@@ -1,0 +1,407 @@
+// dart_abi.cu -- the C ABI of include/dart_loss.h: host-side argument
+// validation, the workspace layout, and the kernel launch sequence.
+// Never allocates, never synchronises; every launch goes to `stream`.
+#include <cmath>
+#include <cstring>
+
+#include "dart_common.cuh"
+#include "dart_internal.h"
+
+using namespace dart;
+
+namespace {
+
+thread_local int32_t g_launches = 0;
+thread_local int32_t g_last_launches = 0;
+thread_local cudaEvent_t g_ev[4] = {nullptr, nullptr, nullptr, nullptr};
+
+void rec(int i, cudaStream_t s) {
+  if (g_ev[i]) (void)cudaEventRecord(g_ev[i], s);
+}
+
+int sm_count() {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return 148;
+  static int cache[64] = {0};
+  if (dev >= 0 && dev < 64 && cache[dev]) return cache[dev];
+  int n = 148;
+  if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n <= 0) n = 148;
+  if (dev >= 0 && dev < 64) cache[dev] = n;
+  return n;
+}
+
+inline size_t al256(size_t x) { return (x + 255) & ~(size_t)255; }
+inline bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+inline size_t esize(int32_t dt) { return dt == DART_BF16 ? 2 : 4; }
+
+// Global-metadata regions first (their offsets depend only on S and G, so
+// dart_select_steps can address them without knowing the shard), then the
+// per-shard regions.
+size_t ws_global_prefix(const dart_meta* m, WsLayout* L) {
+  size_t off = 0;
+  auto take = [&](size_t bytes) {
+    const size_t o = off;
+    off += al256(bytes ? bytes : 1);
+    return o;
+  };
+  const size_t S = (size_t)(m->S > 0 ? m->S : 0);
+  const size_t G = (size_t)(m->G > 0 ? m->G : 0);
+  const size_t h = take(S * 4), gt = take((G + 1) * 8), gs = take(G * 8), gk = take(G * 8);
+  if (L) {
+    L->H_glob = h;
+    L->grp_traj = gt;
+    L->grp_keep_step = gs;
+    L->grp_keep_tok = gk;
+  }
+  return off;
+}
+
+WsLayout ws_layout(const dart_batch* b, const dart_meta* m) {
+  WsLayout L;
+  size_t off = ws_global_prefix(m, &L);
+  auto take = [&](size_t bytes) {
+    const size_t o = off;
+    off += al256(bytes ? bytes : 1);
+    return o;
+  };
+  const size_t T = (size_t)(b->T_loc > 0 ? b->T_loc : 0);
+  const size_t S_loc = (size_t)(b->S_loc > 0 ? b->S_loc : 0);
+  L.tok_adv = take(T * 4);
+  L.tok_step = take(T * 4);
+  L.lse2 = take(T * 4);
+  L.aux_w = take(T * 4);
+  L.aux_kl = take(T * 4);
+  L.aux_flags = take(T);
+  L.gs = take(T * 4);
+  L.step_stats = take(S_loc * NSTAT * 8);
+  L.step_cost = take((S_loc + 1) * 8);
+  L.step_scale = take(S_loc * 8);
+  L.split_alloc = T > 0 && T <= (size_t)SPLIT_MAX_ROWS;
+  if (L.split_alloc) {
+    L.part_m = take(T * KSEG * 4);
+    L.part_s = take(T * KSEG * 8);
+    L.part_u = take(T * KSEG * 8);
+    L.row_cnt = take(T * 4);
+  } else {
+    L.part_m = L.part_s = L.part_u = L.row_cnt = 0;
+  }
+  L.bwd_misc = take(256);
+  L.total = off;
+  return L;
+}
+
+template <typename T>
+inline T* at(void* ws, size_t off) {
+  return reinterpret_cast<T*>(static_cast<uint8_t*>(ws) + off);
+}
+
+bool cfg_ok(const dart_cfg* c) {
+  if (!c) return false;
+  if (!(c->eps_low > 0.f && c->eps_low < 1.f)) return false;
+  if (!(c->eps_high > 0.f && c->eps_high < 1.f)) return false;
+  if (!(c->is_cap > 0.f) || !std::isfinite(c->is_cap)) return false;
+  if (!(c->beta_kl >= 0.f) || !std::isfinite(c->beta_kl)) return false;
+  if (!(c->entropy_q >= 0.f && c->entropy_q < 1.f)) return false;
+  if (!(c->inv_temperature > 0.f && c->inv_temperature <= 1e6f)) return false;
+  if (!(c->adv_eps >= 0.f) || !std::isfinite(c->adv_eps)) return false;
+  if (c->norm_mode < DART_NORM_TOKEN_MEAN_KEPT || c->norm_mode > DART_NORM_SUM) return false;
+  if (c->select_rule < DART_SEL_FLOOR || c->select_rule > DART_SEL_OFF) return false;
+  return true;
+}
+
+bool meta_ok(const dart_meta* m) {
+  if (!m) return false;
+  if (m->G < 0 || m->N_traj < 0 || m->S < 0 || m->T < 0) return false;
+  if (m->N_traj > 0 && m->G < 1) return false;
+  if (!m->traj_step_off || !m->step_tok_off) return false;
+  if (m->N_traj > 0 && (!m->traj_group || !m->traj_reward)) return false;
+  if (m->T > ((int64_t)1 << 40)) return false;
+  return true;
+}
+
+dart_status batch_check(const dart_batch* b, const dart_meta* m, const dart_cfg* c) {
+  if (!b || !meta_ok(m) || !cfg_ok(c)) return DART_ERR_INVALID_ARG;
+  if (b->logits_dtype != DART_BF16 && b->logits_dtype != DART_F32) return DART_ERR_UNSUPPORTED;
+  if (b->T_loc < 0 || b->V < 1 || b->ld < b->V || b->S_loc < 0) return DART_ERR_INVALID_ARG;
+  if (b->V > 0x7fffffffLL) return DART_ERR_INVALID_ARG;
+  if (b->tok_begin < 0 || b->tok_begin + b->T_loc > m->T) return DART_ERR_INVALID_ARG;
+  if (b->step_begin < 0 || b->step_begin + b->S_loc > m->S) return DART_ERR_INVALID_ARG;
+  if (b->T_loc > 0) {
+    if (!b->logits || !b->target || !b->logp_old || !b->logp_rollout) return DART_ERR_INVALID_ARG;
+    if (c->beta_kl > 0.f && !b->logp_ref) return DART_ERR_INVALID_ARG;
+    if (!aligned16(b->logits) || ((size_t)b->ld * esize(b->logits_dtype)) % 16 != 0) return DART_ERR_INVALID_ARG;
+    if (b->S_loc < 1) return DART_ERR_INVALID_ARG;
+  }
+  return DART_OK;
+}
+
+dart_status fwd_out_check(const dart_batch* b, const dart_meta* m, const dart_fwd_out* o) {
+  if (!o || !o->status) return DART_ERR_INVALID_ARG;
+  if (b->T_loc > 0 && (!o->lse || !o->logp || !o->tok_entropy || !o->ell || !o->dell)) return DART_ERR_INVALID_ARG;
+  if (b->S_loc > 0 && (!o->step_entropy || !o->step_ell)) return DART_ERR_INVALID_ARG;
+  if (m->N_traj > 0 && !o->adv) return DART_ERR_INVALID_ARG;
+  if (m->G > 0 && !o->group_ok) return DART_ERR_INVALID_ARG;
+  return DART_OK;
+}
+
+dart_status cuda_status(cudaError_t e) {
+  if (e != cudaSuccess) {
+    (void)cudaGetLastError();
+    return DART_ERR_CUDA;
+  }
+  ++g_launches;
+  return DART_OK;
+}
+
+int choose_nsplit(const dart_batch* b, const WsLayout& L, int64_t nvec) {
+  if (!L.split_alloc || nvec < KSEG) return 1;
+  const int64_t target_units = 4LL * sm_count() * 16;
+  int ns = 1;
+  while (ns < KSEG && b->T_loc * ns < target_units) ns *= 2;
+  return ns;
+}
+
+}  // namespace
+
+#define DART_TRY(expr)                        \
+  do {                                        \
+    dart_status _s = cuda_status((expr));     \
+    if (_s != DART_OK) return _s;             \
+  } while (0)
+// runtime calls that are not kernels of ours (not counted as launches)
+#define DART_TRY_RT(expr)                     \
+  do {                                        \
+    if ((expr) != cudaSuccess) {              \
+      (void)cudaGetLastError();               \
+      return DART_ERR_CUDA;                   \
+    }                                         \
+  } while (0)
+
+extern "C" {
+
+int32_t dart_abi_version(void) { return DART_ABI_VERSION; }
+
+int32_t dart_last_launch_count(void) { return g_last_launches; }
+
+void dart_set_timing_events(void* a, void* b, void* c, void* d) {
+  g_ev[0] = static_cast<cudaEvent_t>(a);
+  g_ev[1] = static_cast<cudaEvent_t>(b);
+  g_ev[2] = static_cast<cudaEvent_t>(c);
+  g_ev[3] = static_cast<cudaEvent_t>(d);
+}
+
+const char* dart_status_str(dart_status s) {
+  switch (s) {
+    case DART_OK: return "DART_OK";
+    case DART_ERR_INVALID_ARG: return "DART_ERR_INVALID_ARG: invalid argument (NULL/misaligned pointer, size or config value)";
+    case DART_ERR_UNSUPPORTED: return "DART_ERR_UNSUPPORTED: unsupported dtype or mode";
+    case DART_ERR_CUDA: return "DART_ERR_CUDA: CUDA launch or runtime failure";
+    case DART_ERR_WORKSPACE: return "DART_ERR_WORKSPACE: workspace missing or smaller than dart_workspace_size()";
+  }
+  return "DART_UNKNOWN_STATUS";
+}
+
+size_t dart_workspace_size(const dart_batch* b, const dart_meta* m, const dart_cfg* c) {
+  (void)c;
+  if (!b || !m) return 0;
+  return ws_layout(b, m).total;
+}
+
+dart_status dart_loss_fwd(const dart_batch* b, const dart_meta* m, const dart_cfg* c, const dart_fwd_out* o,
+                          void* ws, size_t ws_bytes, void* stream) {
+  dart_status st = batch_check(b, m, c);
+  if (st != DART_OK) return st;
+  if ((st = fwd_out_check(b, m, o)) != DART_OK) return st;
+  const WsLayout L = ws_layout(b, m);
+  if (!ws || ws_bytes < L.total) return DART_ERR_WORKSPACE;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  g_launches = 0;
+
+  // K0a: advantages of all G groups + metadata checks
+  AdvParams ap;
+  ap.G = m->G; ap.N_traj = m->N_traj; ap.S = m->S; ap.T = m->T;
+  ap.traj_group = m->traj_group; ap.traj_reward = m->traj_reward;
+  ap.traj_step_off = m->traj_step_off; ap.step_tok_off = m->step_tok_off;
+  ap.adv_eps = (double)c->adv_eps;
+  ap.adv = o->adv; ap.group_ok = o->group_ok;
+  ap.grp_traj = at<int64_t>(ws, L.grp_traj);
+  ap.status = o->status;
+  DART_TRY(launch_adv(ap, s));
+
+  // K0b: token -> (step, A) tables
+  TokMetaParams tp;
+  tp.S = m->S; tp.N_traj = m->N_traj; tp.T_loc = b->T_loc; tp.tok_begin = b->tok_begin;
+  tp.step_begin = b->step_begin; tp.S_loc = b->S_loc;
+  tp.traj_step_off = m->traj_step_off; tp.step_tok_off = m->step_tok_off;
+  tp.adv = o->adv;
+  tp.tok_adv = at<float>(ws, L.tok_adv);
+  tp.tok_step = at<int32_t>(ws, L.tok_step);
+  tp.status = o->status;
+  DART_TRY(launch_tok_meta(tp, s));
+
+  if (b->T_loc > 0) {
+    const size_t es = esize(b->logits_dtype);
+    const int64_t nvec = (int64_t)((b->V * es + 15) / 16);
+    FwdParams fp;
+    fp.logits = static_cast<const uint8_t*>(b->logits);
+    fp.ld_bytes = b->ld * (int64_t)es;
+    fp.V = b->V; fp.T_loc = b->T_loc; fp.nvec = nvec;
+    fp.c2 = (float)((double)c->inv_temperature * LOG2E_D);
+    fp.target = b->target; fp.logp_old = b->logp_old; fp.logp_roll = b->logp_rollout;
+    fp.logp_ref = b->logp_ref;
+    fp.tok_adv = at<float>(ws, L.tok_adv);
+    fp.eps_low = c->eps_low; fp.eps_high = c->eps_high; fp.is_cap = c->is_cap; fp.beta = c->beta_kl;
+    fp.lse = o->lse; fp.logp = o->logp; fp.H = o->tok_entropy; fp.ell = o->ell; fp.dell = o->dell;
+    fp.lse2 = at<float>(ws, L.lse2);
+    fp.aux_w = at<float>(ws, L.aux_w);
+    fp.aux_kl = at<float>(ws, L.aux_kl);
+    fp.aux_flags = at<uint8_t>(ws, L.aux_flags);
+    fp.status = o->status;
+    fp.nsplit = choose_nsplit(b, L, nvec);
+    fp.part_m = L.split_alloc ? at<float>(ws, L.part_m) : nullptr;
+    fp.part_s = L.split_alloc ? at<double>(ws, L.part_s) : nullptr;
+    fp.part_u = L.split_alloc ? at<double>(ws, L.part_u) : nullptr;
+    fp.row_cnt = L.split_alloc ? at<uint32_t>(ws, L.row_cnt) : nullptr;
+    if (fp.nsplit > 1) DART_TRY_RT(cudaMemsetAsync(fp.row_cnt, 0, (size_t)b->T_loc * 4, s));
+    rec(0, s);
+    DART_TRY(launch_fwd_sweep(fp, b->logits_dtype == DART_BF16, sm_count(), s));
+    rec(1, s);
+
+    StepReduceParams sp;
+    sp.T_loc = b->T_loc; sp.tok_begin = b->tok_begin; sp.step_begin = b->step_begin; sp.S_loc = b->S_loc;
+    sp.step_tok_off = m->step_tok_off;
+    sp.H = o->tok_entropy; sp.ell = o->ell;
+    sp.aux_w = fp.aux_w; sp.aux_kl = fp.aux_kl; sp.tok_adv = fp.tok_adv; sp.aux_flags = fp.aux_flags;
+    sp.step_entropy = o->step_entropy; sp.step_ell = o->step_ell;
+    sp.step_stats = at<double>(ws, L.step_stats);
+    DART_TRY(launch_step_reduce(sp, s));
+  }
+  g_last_launches = g_launches;
+  return DART_OK;
+}
+
+dart_status dart_select_steps(const float* gathered, const int64_t* rank_step_off, int32_t world, int64_t S_pad,
+                              const dart_meta* m, const dart_cfg* c, const uint8_t* group_ok, uint8_t* keep,
+                              float* tau, dart_norm* norm, void* ws, size_t ws_bytes, void* stream) {
+  if (!meta_ok(m) || !cfg_ok(c)) return DART_ERR_INVALID_ARG;
+  if (world < 1 || S_pad < 0) return DART_ERR_INVALID_ARG;
+  if (!norm || (m->S > 0 && (!gathered || !keep)) || (m->G > 0 && (!group_ok || !tau))) return DART_ERR_INVALID_ARG;
+  if (world > 1 && !rank_step_off) return DART_ERR_INVALID_ARG;
+  if (world == 1 && S_pad < m->S) return DART_ERR_INVALID_ARG;
+  if ((int64_t)world * S_pad < m->S) return DART_ERR_INVALID_ARG;
+  WsLayout L;
+  const size_t need = ws_global_prefix(m, &L);
+  if (!ws || ws_bytes < need) return DART_ERR_WORKSPACE;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  g_launches = 0;
+
+  const float* H = gathered;
+  if (world > 1) {  // all-gather layout -> global step order
+    UnpackParams up;
+    up.gathered = gathered; up.rank_step_off = rank_step_off; up.world = world;
+    up.S_pad = S_pad; up.S = m->S;
+    up.H = at<float>(ws, L.H_glob);
+    DART_TRY(launch_unpack(up, s));
+    H = up.H;
+  }
+  SelectParams sp;
+  sp.G = m->G; sp.N_traj = m->N_traj; sp.S = m->S; sp.T = m->T;
+  sp.traj_step_off = m->traj_step_off; sp.step_tok_off = m->step_tok_off;
+  sp.grp_traj = at<int64_t>(ws, L.grp_traj);
+  sp.group_ok = group_ok; sp.H = H;
+  sp.q = c->entropy_q; sp.rule = c->select_rule;
+  sp.keep = keep; sp.tau = tau;
+  sp.grp_keep_step = at<int64_t>(ws, L.grp_keep_step);
+  sp.grp_keep_tok = at<int64_t>(ws, L.grp_keep_tok);
+  DART_TRY(launch_select(sp, s));
+
+  NormParams np;
+  np.G = m->G; np.S = m->S; np.T = m->T; np.norm_mode = c->norm_mode;
+  np.grp_keep_step = sp.grp_keep_step; np.grp_keep_tok = sp.grp_keep_tok;
+  np.norm = norm;
+  DART_TRY(launch_norm(np, s));
+  g_last_launches = g_launches;
+  return DART_OK;
+}
+
+dart_status dart_loss_bwd(const dart_batch* b, const dart_meta* m, const dart_cfg* c, const dart_fwd_out* f,
+                          const uint8_t* keep, const dart_norm* norm, void* dlogits, int32_t grad_dtype,
+                          int64_t ldg, dart_stats* stats, void* ws, size_t ws_bytes, void* stream) {
+  dart_status st = batch_check(b, m, c);
+  if (st != DART_OK) return st;
+  if ((st = fwd_out_check(b, m, f)) != DART_OK) return st;
+  if (grad_dtype != DART_BF16 && grad_dtype != DART_F32) return DART_ERR_UNSUPPORTED;
+  if (!norm || !stats || (m->S > 0 && !keep)) return DART_ERR_INVALID_ARG;
+  if (b->T_loc > 0) {
+    if (!dlogits || ldg < b->V || !aligned16(dlogits) || ((size_t)ldg * esize(grad_dtype)) % 16 != 0)
+      return DART_ERR_INVALID_ARG;
+  }
+  const WsLayout L = ws_layout(b, m);
+  if (!ws || ws_bytes < L.total) return DART_ERR_WORKSPACE;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  g_launches = 0;
+  const size_t es = esize(b->logits_dtype);
+  const int64_t nvec = (int64_t)((b->V * es + 15) / 16);
+  const int64_t nch = (nvec + CH_VEC - 1) / CH_VEC;
+
+  BwdPrepParams pp;
+  pp.T_loc = b->T_loc; pp.tok_begin = b->tok_begin; pp.step_begin = b->step_begin; pp.S_loc = b->S_loc;
+  pp.nch = nch; pp.norm_mode = c->norm_mode; pp.zero_fill = c->zero_fill_masked ? 1 : 0;
+  pp.step_tok_off = m->step_tok_off; pp.keep = keep; pp.norm = norm;
+  pp.step_ell = f->step_ell; pp.step_stats = at<double>(ws, L.step_stats);
+  pp.step_scale = at<double>(ws, L.step_scale);
+  pp.step_cost = at<int64_t>(ws, L.step_cost);
+  pp.stats = stats;
+  DART_TRY(launch_bwd_prep(pp, s));
+
+  if (b->T_loc > 0) {
+    GsParams gp;
+    gp.T_loc = b->T_loc; gp.tok_step = at<int32_t>(ws, L.tok_step); gp.step_scale = pp.step_scale;
+    gp.dell = f->dell; gp.invT = (double)c->inv_temperature; gp.gs = at<float>(ws, L.gs);
+    DART_TRY(launch_gs(gp, s));
+
+    BwdParams bp;
+    bp.logits = static_cast<const uint8_t*>(b->logits);
+    bp.ld_bytes = b->ld * (int64_t)es;
+    bp.V = b->V; bp.T_loc = b->T_loc; bp.nvec = nvec; bp.nch = nch;
+    bp.dlogits = static_cast<uint8_t*>(dlogits);
+    bp.ldg_bytes = ldg * (int64_t)esize(grad_dtype);
+    bp.c2 = (float)((double)c->inv_temperature * LOG2E_D);
+    bp.target = b->target;
+    bp.lse2 = at<float>(ws, L.lse2);
+    bp.gs = gp.gs;
+    bp.step_tok_off = m->step_tok_off;
+    bp.tok_begin = b->tok_begin; bp.step_begin = b->step_begin; bp.S_loc = b->S_loc;
+    bp.keep = keep;
+    bp.step_cost = pp.step_cost;
+    bp.zero_fill = pp.zero_fill;
+    rec(2, s);
+    DART_TRY(launch_bwd_sweep(bp, b->logits_dtype == DART_BF16, grad_dtype == DART_BF16, sm_count(), s));
+    rec(3, s);
+  }
+  g_last_launches = g_launches;
+  return DART_OK;
+}
+
+dart_status dart_loss_pass(const dart_batch* b, const dart_meta* m, const dart_cfg* c, const dart_fwd_out* f,
+                           uint8_t* keep, float* tau, dart_norm* norm, void* dlogits, int32_t grad_dtype,
+                           int64_t ldg, dart_stats* stats, void* ws, size_t ws_bytes, void* stream) {
+  dart_status st = batch_check(b, m, c);
+  if (st != DART_OK) return st;
+  // single rank: the shard must be the whole batch
+  if (b->tok_begin != 0 || b->T_loc != m->T || b->step_begin != 0 || b->S_loc != m->S) return DART_ERR_INVALID_ARG;
+  int32_t total = 0;
+  if ((st = dart_loss_fwd(b, m, c, f, ws, ws_bytes, stream)) != DART_OK) return st;
+  total += g_last_launches;
+  if ((st = dart_select_steps(f->step_entropy, nullptr, 1, m->S, m, c, f->group_ok, keep, tau, norm, ws, ws_bytes,
+                              stream)) != DART_OK)
+    return st;
+  total += g_last_launches;
+  if ((st = dart_loss_bwd(b, m, c, f, keep, norm, dlogits, grad_dtype, ldg, stats, ws, ws_bytes, stream)) != DART_OK)
+    return st;
+  total += g_last_launches;
+  g_last_launches = total;
+  return DART_OK;
+}
+
+}  // extern "C"

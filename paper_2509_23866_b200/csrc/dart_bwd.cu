@@ -1,0 +1,420 @@
+// dart_bwd.cu -- backward half of the DART loss pass (sm_100a).
+//
+//   K6  bwd_prep_kernel  one CTA, fixed order over the local steps: per-step
+//                        loss weight c_s (normaliser of PAPER.md:255, SURVEY
+//                        Q11), the local loss partial sum_{kept s} c_s sum ell
+//                        and statistics (fp64), and the prefix of per-step
+//                        chunk costs that balances the sweep across warps.
+//   K4a gs_kernel        per local row: g_t = c_s * dell_t * inv_temperature.
+//   K4  bwd_sweep        THE SECOND HOT LOOP: for rows of kept steps, re-read
+//                        the logits (bulk copies into a per-warp ring) and
+//                        write dL/dz_v = g_t (delta_{v,y} - p_v) rounded to
+//                        bf16 (RNE); rows of masked steps are written as
+//                        zeros without being read (the
+//                        indicator removes them from the objective).
+#include "dart_common.cuh"
+#include "dart_internal.h"
+
+namespace dart {
+
+// ============================================================== K6
+constexpr int NV = 11;  // dart_stats fields
+
+__global__ void __launch_bounds__(1024) bwd_prep_kernel(BwdPrepParams p) {
+  __shared__ double red[32][NV];
+  __shared__ long long wsum[32];
+  __shared__ long long s_carry;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const dart_norm* nrm = reinterpret_cast<const dart_norm*>(p.norm);
+  const double inv_norm = nrm->inv_norm;
+  const bool step_mode = (p.norm_mode == DART_NORM_STEP_MEAN_KEPT || p.norm_mode == DART_NORM_STEP_MEAN_ALL);
+  double tot[NV];
+#pragma unroll
+  for (int i = 0; i < NV; ++i) tot[i] = 0.0;  // meaningful in thread 0 only
+  if (tid == 0) { s_carry = 0; p.step_cost[0] = 0; }
+  __syncthreads();
+  for (int64_t base = 0; base < p.S_loc; base += blockDim.x) {
+    const int64_t s = base + tid;
+    double v[NV];
+#pragma unroll
+    for (int i = 0; i < NV; ++i) v[i] = 0.0;
+    long long cost = 0;
+    if (s < p.S_loc) {
+      const int64_t sg = p.step_begin + s;
+      const int64_t n = p.step_tok_off[sg + 1] - p.step_tok_off[sg];
+      const bool kept = p.keep[sg] != 0;
+      double c = 0.0;
+      if (kept) c = step_mode ? inv_norm / (double)n : inv_norm;
+      p.step_scale[s] = c;
+      cost = (long long)n * p.nch * (kept ? 2 : (p.zero_fill ? 1 : 0));
+      const double* st = p.step_stats + s * NSTAT;
+      v[1] = (double)n;          // n_tok
+      v[9] = st[6];              // sum_H (all tokens)
+      if (kept) {
+        v[0] = c * p.step_ell[s];  // loss partial
+        v[2] = (double)n;
+        v[3] = 1.0;
+        v[4] = st[1];  // clip
+        v[5] = st[2];  // trunc
+        v[6] = st[0];  // w
+        v[7] = st[3];  // adv
+        v[8] = st[4];  // adv^2
+        v[10] = st[5]; // kl
+      }
+    }
+    // --- inclusive block scan of cost
+    long long x = cost;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const long long y = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x += y;
+    }
+    if (lane == 31) wsum[warp] = x;
+    // --- fixed-order reduction of v
+#pragma unroll
+    for (int i = 0; i < NV; ++i) v[i] = warp_sum_d(v[i]);
+    if (lane == 0) {
+#pragma unroll
+      for (int i = 0; i < NV; ++i) red[warp][i] = v[i];
+    }
+    __syncthreads();
+    if (warp == 0) {
+      long long w = (lane < (int)(blockDim.x >> 5)) ? wsum[lane] : 0;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const long long y = __shfl_up_sync(0xffffffffu, w, o);
+        if (lane >= o) w += y;
+      }
+      wsum[lane] = w;  // inclusive prefix of warp totals
+    }
+    __syncthreads();
+    const long long before = s_carry + (warp > 0 ? wsum[warp - 1] : 0);
+    if (s < p.S_loc) p.step_cost[s + 1] = before + x;
+    if (tid == 0) {
+      const int nw = blockDim.x >> 5;
+      for (int w = 0; w < nw; ++w)
+#pragma unroll
+        for (int i = 0; i < NV; ++i) tot[i] += red[w][i];
+    }
+    __syncthreads();
+    if (tid == 0) s_carry += wsum[(blockDim.x >> 5) - 1];
+    __syncthreads();
+  }
+  if (tid == 0) {
+    dart_stats* o = reinterpret_cast<dart_stats*>(p.stats);
+    o->loss = tot[0];
+    o->n_tok = tot[1];
+    o->n_kept_tok = tot[2];
+    o->n_kept_step = tot[3];
+    o->sum_clip = tot[4];
+    o->sum_trunc = tot[5];
+    o->sum_w = tot[6];
+    o->sum_adv = tot[7];
+    o->sum_adv2 = tot[8];
+    o->sum_H = tot[9];
+    o->sum_kl = tot[10];
+  }
+}
+
+// ============================================================== K4a
+__global__ void gs_kernel(GsParams p) {
+  const int64_t nthreads = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < p.T_loc; t += nthreads) {
+    p.gs[t] = (float)(p.step_scale[p.tok_step[t]] * (double)p.dell[t] * p.invT);
+  }
+}
+
+// ============================================================== K4
+// Cursor over the warp's chunk range [x0, x1) in cost units.  A chunk of a
+// kept step costs 2 (read + write), of a masked step 1 (write) or 0 (skipped).
+struct BCur {
+  int64_t s;       // local step
+  int64_t t, tend; // local row, end row of the step
+  int64_t c;       // chunk within row
+  int64_t start;   // cost at the start of this chunk
+  int uc;          // unit cost of the step
+  bool kept, valid;
+};
+
+__device__ __forceinline__ void bcur_set_step(BCur& b, const BwdParams& p, int64_t s) {
+  // skip zero-cost steps
+  while (s < p.S_loc && p.step_cost[s + 1] == p.step_cost[s]) ++s;
+  b.s = s;
+  if (s >= p.S_loc) { b.valid = false; return; }
+  const int64_t sg = p.step_begin + s;
+  b.t = p.step_tok_off[sg] - p.tok_begin;
+  b.tend = p.step_tok_off[sg + 1] - p.tok_begin;
+  b.c = 0;
+  b.start = p.step_cost[s];
+  b.kept = p.keep[sg] != 0;
+  b.uc = b.kept ? 2 : 1;
+}
+
+__device__ __forceinline__ void bcur_seek(BCur& b, const BwdParams& p, int64_t x0, int64_t x1) {
+  const int64_t total = p.step_cost[p.S_loc];
+  b.valid = false;
+  if (x0 >= total || x0 >= x1) return;
+  const int64_t s = upper_bound_i64(p.step_cost, 0, p.S_loc + 1, x0) - 1;
+  b.valid = true;
+  bcur_set_step(b, p, s);
+  if (!b.valid) return;
+  const int64_t off = x0 - b.start;
+  const int64_t j = (off + b.uc - 1) / b.uc;  // first chunk starting at or after x0
+  const int64_t nj = (b.tend - b.t) * p.nch;
+  if (j >= nj) {
+    bcur_set_step(b, p, b.s + 1);
+  } else {
+    b.t += j / p.nch;
+    b.c = j % p.nch;
+    b.start += j * b.uc;
+  }
+  b.valid = b.valid && b.s < p.S_loc && b.start < x1;
+}
+
+__device__ __forceinline__ void bcur_next(BCur& b, const BwdParams& p, int64_t x1) {
+  b.start += b.uc;
+  if (++b.c == p.nch) {
+    b.c = 0;
+    if (++b.t == b.tend) bcur_set_step(b, p, b.s + 1);
+  }
+  b.valid = b.valid && b.s < p.S_loc && b.start < x1;
+}
+
+// advance to the next chunk of a kept step (skipping masked steps whole)
+__device__ __forceinline__ void bcur_to_kept(BCur& b, const BwdParams& p, int64_t x1) {
+  while (b.valid && !b.kept) {
+    bcur_set_step(b, p, b.s + 1);
+    b.valid = b.valid && b.s < p.S_loc && b.start < x1;
+  }
+}
+
+__device__ __forceinline__ void store_vals_bf16(uint8_t* dst, const float* v, int nvalid, int EPV) {
+  if (nvalid == 8 && EPV == 8) {
+    uint4 o;
+    o.x = pack_bf16x2(v[0], v[1]);
+    o.y = pack_bf16x2(v[2], v[3]);
+    o.z = pack_bf16x2(v[4], v[5]);
+    o.w = pack_bf16x2(v[6], v[7]);
+    stg128_cs(dst, o);
+  } else if (nvalid == 4 && EPV == 4) {
+    uint2 o;
+    o.x = pack_bf16x2(v[0], v[1]);
+    o.y = pack_bf16x2(v[2], v[3]);
+    *reinterpret_cast<uint2*>(dst) = o;
+  } else {
+    for (int e = 0; e < nvalid; ++e) reinterpret_cast<__nv_bfloat16*>(dst)[e] = __float2bfloat16_rn(v[e]);
+  }
+}
+
+__device__ __forceinline__ void store_vals_f32(uint8_t* dst, const float* v, int nvalid, int EPV) {
+  if (nvalid == EPV) {
+    for (int e = 0; e < EPV; e += 4)
+      stg128_cs(dst + 4 * e, make_uint4(__float_as_uint(v[e]), __float_as_uint(v[e + 1]), __float_as_uint(v[e + 2]),
+                                        __float_as_uint(v[e + 3])));
+  } else {
+    for (int e = 0; e < nvalid; ++e) reinterpret_cast<float*>(dst)[e] = v[e];
+  }
+}
+
+template <typename Tin, typename Tout, int WARPS, int STAGES>
+__global__ void __launch_bounds__(WARPS * 32)
+bwd_sweep_kernel(const BwdParams p) {
+  extern __shared__ __align__(128) uint8_t smem[];
+  constexpr int EPV = 16 / sizeof(Tin);       // logits per 16-byte input vector
+  constexpr bool OUT_BF16 = sizeof(Tout) == 2;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  uint8_t* ring = smem + (size_t)warp * STAGES * CH_BYTES;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + (size_t)WARPS * STAGES * CH_BYTES) + warp * STAGES;
+  if (lane == 0) {
+#pragma unroll
+    for (int s = 0; s < STAGES; ++s) mbar_init(&bars[s], 1);
+    fence_mbar_init();
+  }
+  __syncwarp();
+
+  const int64_t W = (int64_t)gridDim.x * WARPS;
+  const int64_t wid = (int64_t)blockIdx.x * WARPS + warp;
+  const int64_t total = p.step_cost[p.S_loc];
+  // total <= T_loc * nch * 2 (~1e8 at 2M rows) and W ~ 1e3-1e5: no int64 overflow
+  const int64_t x0 = (total * wid) / W;
+  const int64_t x1 = (total * (wid + 1)) / W;
+  const int tail_elems = (int)(p.V % EPV);
+  const float c2 = p.c2;
+  const uint64_t pol = policy_evict_first();
+
+  BCur cc;
+  bcur_seek(cc, p, x0, x1);
+  BCur pc = cc;
+  bcur_to_kept(pc, p, x1);
+#pragma unroll 1
+  for (int s = 0; s < STAGES; ++s) {
+    if (!pc.valid) break;
+    const int64_t v0 = pc.c * CH_VEC;
+    const int64_t nv = min((int64_t)CH_VEC, p.nvec - v0);
+    if (lane == 0) {
+      mbar_arrive_expect_tx(&bars[s], (uint32_t)nv * 16u);
+      bulk_g2s_hint(ring + (size_t)s * CH_BYTES, p.logits + pc.t * p.ld_bytes + v0 * 16, (uint32_t)nv * 16u,
+                    &bars[s], pol);
+    }
+    bcur_next(pc, p, x1);
+    bcur_to_kept(pc, p, x1);
+  }
+
+  int slot = 0;
+  uint32_t phase = 0;
+  int64_t cur_t = -1;
+  float g = 0.f, nl2 = 0.f, zy = 0.f;
+  int32_t y = -1;
+
+#pragma unroll 1
+  while (cc.valid) {
+    const int64_t t = cc.t;
+    const int64_t v0 = cc.c * CH_VEC;
+    const int nv = (int)min((int64_t)CH_VEC, p.nvec - v0);
+    uint8_t* orow = p.dlogits + t * p.ldg_bytes;
+    if (cc.kept) {
+      if (t != cur_t) {
+        cur_t = t;
+        g = p.gs[t];
+        nl2 = -p.lse2[t];
+        y = p.target[t];
+        if (y >= 0 && y < p.V) {
+          const uint8_t* rp = p.logits + t * p.ld_bytes;
+          zy = (sizeof(Tin) == 2) ? __uint_as_float(((uint32_t)(*reinterpret_cast<const uint16_t*>(rp + 2 * (int64_t)y))) << 16)
+                                  : *reinterpret_cast<const float*>(rp + 4 * (int64_t)y);
+        } else {
+          y = -1;
+        }
+      }
+      mbar_wait(&bars[slot], phase);
+      const uint8_t* sp = ring + (size_t)slot * CH_BYTES;
+      const float2 cc2 = make_float2(c2, c2), nl = make_float2(nl2, nl2), ng = make_float2(-g, -g);
+      uint4 x[VPL];
+#pragma unroll
+      for (int k = 0; k < VPL; ++k) {
+        const int vi = lane + 32 * k;
+        x[k] = (vi < nv) ? lds128(sp + vi * 16) : make_uint4(0u, 0u, 0u, 0u);
+      }
+      // consume every loaded word before the slot is handed back to the copy
+      // engine (forces the LDS results to have landed: WAR across proxies)
+      uint32_t dep = 0;
+#pragma unroll
+      for (int k = 0; k < VPL; ++k) dep |= x[k].x | x[k].y | x[k].z | x[k].w;
+      asm volatile("" ::"r"(dep));
+      __syncwarp();
+      // the slot's data is in registers: refill it now (overlaps the math below)
+      if (pc.valid) {
+        const int64_t pv0 = pc.c * CH_VEC;
+        const int64_t pnv = min((int64_t)CH_VEC, p.nvec - pv0);
+        if (lane == 0) {
+          fence_proxy_async_smem();
+          mbar_arrive_expect_tx(&bars[slot], (uint32_t)pnv * 16u);
+          bulk_g2s_hint(ring + (size_t)slot * CH_BYTES, p.logits + pc.t * p.ld_bytes + pv0 * 16,
+                        (uint32_t)pnv * 16u, &bars[slot], pol);
+        }
+        bcur_next(pc, p, x1);
+        bcur_to_kept(pc, p, x1);
+      }
+      if (++slot == STAGES) { slot = 0; phase ^= 1u; }
+#pragma unroll
+      for (int k = 0; k < VPL; ++k) {
+        const int vi = lane + 32 * k;
+        if (vi < nv) {
+          const int64_t gv = v0 + vi;
+          float o[EPV];
+          const uint32_t* w = reinterpret_cast<const uint32_t*>(&x[k]);
+          if (sizeof(Tin) == 2) {
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+              const float2 z = make_float2(bf16lo(w[j]), bf16hi(w[j]));
+              const float2 d = __ffma2_rn(z, cc2, nl);
+              const float2 pr = make_float2(ex2(d.x), ex2(d.y));
+              const float2 dz = __fmul2_rn(pr, ng);
+              o[2 * j] = dz.x;
+              o[2 * j + 1] = dz.y;
+            }
+          } else {
+#pragma unroll
+            for (int j = 0; j < 2; ++j) {
+              const float2 z = make_float2(__uint_as_float(w[2 * j]), __uint_as_float(w[2 * j + 1]));
+              const float2 d = __ffma2_rn(z, cc2, nl);
+              const float2 pr = make_float2(ex2(d.x), ex2(d.y));
+              const float2 dz = __fmul2_rn(pr, ng);
+              o[2 * j] = dz.x;
+              o[2 * j + 1] = dz.y;
+            }
+          }
+          const int nvalid = (tail_elems && gv == p.nvec - 1) ? tail_elems : EPV;
+          uint8_t* dst = orow + gv * EPV * (int64_t)sizeof(Tout);
+          if (OUT_BF16) store_vals_bf16(dst, o, nvalid, EPV);
+          else store_vals_f32(dst, o, nvalid, EPV);
+        }
+      }
+      // target element: dz_y = g (1 - p_y), written after the vector store (same thread)
+      if (y >= 0) {
+        const int64_t yv = y / EPV;
+        if (yv >= v0 && yv < v0 + nv && lane == (int)((yv - v0) & 31)) {
+          const float py = ex2(fmaf(zy, c2, nl2));
+          const float dzy = fmaf(-g, py, g);
+          if (OUT_BF16) reinterpret_cast<__nv_bfloat16*>(orow)[y] = __float2bfloat16_rn(dzy);
+          else reinterpret_cast<float*>(orow)[y] = dzy;
+        }
+      }
+    } else {
+      // masked step: zeros, no read
+#pragma unroll
+      for (int k = 0; k < VPL; ++k) {
+        const int vi = lane + 32 * k;
+        if (vi < nv) {
+          const int64_t gv = v0 + vi;
+          float o[EPV];
+#pragma unroll
+          for (int e = 0; e < EPV; ++e) o[e] = 0.f;
+          const int nvalid = (tail_elems && gv == p.nvec - 1) ? tail_elems : EPV;
+          uint8_t* dst = orow + gv * EPV * (int64_t)sizeof(Tout);
+          if (OUT_BF16) store_vals_bf16(dst, o, nvalid, EPV);
+          else store_vals_f32(dst, o, nvalid, EPV);
+        }
+      }
+    }
+    bcur_next(cc, p, x1);
+  }
+}
+
+// ============================================================== launchers
+cudaError_t launch_bwd_prep(const BwdPrepParams& p, cudaStream_t st) {
+  bwd_prep_kernel<<<1, 1024, 0, st>>>(p);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_gs(const GsParams& p, cudaStream_t st) {
+  if (p.T_loc <= 0) return cudaSuccess;
+  int64_t blocks = (p.T_loc + 255) / 256;
+  if (blocks > 8192) blocks = 8192;
+  gs_kernel<<<(unsigned)blocks, 256, 0, st>>>(p);
+  return cudaGetLastError();
+}
+
+template <typename Tin, typename Tout, int WARPS, int STAGES>
+static cudaError_t launch_bwd_t(const BwdParams& p, int num_sms, cudaStream_t st) {
+  const size_t smem = (size_t)WARPS * STAGES * CH_BYTES + (size_t)WARPS * STAGES * 8;
+  auto kern = bwd_sweep_kernel<Tin, Tout, WARPS, STAGES>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  int per_sm = 0;
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, WARPS * 32, smem);
+  if (e != cudaSuccess) return e;
+  if (per_sm < 1) per_sm = 1;
+  int64_t grid = (int64_t)num_sms * per_sm;
+  kern<<<(unsigned)grid, WARPS * 32, smem, st>>>(p);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_bwd_sweep(const BwdParams& p, bool in_bf16, bool out_bf16, int num_sms, cudaStream_t st) {
+  if (in_bf16 && out_bf16) return launch_bwd_t<__nv_bfloat16, __nv_bfloat16, BWD_WARPS, BWD_STAGES>(p, num_sms, st);
+  if (in_bf16) return launch_bwd_t<__nv_bfloat16, float, BWD_WARPS, BWD_STAGES>(p, num_sms, st);
+  if (out_bf16) return launch_bwd_t<float, __nv_bfloat16, BWD_WARPS, BWD_STAGES>(p, num_sms, st);
+  return launch_bwd_t<float, float, BWD_WARPS, BWD_STAGES>(p, num_sms, st);
+}
+
+}  // namespace dart

@@ -1,0 +1,157 @@
+// dart_internal.h -- kernel parameter blocks and launchers (internal, C++).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace dart {
+
+// Sweep configuration (compile-time; see DESIGN.md §6 for the sizing).
+#ifndef DART_FWD_WARPS
+#define DART_FWD_WARPS 8
+#endif
+#ifndef DART_FWD_STAGES
+#define DART_FWD_STAGES 3
+#endif
+#ifndef DART_BWD_WARPS
+#define DART_BWD_WARPS 8
+#endif
+#ifndef DART_BWD_STAGES
+#define DART_BWD_STAGES 3
+#endif
+constexpr int FWD_WARPS = DART_FWD_WARPS;
+constexpr int FWD_STAGES = DART_FWD_STAGES;
+constexpr int BWD_WARPS = DART_BWD_WARPS;
+constexpr int BWD_STAGES = DART_BWD_STAGES;
+
+struct AdvParams {
+  int64_t G, N_traj, S, T;
+  const int32_t* traj_group;
+  const float* traj_reward;
+  const int64_t* traj_step_off;
+  const int64_t* step_tok_off;
+  double adv_eps;
+  float* adv;
+  uint8_t* group_ok;
+  int64_t* grp_traj;  // [G+1]
+  uint32_t* status;
+};
+
+struct TokMetaParams {
+  int64_t S, N_traj, T_loc, tok_begin, step_begin, S_loc;
+  const int64_t* traj_step_off;
+  const int64_t* step_tok_off;
+  const float* adv;
+  float* tok_adv;
+  int32_t* tok_step;
+  uint32_t* status;
+};
+
+struct FwdParams {
+  const uint8_t* logits;
+  int64_t ld_bytes, V, T_loc, nvec;
+  float c2;  // inv_temperature * log2(e), fp32 (the value every logit is scaled by)
+  const int32_t* target;
+  const float* logp_old;
+  const float* logp_roll;
+  const float* logp_ref;
+  const float* tok_adv;
+  double eps_low, eps_high, is_cap, beta;
+  float *lse, *logp, *H, *ell, *dell, *lse2, *aux_w, *aux_kl;
+  uint8_t* aux_flags;
+  uint32_t* status;
+  int nsplit;
+  float* part_m;
+  double *part_s, *part_u;
+  uint32_t* row_cnt;
+};
+
+struct StepReduceParams {
+  int64_t T_loc, tok_begin, step_begin, S_loc;
+  const int64_t* step_tok_off;
+  const float *H, *ell, *aux_w, *aux_kl, *tok_adv;
+  const uint8_t* aux_flags;
+  float* step_entropy;
+  double* step_ell;
+  double* step_stats;
+};
+
+struct SelectParams {
+  int64_t G, N_traj, S, T;
+  const int64_t* traj_step_off;
+  const int64_t* step_tok_off;
+  const int64_t* grp_traj;
+  const uint8_t* group_ok;
+  const float* H;  // [S] global step entropies
+  float q;
+  int rule;
+  uint8_t* keep;
+  float* tau;
+  int64_t *grp_keep_step, *grp_keep_tok;
+};
+
+struct NormParams {
+  int64_t G, S, T;
+  int norm_mode;
+  const int64_t *grp_keep_step, *grp_keep_tok;
+  void* norm;  // dart_norm*
+};
+
+struct UnpackParams {
+  const float* gathered;
+  const int64_t* rank_step_off;
+  int world;
+  int64_t S_pad, S;
+  float* H;
+};
+
+struct BwdPrepParams {
+  int64_t T_loc, tok_begin, step_begin, S_loc, nch;  // nch = chunks per row
+  int norm_mode, zero_fill;
+  const int64_t* step_tok_off;
+  const uint8_t* keep;   // [S] global
+  const void* norm;      // dart_norm*
+  const double* step_ell;
+  const double* step_stats;
+  double* step_scale;    // [S_loc]
+  int64_t* step_cost;    // [S_loc+1]
+  void* stats;           // dart_stats*
+};
+
+struct GsParams {
+  int64_t T_loc;
+  const int32_t* tok_step;
+  const double* step_scale;
+  const float* dell;
+  double invT;
+  float* gs;
+};
+
+struct BwdParams {
+  const uint8_t* logits;
+  int64_t ld_bytes, V, T_loc, nvec, nch;
+  uint8_t* dlogits;
+  int64_t ldg_bytes;
+  float c2;
+  const int32_t* target;
+  const float* lse2;
+  const float* gs;
+  const int64_t* step_tok_off;  // global CSR
+  int64_t tok_begin, step_begin, S_loc;
+  const uint8_t* keep;          // [S] global
+  const int64_t* step_cost;     // [S_loc+1] prefix of chunk costs
+  int zero_fill;
+};
+
+cudaError_t launch_adv(const AdvParams& p, cudaStream_t st);
+cudaError_t launch_tok_meta(const TokMetaParams& p, cudaStream_t st);
+cudaError_t launch_fwd_sweep(const FwdParams& p, bool bf16, int num_sms, cudaStream_t st);
+cudaError_t launch_step_reduce(const StepReduceParams& p, cudaStream_t st);
+cudaError_t launch_unpack(const UnpackParams& p, cudaStream_t st);
+cudaError_t launch_select(const SelectParams& p, cudaStream_t st);
+cudaError_t launch_norm(const NormParams& p, cudaStream_t st);
+cudaError_t launch_bwd_prep(const BwdPrepParams& p, cudaStream_t st);
+cudaError_t launch_gs(const GsParams& p, cudaStream_t st);
+cudaError_t launch_bwd_sweep(const BwdParams& p, bool in_bf16, bool out_bf16, int num_sms, cudaStream_t st);
+
+}  // namespace dart

@@ -1,0 +1,378 @@
+"""Thin ctypes binding of libdart_loss.so (include/dart_loss.h).
+
+Argument marshalling only: every step of the DART loss pass runs in the CUDA
+library.  PyTorch supplies device memory, the stream and (for N > 1 ranks)
+the two collectives between the ABI calls:
+
+    dart_loss_fwd -> all_gather(step entropies) -> dart_select_steps
+                  -> dart_loss_bwd -> all_reduce(stats)
+
+There is no CPU fallback: importing this module without the built library, or
+calling it on tensors that are not on a CUDA device, raises.
+"""
+from __future__ import annotations
+
+import ctypes
+import dataclasses
+import os
+from typing import Optional
+
+import torch
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libdart_loss.so")
+
+# enums (include/dart_loss.h)
+DART_OK, DART_ERR_INVALID_ARG, DART_ERR_UNSUPPORTED, DART_ERR_CUDA, DART_ERR_WORKSPACE = range(5)
+DART_BF16, DART_F32 = 0, 1
+NORM_TOKEN_MEAN_KEPT, NORM_STEP_MEAN_KEPT, NORM_TOKEN_MEAN_ALL, NORM_STEP_MEAN_ALL, NORM_SUM = range(5)
+SEL_FLOOR, SEL_CEIL, SEL_LINEAR, SEL_OFF = range(4)
+STATUS_BITS = {
+    1 << 0: "NONFINITE_LOGIT", 1 << 1: "TARGET_RANGE", 1 << 2: "ROW_ALL_NEGINF",
+    1 << 3: "NONFINITE_LOGP", 1 << 4: "EMPTY", 1 << 5: "BAD_CSR", 1 << 6: "TARGET_NEGINF",
+}
+ABI_VERSION = 1
+
+
+class dart_cfg(ctypes.Structure):
+    _fields_ = [("eps_low", ctypes.c_float), ("eps_high", ctypes.c_float), ("is_cap", ctypes.c_float),
+                ("beta_kl", ctypes.c_float), ("entropy_q", ctypes.c_float),
+                ("inv_temperature", ctypes.c_float), ("adv_eps", ctypes.c_float),
+                ("norm_mode", ctypes.c_int32), ("select_rule", ctypes.c_int32),
+                ("zero_fill_masked", ctypes.c_int32)]
+
+
+class dart_meta(ctypes.Structure):
+    _fields_ = [("G", ctypes.c_int64), ("N_traj", ctypes.c_int64), ("S", ctypes.c_int64),
+                ("T", ctypes.c_int64), ("traj_group", ctypes.c_void_p), ("traj_reward", ctypes.c_void_p),
+                ("traj_step_off", ctypes.c_void_p), ("step_tok_off", ctypes.c_void_p)]
+
+
+class dart_batch(ctypes.Structure):
+    _fields_ = [("logits", ctypes.c_void_p), ("logits_dtype", ctypes.c_int32), ("T_loc", ctypes.c_int64),
+                ("V", ctypes.c_int64), ("ld", ctypes.c_int64), ("tok_begin", ctypes.c_int64),
+                ("step_begin", ctypes.c_int64), ("S_loc", ctypes.c_int64), ("target", ctypes.c_void_p),
+                ("logp_old", ctypes.c_void_p), ("logp_rollout", ctypes.c_void_p),
+                ("logp_ref", ctypes.c_void_p)]
+
+
+class dart_fwd_out(ctypes.Structure):
+    _fields_ = [("lse", ctypes.c_void_p), ("logp", ctypes.c_void_p), ("tok_entropy", ctypes.c_void_p),
+                ("ell", ctypes.c_void_p), ("dell", ctypes.c_void_p), ("step_entropy", ctypes.c_void_p),
+                ("step_ell", ctypes.c_void_p), ("adv", ctypes.c_void_p), ("group_ok", ctypes.c_void_p),
+                ("status", ctypes.c_void_p)]
+
+
+NORM_FIELDS = ["n_keep_tok", "n_keep_step", "n_tok", "n_step", "inv_norm"]  # 4 x i64 + f64
+STATS_FIELDS = ["loss", "n_tok", "n_kept_tok", "n_kept_step", "sum_clip", "sum_trunc", "sum_w",
+                "sum_adv", "sum_adv2", "sum_H", "sum_kl"]
+
+_lib = None
+
+EXPORTED = ["dart_workspace_size", "dart_loss_fwd", "dart_select_steps", "dart_loss_bwd", "dart_loss_pass",
+            "dart_status_str", "dart_abi_version", "dart_last_launch_count", "dart_set_timing_events"]
+
+
+class DartError(RuntimeError):
+    pass
+
+
+def lib():
+    """Load libdart_loss.so (fails loudly if it is missing: no fallback)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise DartError(f"{LIB_PATH} not built: run `python -c 'import __graft_entry__ as g; g.build()'` "
+                        "(there is no CPU fallback)")
+    L = ctypes.CDLL(LIB_PATH)
+    P = ctypes.POINTER
+    L.dart_workspace_size.restype = ctypes.c_size_t
+    L.dart_workspace_size.argtypes = [P(dart_batch), P(dart_meta), P(dart_cfg)]
+    L.dart_loss_fwd.restype = ctypes.c_int
+    L.dart_loss_fwd.argtypes = [P(dart_batch), P(dart_meta), P(dart_cfg), P(dart_fwd_out), ctypes.c_void_p,
+                                ctypes.c_size_t, ctypes.c_void_p]
+    L.dart_select_steps.restype = ctypes.c_int
+    L.dart_select_steps.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64,
+                                    P(dart_meta), P(dart_cfg), ctypes.c_void_p, ctypes.c_void_p,
+                                    ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_size_t,
+                                    ctypes.c_void_p]
+    L.dart_loss_bwd.restype = ctypes.c_int
+    L.dart_loss_bwd.argtypes = [P(dart_batch), P(dart_meta), P(dart_cfg), P(dart_fwd_out), ctypes.c_void_p,
+                                ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64,
+                                ctypes.c_void_p, ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p]
+    L.dart_loss_pass.restype = ctypes.c_int
+    L.dart_loss_pass.argtypes = [P(dart_batch), P(dart_meta), P(dart_cfg), P(dart_fwd_out), ctypes.c_void_p,
+                                 ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int32,
+                                 ctypes.c_int64, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_size_t,
+                                 ctypes.c_void_p]
+    L.dart_status_str.restype = ctypes.c_char_p
+    L.dart_status_str.argtypes = [ctypes.c_int]
+    L.dart_abi_version.restype = ctypes.c_int32
+    L.dart_last_launch_count.restype = ctypes.c_int32
+    L.dart_set_timing_events.restype = None
+    L.dart_set_timing_events.argtypes = [ctypes.c_void_p] * 4
+    if L.dart_abi_version() != ABI_VERSION:
+        raise DartError(f"libdart_loss ABI {L.dart_abi_version()} != binding {ABI_VERSION}")
+    _lib = L
+    return L
+
+
+def _check(rc):
+    if rc != DART_OK:
+        raise DartError(lib().dart_status_str(rc).decode())
+
+
+def _ptr(t: Optional[torch.Tensor]):
+    return None if t is None else ctypes.c_void_p(t.data_ptr())
+
+
+def _require_cuda(*ts):
+    for t in ts:
+        if t is not None and not t.is_cuda:
+            raise DartError("DART tensors must live on a CUDA device (no CPU fallback)")
+
+
+def set_timing_events(fwd_begin=None, fwd_end=None, bwd_begin=None, bwd_end=None):
+    """Have the library record torch.cuda.Event's around its two sweep kernels
+    (None disables).  The events must have been recorded once (created)."""
+    ev = [ctypes.c_void_p(e.cuda_event) if e is not None else None for e in (fwd_begin, fwd_end, bwd_begin, bwd_end)]
+    lib().dart_set_timing_events(*ev)
+
+
+# --------------------------------------------------------------------- config
+@dataclasses.dataclass
+class Config:
+    """Hyper-parameters; defaults are the paper's."""
+    eps_low: float = 0.2
+    eps_high: float = 0.28
+    is_cap: float = 1.0
+    beta_kl: float = 0.1
+    entropy_q: float = 0.2
+    inv_temperature: float = 1.0
+    adv_eps: float = 0.0
+    norm_mode: int = NORM_TOKEN_MEAN_KEPT
+    select_rule: int = SEL_FLOOR
+    zero_fill_masked: int = 1
+
+    def c(self):
+        return dart_cfg(self.eps_low, self.eps_high, self.is_cap, self.beta_kl, self.entropy_q,
+                        self.inv_temperature, self.adv_eps, self.norm_mode, self.select_rule,
+                        self.zero_fill_masked)
+
+    def as_f32(self):
+        """The values the library actually sees (float32-rounded), for the oracle."""
+        import numpy as np
+        d = dataclasses.asdict(self)
+        for k in ("eps_low", "eps_high", "is_cap", "beta_kl", "entropy_q", "inv_temperature", "adv_eps"):
+            d[k] = float(np.float32(d[k]))
+        return d
+
+
+# --------------------------------------------------------------------- metadata
+class Meta:
+    """Global batch metadata on the device (replicated on every rank)."""
+
+    def __init__(self, G, traj_group, traj_reward, traj_step_off, step_tok_off, device):
+        dev = torch.device(device)
+        self.G = int(G)
+        self.traj_group = torch.as_tensor(traj_group, dtype=torch.int32).to(dev)
+        self.traj_reward = torch.as_tensor(traj_reward, dtype=torch.float32).to(dev)
+        self.traj_step_off = torch.as_tensor(traj_step_off, dtype=torch.int64).to(dev)
+        self.step_tok_off = torch.as_tensor(step_tok_off, dtype=torch.int64).to(dev)
+        self.N_traj = int(self.traj_group.numel())
+        self.S = int(self.step_tok_off.numel()) - 1
+        self.T = int(step_tok_off[-1]) if len(step_tok_off) else 0
+        _require_cuda(self.traj_group)
+
+    @classmethod
+    def from_layout(cls, layout, device):
+        return cls(layout.G, layout.traj_group, layout.traj_reward, layout.traj_step_off,
+                   layout.step_tok_off, device)
+
+    def c(self):
+        return dart_meta(self.G, self.N_traj, self.S, self.T, _ptr(self.traj_group), _ptr(self.traj_reward),
+                         _ptr(self.traj_step_off), _ptr(self.step_tok_off))
+
+
+@dataclasses.dataclass
+class Shard:
+    """Local shard = whole trajectories [traj_begin, traj_end)."""
+    traj_begin: int
+    traj_end: int
+    step_begin: int
+    step_end: int
+    tok_begin: int
+    tok_end: int
+
+    @property
+    def T_loc(self):
+        return self.tok_end - self.tok_begin
+
+    @property
+    def S_loc(self):
+        return self.step_end - self.step_begin
+
+
+def whole_shard(layout):
+    return Shard(0, layout.N_traj, 0, layout.S, 0, layout.T)
+
+
+# --------------------------------------------------------------------- the pass
+class DartLoss:
+    """Buffers + the three ABI calls for one shard of a batch layout.
+
+    `run()` executes one pass on the current CUDA stream; with a process group
+    of size > 1 it issues the step-entropy all-gather between fwd and select
+    and the statistics all-reduce after bwd (NCCL over NVLink).
+    """
+
+    def __init__(self, layout, shard: Shard, V: int, cfg: Config, device, logits_dtype=torch.bfloat16,
+                 grad_dtype=torch.bfloat16, group=None, world_shards=None, ld: Optional[int] = None,
+                 ldg: Optional[int] = None):
+        self.L = lib()
+        dev = torch.device(device)
+        self.device = dev
+        self.layout = layout
+        self.shard = shard
+        self.V = int(V)
+        self.ld = int(ld) if ld is not None else self.V
+        self.ldg = int(ldg) if ldg is not None else self.V
+        self.cfg = cfg
+        self.group = group
+        self.meta = Meta.from_layout(layout, dev)
+        self.logits_dtype = logits_dtype
+        self.grad_dtype = grad_dtype
+        T, S_loc = shard.T_loc, shard.S_loc
+        f32 = dict(dtype=torch.float32, device=dev)
+        self.lse = torch.empty(T, **f32)
+        self.logp = torch.empty(T, **f32)
+        self.H = torch.empty(T, **f32)
+        self.ell = torch.empty(T, **f32)
+        self.dell = torch.empty(T, **f32)
+        self.step_H = torch.empty(max(S_loc, 1), **f32)
+        self.step_ell = torch.empty(max(S_loc, 1), dtype=torch.float64, device=dev)
+        self.adv = torch.empty(max(layout.N_traj, 1), **f32)
+        self.group_ok = torch.empty(max(layout.G, 1), dtype=torch.uint8, device=dev)
+        self.status = torch.zeros(1, dtype=torch.int32, device=dev)
+        self.keep = torch.empty(max(layout.S, 1), dtype=torch.uint8, device=dev)
+        self.tau = torch.empty(max(layout.G, 1), **f32)
+        self.norm = torch.empty(5, dtype=torch.int64, device=dev)          # dart_norm (40 B)
+        self.stats = torch.empty(len(STATS_FIELDS), dtype=torch.float64, device=dev)
+        self.dlogits_store = torch.empty((T, self.ldg), dtype=grad_dtype, device=dev)
+        self.dlogits = self.dlogits_store[:, :self.V]
+        # world layout for select (rank r owns global steps [rank_step_off[r], [r+1]))
+        if world_shards is None:
+            world_shards = [shard]
+        self.world = len(world_shards)
+        self.S_pad = max(max(s.S_loc for s in world_shards), 1)
+        if self.world == 1:
+            self.S_pad = layout.S
+        self.rank_step_off = torch.tensor([s.step_begin for s in world_shards] + [world_shards[-1].step_end],
+                                          dtype=torch.int64, device=dev)
+        self.gathered = torch.empty(self.world * self.S_pad, **f32) if self.world > 1 else None
+        self.step_H_pad = torch.zeros(self.S_pad, **f32) if self.world > 1 else None
+        b = self._batch(None, None, None, None, None)
+        self.ws_bytes = int(self.L.dart_workspace_size(ctypes.byref(b), ctypes.byref(self.meta.c()),
+                                                       ctypes.byref(cfg.c())))
+        self.ws = torch.empty(self.ws_bytes, dtype=torch.uint8, device=dev)
+        self.launches = 0
+
+    def _batch(self, logits, target, logp_old, logp_roll, logp_ref):
+        dt = DART_BF16 if self.logits_dtype == torch.bfloat16 else DART_F32
+        s = self.shard
+        return dart_batch(_ptr(logits), dt, s.T_loc, self.V, self.ld, s.tok_begin, s.step_begin, s.S_loc,
+                          _ptr(target), _ptr(logp_old), _ptr(logp_roll), _ptr(logp_ref))
+
+    def _fwd_out(self):
+        return dart_fwd_out(_ptr(self.lse), _ptr(self.logp), _ptr(self.H), _ptr(self.ell), _ptr(self.dell),
+                            _ptr(self.step_H), _ptr(self.step_ell), _ptr(self.adv), _ptr(self.group_ok),
+                            _ptr(self.status))
+
+    def _check_inputs(self, logits, target, logp_old, logp_roll, logp_ref):
+        _require_cuda(logits, target, logp_old, logp_roll, logp_ref)
+        if logits.dtype != self.logits_dtype:
+            raise DartError(f"logits dtype {logits.dtype} != {self.logits_dtype}")
+        if logits.dim() != 2 or logits.shape[0] != self.shard.T_loc or logits.shape[1] != self.V:
+            raise DartError(f"logits shape {tuple(logits.shape)} != ({self.shard.T_loc}, {self.V})")
+        if logits.stride(1) != 1 or logits.stride(0) != self.ld:
+            raise DartError(f"logits must be row-major with row pitch ld={self.ld}")
+        for name, t, dt in (("target", target, torch.int32), ("logp_old", logp_old, torch.float32),
+                            ("logp_rollout", logp_roll, torch.float32)):
+            if t.dtype != dt or not t.is_contiguous() or t.numel() != self.shard.T_loc:
+                raise DartError(f"{name} must be a contiguous {dt} [{self.shard.T_loc}] tensor")
+
+    def forward(self, logits, target, logp_old, logp_roll, logp_ref=None, stream=None):
+        self._check_inputs(logits, target, logp_old, logp_roll, logp_ref)
+        st = (stream or torch.cuda.current_stream(self.device)).cuda_stream
+        b = self._batch(logits, target, logp_old, logp_roll, logp_ref if self.cfg.beta_kl > 0 else None)
+        self._inputs = (b, logits, target, logp_old, logp_roll, logp_ref)
+        _check(self.L.dart_loss_fwd(ctypes.byref(b), ctypes.byref(self.meta.c()), ctypes.byref(self.cfg.c()),
+                                    ctypes.byref(self._fwd_out()), _ptr(self.ws), self.ws_bytes,
+                                    ctypes.c_void_p(st)))
+        self.launches += self.L.dart_last_launch_count()
+
+    def gather(self):
+        """C1: all-gather of the per-rank step entropies (padded to S_pad)."""
+        if self.world == 1:
+            return
+        import torch.distributed as dist
+        self.step_H_pad[:self.shard.S_loc].copy_(self.step_H[:self.shard.S_loc])
+        dist.all_gather_into_tensor(self.gathered, self.step_H_pad, group=self.group)
+
+    def set_gathered(self, gathered: torch.Tensor):
+        """Provide the all-gathered [world * S_pad] step entropies directly
+        (virtual ranks on one device emulate C1 by concatenation)."""
+        self.gathered.copy_(gathered)
+
+    def select(self, stream=None):
+        st = (stream or torch.cuda.current_stream(self.device)).cuda_stream
+        src = self.gathered if self.world > 1 else self.step_H
+        _check(self.L.dart_select_steps(_ptr(src), _ptr(self.rank_step_off), self.world, self.S_pad,
+                                        ctypes.byref(self.meta.c()), ctypes.byref(self.cfg.c()),
+                                        _ptr(self.group_ok), _ptr(self.keep), _ptr(self.tau), _ptr(self.norm),
+                                        _ptr(self.ws), self.ws_bytes, ctypes.c_void_p(st)))
+        self.launches += self.L.dart_last_launch_count()
+
+    def backward(self, stream=None):
+        st = (stream or torch.cuda.current_stream(self.device)).cuda_stream
+        b = self._inputs[0]
+        gdt = DART_BF16 if self.grad_dtype == torch.bfloat16 else DART_F32
+        _check(self.L.dart_loss_bwd(ctypes.byref(b), ctypes.byref(self.meta.c()), ctypes.byref(self.cfg.c()),
+                                    ctypes.byref(self._fwd_out()), _ptr(self.keep), _ptr(self.norm),
+                                    _ptr(self.dlogits_store), gdt, self.ldg, _ptr(self.stats), _ptr(self.ws),
+                                    self.ws_bytes, ctypes.c_void_p(st)))
+        self.launches += self.L.dart_last_launch_count()
+
+    def reduce_stats(self):
+        """C2: all-reduce(SUM) of the fp64 loss / statistics partials."""
+        if self.world == 1 or self.group is False:
+            return
+        import torch.distributed as dist
+        dist.all_reduce(self.stats, group=self.group)
+
+    def run(self, logits, target, logp_old, logp_roll, logp_ref=None):
+        """One whole pass (fwd -> C1 -> select -> bwd -> C2), stream-ordered."""
+        self.forward(logits, target, logp_old, logp_roll, logp_ref)
+        self.gather()
+        self.select()
+        self.backward()
+        self.reduce_stats()
+        return self.dlogits
+
+    # ----------------------------------------------------------- results
+    def check_status(self):
+        v = int(self.status.item())
+        if v:
+            names = [n for bit, n in STATUS_BITS.items() if v & bit]
+            raise DartError(f"DART device status 0x{v:x}: {', '.join(names)}")
+
+    def norm_dict(self):
+        n = self.norm.cpu()
+        d = {k: int(n[i]) for i, k in enumerate(NORM_FIELDS[:4])}
+        d["inv_norm"] = float(n[4:5].view(torch.float64)[0])
+        return d
+
+    def stats_dict(self):
+        s = self.stats.cpu().tolist()
+        return dict(zip(STATS_FIELDS, s))

@@ -77,8 +77,8 @@ class Batch:
                  logp_old=self.logp_old.cpu().numpy().astype(np.float64),
                  logp_rollout=self.logp_rollout.cpu().numpy().astype(np.float64),
                  logp_ref=self.logp_ref.cpu().numpy().astype(np.float64))
-        if logits:
-            d["logits"] = self.logits.float().cpu().numpy().astype(np.float64)
+        if logits:   # float32 holds bf16 exactly; the oracle widens each row to float64
+            d["logits"] = self.logits.float().cpu().numpy()
         return d
 
 

@@ -1,0 +1,210 @@
+"""GPU path vs the float64 oracle, through the C ABI (needs a B200)."""
+import numpy as np
+import pytest
+import torch
+
+from paper_2509_23866_b200 import dart, synth
+from tests.gpu_helpers import compare, run_gpu
+
+pytestmark = pytest.mark.gpu
+
+NORMS = [dart.NORM_TOKEN_MEAN_KEPT, dart.NORM_STEP_MEAN_KEPT, dart.NORM_TOKEN_MEAN_ALL,
+         dart.NORM_STEP_MEAN_ALL, dart.NORM_SUM]
+
+
+@pytest.mark.parametrize("name", ["tiny", "tiny_ragged"])
+@pytest.mark.parametrize("beta", [0.0, 0.1])
+def test_tiny_all_fields(name, beta):
+    b = synth.make_batch(name, seed=0)
+    cfg = dart.Config(is_cap=2.0, beta_kl=beta)
+    dl = run_gpu(b, cfg)
+    dl.check_status()
+    compare(dl, b, cfg)
+
+
+@pytest.mark.parametrize("seed", range(4))
+@pytest.mark.parametrize("norm", NORMS)
+def test_small_multi_group_norm_modes(seed, norm):
+    b = synth.make_batch("small_multi", seed=seed, real_reward=(seed % 2 == 1))
+    cfg = dart.Config(norm_mode=norm, entropy_q=0.3)
+    dl = run_gpu(b, cfg)
+    dl.check_status()
+    compare(dl, b, cfg)
+
+
+@pytest.mark.parametrize("rule", [dart.SEL_FLOOR, dart.SEL_CEIL, dart.SEL_LINEAR, dart.SEL_OFF])
+@pytest.mark.parametrize("q", [0.0, 0.2, 0.5, 0.9])
+def test_selection_rules(rule, q):
+    b = synth.make_batch("small_multi", seed=7)
+    cfg = dart.Config(select_rule=rule, entropy_q=q)
+    dl = run_gpu(b, cfg)
+    compare(dl, b, cfg)
+
+
+@pytest.mark.parametrize("invT,cap,adv_eps", [(1.0, 1.0, 0.0), (0.7, 1.5, 0.0), (1.3, 0.8, 1e-3)])
+def test_temperature_cap_adv_eps(invT, cap, adv_eps):
+    b = synth.make_batch("small_multi", seed=3, inv_temperature=invT)
+    cfg = dart.Config(inv_temperature=invT, is_cap=cap, adv_eps=adv_eps)
+    dl = run_gpu(b, cfg)
+    compare(dl, b, cfg)
+
+
+@pytest.mark.parametrize("dtype,V,ld", [(torch.float32, 1001, 1004), (torch.bfloat16, 1001, 1008),
+                                         (torch.bfloat16, 4099, 4104), (torch.float32, 3, 4),
+                                         (torch.bfloat16, 8, 8)])
+def test_odd_vocab_and_row_pitch(dtype, V, ld):
+    layout, _, _, _ = synth.config_layout("small_multi", seed=1)
+    b = synth.make_batch("small_multi", seed=1, layout=layout, V=V, dtype=dtype, pad_ld=ld)
+    cfg = dart.Config()
+    dl = run_gpu(b, cfg, grad_dtype=dtype)
+    dl.check_status()
+    compare(dl, b, cfg)
+
+
+@pytest.mark.parametrize("grad_dtype", [torch.bfloat16, torch.float32])
+def test_mid_vocab_152064(grad_dtype):
+    b = synth.make_batch("mid", seed=0)
+    cfg = dart.Config()
+    dl = run_gpu(b, cfg, grad_dtype=grad_dtype)
+    dl.check_status()
+    rng = np.random.default_rng(0)
+    rows = sorted(set(rng.choice(b.layout.T, 24, replace=False).tolist()) | {0, b.layout.T - 1})
+    compare(dl, b, cfg, rows=rows)
+
+
+def test_zero_fill_off_leaves_masked_rows():
+    b = synth.make_batch("small_multi", seed=2)
+    cfg = dart.Config(zero_fill_masked=0, entropy_q=0.5)
+    dev = torch.device("cuda")
+    dl = dart.DartLoss(b.layout, dart.whole_shard(b.layout), b.V, cfg, dev, logits_dtype=b.logits.dtype,
+                       grad_dtype=torch.float32)
+    dl.dlogits_store.fill_(7.0)
+    dl.run(b.logits.to(dev), b.target.to(dev), b.logp_old.to(dev), b.logp_rollout.to(dev), b.logp_ref.to(dev))
+    torch.cuda.synchronize()
+    keep = dl.keep.cpu().numpy()
+    tok_keep = np.repeat(keep, np.diff(b.layout.step_tok_off)).astype(bool)
+    dz = dl.dlogits.cpu().numpy()
+    assert np.all(dz[~tok_keep] == 7.0)
+    assert np.all(dz[tok_keep] != 7.0)
+
+
+def test_deterministic_bitwise():
+    b = synth.make_batch("mid", seed=1)
+    cfg = dart.Config()
+    d1 = run_gpu(b, cfg)
+    r1 = [x.clone() for x in (d1.lse, d1.H, d1.ell, d1.step_H, d1.dlogits, d1.stats)]
+    d2 = run_gpu(b, cfg, runs=2)
+    r2 = [d2.lse, d2.H, d2.ell, d2.step_H, d2.dlogits, d2.stats]
+    for a, c in zip(r1, r2):
+        assert torch.equal(a, c)
+
+
+def test_neg_inf_logits_and_one_hot_rows():
+    layout, _, _, _ = synth.config_layout("small_multi", seed=4)
+    b = synth.make_batch("small_multi", seed=4, layout=layout, V=1000, dtype=torch.bfloat16)
+    z = b.logits
+    z[3, 100:900] = float("-inf")                 # partial -inf row (slow path)
+    z[5, :] = float("-inf")
+    z[5, b.target[5]] = 2.0                       # one-hot row via -inf (P3)
+    z[7, ::3] = float("-inf")
+    cfg = dart.Config(entropy_q=0.0)
+    dl = run_gpu(b, cfg)
+    dl.check_status()
+    assert abs(float(dl.H[5])) <= 1e-6 and abs(float(dl.logp[5])) <= 1e-6
+    compare(dl, b, cfg)
+
+
+@pytest.mark.parametrize("what,bit", [("nan", 1 << 0), ("posinf", 1 << 0), ("target", 1 << 1),
+                                      ("allneginf", 1 << 2), ("logp", 1 << 3), ("target_neginf", 1 << 6)])
+def test_status_bits(what, bit):
+    b = synth.make_batch("tiny", seed=0)
+    if what == "nan":
+        b.logits[4, 17] = float("nan")
+    elif what == "posinf":
+        b.logits[4, 17] = float("inf")
+    elif what == "target":
+        b.target[9] = b.V + 3
+    elif what == "allneginf":
+        b.logits[11, :] = float("-inf")
+    elif what == "logp":
+        b.logp_old[2] = float("nan")
+    elif what == "target_neginf":
+        b.logits[6, b.target[6]] = float("-inf")
+    dl = run_gpu(b, dart.Config(is_cap=2.0))
+    v = int(dl.status.item())
+    assert v & bit, hex(v)
+    with pytest.raises(dart.DartError):
+        dl.check_status()
+
+
+def test_bad_metadata_status():
+    b = synth.make_batch("tiny", seed=0)
+    L = b.layout
+    L.step_tok_off = L.step_tok_off.copy()
+    L.step_tok_off[3] = L.step_tok_off[2]          # empty step
+    dl = run_gpu(b, dart.Config(is_cap=2.0))
+    assert int(dl.status.item()) & (1 << 4)
+
+
+def test_single_config_full_size_sampled():
+    """BASELINE.json single-GPU config at full size (T = 61440, V = 152064) in
+    the bench's launch configuration: sampled rows vs the oracle, properties
+    on everything else."""
+    b = synth.make_batch("single", seed=0, device="cuda")
+    cfg = dart.Config()
+    dl = run_gpu(b, cfg)
+    dl.check_status()
+    L = b.layout
+    rng = np.random.default_rng(1)
+    rows = sorted(rng.choice(L.T, 16, replace=False).tolist())
+    from oracle import dart_oracle as O
+    from tests.gpu_helpers import oracle_select_on, bf16_ulp, P_REL
+    cfgf = cfg.as_f32()
+    # selection decided identically from the same values; >= 80% kept per valid group
+    keep = dl.keep.cpu().numpy()
+    keep_same, _ = oracle_select_on(dl, b, cfgf)
+    assert np.array_equal(keep, keep_same)
+    ok = dl.group_ok.cpu().numpy()
+    for g in range(L.G):
+        steps = np.arange(L.traj_step_off[g * 8], L.traj_step_off[(g + 1) * 8])
+        if ok[g]:
+            assert keep[steps].sum() >= np.ceil(0.8 * len(steps))
+    # sampled rows: per-token values and gradient rows against the oracle
+    A, _ = O.advantages(L.traj_reward, L.traj_group, L.traj_step_off, L.G)
+    s_of_t = O.step_of_token(L.step_tok_off, L.T)
+    tr_of_s = O.traj_of_step(L.traj_step_off, L.S)
+    c_tok_step = None
+    nd = dl.norm_dict()
+    for t in rows:
+        z = b.logits[t].float().cpu().numpy()
+        y = int(b.target[t])
+        lse, logp, H, p = O.token_row(z, y)
+        assert abs(float(dl.lse[t]) - lse) <= 1e-5 * abs(lse) + 1e-6
+        assert abs(float(dl.H[t]) - H) <= 1e-5 * H + 1e-6
+        assert abs(float(dl.logp[t]) - logp) <= 1e-5
+        ell, dell, w, r, clipped, kl = O.token_loss(logp, float(b.logp_old[t]), float(b.logp_rollout[t]),
+                                                    float(b.logp_ref[t]), A[tr_of_s[s_of_t[t]]], cfgf)
+        assert abs(float(dl.ell[t]) - ell) <= 1e-5 * abs(ell) + 2e-6
+        kept = keep[s_of_t[t]]
+        g = (nd["inv_norm"] * dell) if kept else 0.0
+        dz = dl.dlogits[t].float().cpu().numpy()
+        if g == 0.0:
+            assert np.all(dz == 0)
+            continue
+        onehot = np.zeros_like(p)
+        onehot[y] = 1.0
+        dref = g * (onehot - p)
+        tol = bf16_ulp(dref) + abs(g) * P_REL * np.maximum(p, onehot) + abs(g) * 2.0 ** -125 + 1e-38
+        assert np.all(np.abs(dz - dref) <= tol), t
+    # masked rows all zero; every kept row sums to ~0 (softmax gradient)
+    tok_keep = np.repeat(keep, np.diff(L.step_tok_off)).astype(bool)
+    masked = np.nonzero(~tok_keep)[0][:64]
+    assert torch.all(dl.dlogits[torch.as_tensor(masked, device="cuda")] == 0)
+    sums = dl.dlogits[:4096].float().sum(dim=1).abs().cpu().numpy()
+    gs = np.abs(dl.dell[:4096].cpu().numpy()) * nd["inv_norm"]
+    assert np.all(sums <= gs * 0.01 + 1e-30)
+    # loss = sum over kept steps of c * step_ell (fp64, from the GPU's own per-token values)
+    st = dl.stats_dict()
+    ell_all = dl.ell.cpu().numpy().astype(np.float64)
+    L_chk = np.sum(ell_all[tok_keep]) * nd["inv_norm"]
+    assert abs(st["loss"] - L_chk) <= 1e-9 * np.sum(np.abs(ell_all[tok_keep])) * nd["inv_norm"] + 1e-15
