@@ -153,12 +153,14 @@ dart_status cuda_status(cudaError_t e) {
   return DART_OK;
 }
 
-int choose_nsplit(const dart_batch* b, const WsLayout& L, int64_t nvec) {
-  if (!L.split_alloc || nvec < KSEG) return 1;
+// log2 of the number of warps a row is split over: only for few rows, and
+// only when every canonical segment is non-empty (rows >= KSEG chunks)
+int choose_lg_nsplit(const dart_batch* b, const WsLayout& L, int64_t nvec) {
+  if (!L.split_alloc || nvec < (int64_t)KSEG * CH_VEC) return 0;
   const int64_t target_units = 4LL * sm_count() * 16;
-  int ns = 1;
-  while (ns < KSEG && b->T_loc * ns < target_units) ns *= 2;
-  return ns;
+  int lg = 0;
+  while ((1 << lg) < KSEG && (b->T_loc << lg) < target_units) ++lg;
+  return lg;
 }
 
 }  // namespace
@@ -257,12 +259,12 @@ dart_status dart_loss_fwd(const dart_batch* b, const dart_meta* m, const dart_cf
     fp.aux_kl = at<float>(ws, L.aux_kl);
     fp.aux_flags = at<uint8_t>(ws, L.aux_flags);
     fp.status = o->status;
-    fp.nsplit = choose_nsplit(b, L, nvec);
+    fp.lg_nsplit = choose_lg_nsplit(b, L, nvec);
     fp.part_m = L.split_alloc ? at<float>(ws, L.part_m) : nullptr;
     fp.part_s = L.split_alloc ? at<double>(ws, L.part_s) : nullptr;
     fp.part_u = L.split_alloc ? at<double>(ws, L.part_u) : nullptr;
     fp.row_cnt = L.split_alloc ? at<uint32_t>(ws, L.row_cnt) : nullptr;
-    if (fp.nsplit > 1) DART_TRY_RT(cudaMemsetAsync(fp.row_cnt, 0, (size_t)b->T_loc * 4, s));
+    if (fp.lg_nsplit > 0) DART_TRY_RT(cudaMemsetAsync(fp.row_cnt, 0, (size_t)b->T_loc * 4, s));
     rec(0, s);
     DART_TRY(launch_fwd_sweep(fp, b->logits_dtype == DART_BF16, sm_count(), s));
     rec(1, s);

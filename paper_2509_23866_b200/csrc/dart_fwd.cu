@@ -117,63 +117,64 @@ __global__ void tok_meta_kernel(TokMetaParams p) {
 }
 
 // ============================================================== K1 helpers
-struct Cur {
-  int64_t u;      // unit = row * nsplit + part
-  int32_t k;      // current canonical segment
-  int32_t kend;   // one past the unit's last segment
-  int64_t v;      // next vector (16 B) to take, row-relative
-  int64_t vend;   // end vector of segment k
-  bool valid;
-};
-
-__device__ __forceinline__ int64_t seg_begin(int64_t nvec, int k) { return (nvec * k) / KSEG; }
-
-__device__ __forceinline__ void cur_unit(Cur& c, int64_t u, int64_t units, int nsplit, int64_t nvec) {
-  c.valid = false;
-  if (u >= units) return;
-  const int part = (int)(u % nsplit);
-  int k = part * KSEG / nsplit;
-  const int kend = (part + 1) * KSEG / nsplit;
-  while (k < kend && seg_begin(nvec, k + 1) == seg_begin(nvec, k)) ++k;
-  c.u = u;
-  c.k = k;
-  c.kend = kend;
-  c.v = seg_begin(nvec, k);
-  c.vend = seg_begin(nvec, k + 1);
-  c.valid = (k < kend);
+// Canonical row decomposition: KSEG segments whose boundaries are multiples of
+// the chunk (CH_VEC vectors) -- only the row's last chunk can be partial.  The
+// per-row reduction order (lane <- vector mod 32, chunk-wise max update,
+// segment partials folded left to right) depends only on nvec, never on how
+// rows or segments are distributed over warps.
+__device__ __forceinline__ int64_t seg_begin(int64_t nvec, int k) {
+  if (k >= KSEG) return nvec;
+  return ((nvec * k) / KSEG) & ~(int64_t)(CH_VEC - 1);
 }
 
-// take the chunk at the cursor and advance; returns segment/unit-end flags
-struct ChunkInfo {
-  int64_t row, v0;
-  int32_t nv, k;
-  bool seg_end, unit_end;
-};
+// Work stream of one warp: units u = wid, wid+W, ...; unit = (row, part);
+// part p covers segments [p*KSEG/nsplit, (p+1)*KSEG/nsplit) (nsplit = 2^lg).
+struct Stream {
+  int64_t u, row, v, vend;
+  int32_t k, kend;
+  bool valid;
 
-__device__ __forceinline__ ChunkInfo cur_take(Cur& c, int64_t W, int64_t units, int nsplit, int64_t nvec) {
-  ChunkInfo ci;
-  ci.row = c.u / nsplit;
-  ci.v0 = c.v;
-  const int64_t rem = c.vend - c.v;
-  ci.nv = (int32_t)(rem < CH_VEC ? rem : CH_VEC);
-  ci.k = c.k;
-  c.v += ci.nv;
-  ci.seg_end = (c.v == c.vend);
-  ci.unit_end = false;
-  if (ci.seg_end) {
-    int k = c.k + 1;
-    while (k < c.kend && seg_begin(nvec, k + 1) == seg_begin(nvec, k)) ++k;
-    if (k >= c.kend) {
-      ci.unit_end = true;
-      cur_unit(c, c.u + W, units, nsplit, nvec);
-    } else {
-      c.k = k;
-      c.v = seg_begin(nvec, k);
-      c.vend = seg_begin(nvec, k + 1);
+  __device__ __forceinline__ void set_unit(int64_t uu, int64_t units, int lg, int64_t nvec) {
+    u = uu;
+    valid = uu < units;
+    if (!valid) return;
+    row = uu >> lg;
+    const int part = (int)(uu & ((1 << lg) - 1));
+    k = (part * KSEG) >> lg;
+    kend = ((part + 1) * KSEG) >> lg;
+    v = seg_begin(nvec, k);
+    vend = seg_begin(nvec, k + 1);
+    while (v == vend && k + 1 < kend) { ++k; vend = seg_begin(nvec, k + 1); }  // skip empty segments
+  }
+  // take the next chunk [v0, v0+nv) of this stream and advance
+  __device__ __forceinline__ void take(int64_t& row_o, int64_t& v0, int& nv, int& k_o, bool& seg_end,
+                                       bool& unit_end, int64_t W, int64_t units, int lg, int64_t nvec) {
+    row_o = row;
+    v0 = v;
+    const int64_t rem = vend - v;
+    nv = (int)(rem < CH_VEC ? rem : CH_VEC);
+    k_o = k;
+    v += nv;
+    seg_end = (v == vend);
+    unit_end = false;
+    if (seg_end) {
+      int kk = k + 1;
+      int64_t ve = vend;
+      while (kk < kend) {
+        ve = seg_begin(nvec, kk + 1);
+        if (ve > v) break;
+        ++kk;
+      }
+      if (kk >= kend) {
+        unit_end = true;
+        set_unit(u + W, units, lg, nvec);
+      } else {
+        k = kk;
+        vend = ve;
+      }
     }
   }
-  return ci;
-}
+};
 
 // per-lane online state (log2 domain)
 struct LaneAcc {
@@ -210,14 +211,12 @@ __device__ __forceinline__ void acc_pair(LaneAcc& a, int j, float2 z, float2 cc,
 // ------------------------------------------------------------ chunk bodies
 // bf16: one 16-byte vector = 8 logits = 4 bf16x2 words
 template <bool FULL>
-__device__ __forceinline__ void chunk_bf16(const uint8_t* slot, int nv, int lane, float c2, LaneAcc& a,
+__device__ __forceinline__ void chunk_bf16(uint4 (&x)[VPL], int nv, int lane, float c2, LaneAcc& a,
                                            uint32_t& bad, int tail_idx, uint32_t tail_keep_mask) {
-  uint4 x[VPL];
+  if (!FULL) {
 #pragma unroll
-  for (int k = 0; k < VPL; ++k) {
-    const int vi = lane + 32 * k;
-    if (FULL || vi < nv) x[k] = lds128(slot + vi * 16);
-    else x[k] = make_uint4(0xff80ff80u, 0xff80ff80u, 0xff80ff80u, 0xff80ff80u);
+    for (int k = 0; k < VPL; ++k)
+      if (lane + 32 * k >= nv) x[k] = make_uint4(0xff80ff80u, 0xff80ff80u, 0xff80ff80u, 0xff80ff80u);
   }
   if (tail_idx >= 0) {  // last vector of the row: logits >= V are not part of the row
 #pragma unroll
@@ -258,15 +257,15 @@ __device__ __forceinline__ void chunk_bf16(const uint8_t* slot, int nv, int lane
 
 // f32: one vector = 4 logits
 template <bool FULL>
-__device__ __forceinline__ void chunk_f32(const uint8_t* slot, int nv, int lane, float c2, LaneAcc& a,
+__device__ __forceinline__ void chunk_f32(const uint4 (&xr)[VPL], int nv, int lane, float c2, LaneAcc& a,
                                           uint32_t& bad, int tail_idx, uint32_t tail_keep_mask) {
   float4 x[VPL];
 #pragma unroll
   for (int k = 0; k < VPL; ++k) {
     const int vi = lane + 32 * k;
     if (FULL || vi < nv) {
-      uint4 r = lds128(slot + vi * 16);
-      x[k] = make_float4(__uint_as_float(r.x), __uint_as_float(r.y), __uint_as_float(r.z), __uint_as_float(r.w));
+      x[k] = make_float4(__uint_as_float(xr[k].x), __uint_as_float(xr[k].y), __uint_as_float(xr[k].z),
+                         __uint_as_float(xr[k].w));
     } else {
       x[k] = make_float4(-INFINITY, -INFINITY, -INFINITY, -INFINITY);
     }
@@ -413,8 +412,9 @@ fwd_sweep_kernel(const FwdParams p) {
 
   const int64_t W = (int64_t)gridDim.x * WARPS;
   const int64_t wid = (int64_t)blockIdx.x * WARPS + warp;
-  const int nsplit = p.nsplit;
-  const int64_t units = p.T_loc * nsplit;
+  const int lg = p.lg_nsplit;
+  const int nsplit = 1 << lg;
+  const int64_t units = p.T_loc << lg;
   const int64_t nvec = p.nvec;
   const float c2 = p.c2;
   const float m0 = NEG_CLAMP * c2;
@@ -423,18 +423,18 @@ fwd_sweep_kernel(const FwdParams p) {
   const uint32_t tail_keep = tail_elems ? ((1u << tail_elems) - 1u) : 0xffu;
   const uint64_t pol = policy_evict_first();
 
-  Cur pc, cc;
-  cur_unit(pc, wid, units, nsplit, nvec);
-  cc = pc;
+  Stream cs, ps;
+  cs.set_unit(wid, units, lg, nvec);
+  ps = cs;
   // prologue: fill the ring
 #pragma unroll 1
   for (int s = 0; s < STAGES; ++s) {
-    if (!pc.valid) break;
-    ChunkInfo ci = cur_take(pc, W, units, nsplit, nvec);
+    if (!ps.valid) break;
+    int64_t r, v0; int nv, k; bool se, ue;
+    ps.take(r, v0, nv, k, se, ue, W, units, lg, nvec);
     if (lane == 0) {
-      mbar_arrive_expect_tx(&bars[s], (uint32_t)ci.nv * 16u);
-      bulk_g2s_hint(ring + (size_t)s * CH_BYTES, p.logits + ci.row * p.ld_bytes + ci.v0 * 16,
-                    (uint32_t)ci.nv * 16u, &bars[s], pol);
+      mbar_arrive_expect_tx(&bars[s], (uint32_t)nv * 16u);
+      bulk_g2s_hint(ring + (size_t)s * CH_BYTES, p.logits + r * p.ld_bytes + v0 * 16, (uint32_t)nv * 16u, &bars[s], pol);
     }
   }
 
@@ -446,40 +446,55 @@ fwd_sweep_kernel(const FwdParams p) {
   uint32_t bad = 0;
 
 #pragma unroll 1
-  while (cc.valid) {
-    const ChunkInfo ci = cur_take(cc, W, units, nsplit, nvec);
+  while (cs.valid) {
+    int64_t row, v0; int nv, k; bool seg_end, unit_end;
+    cs.take(row, v0, nv, k, seg_end, unit_end, W, units, lg, nvec);
     mbar_wait(&bars[slot], phase);
     const uint8_t* sp = ring + (size_t)slot * CH_BYTES;
-    int tail_idx = -1;
-    if (tail_elems && ci.v0 + ci.nv == nvec) tail_idx = ci.nv - 1;
-    if (IS_BF16) {
-      if (ci.nv == CH_VEC) chunk_bf16<true>(sp, ci.nv, lane, c2, a, bad, tail_idx, tail_keep);
-      else chunk_bf16<false>(sp, ci.nv, lane, c2, a, bad, tail_idx, tail_keep);
-    } else {
-      if (ci.nv == CH_VEC) chunk_f32<true>(sp, ci.nv, lane, c2, a, bad, tail_idx, tail_keep);
-      else chunk_f32<false>(sp, ci.nv, lane, c2, a, bad, tail_idx, tail_keep);
+    // registers <- slot, then hand the slot straight back to the copy engine so
+    // STAGES chunks stay in flight while this one is being reduced
+    uint4 x[VPL];
+#pragma unroll
+    for (int kk = 0; kk < VPL; ++kk) {
+      const int vi = lane + 32 * kk;
+      x[kk] = (vi < nv) ? lds128(sp + vi * 16) : make_uint4(0u, 0u, 0u, 0u);
+    }
+    {
+      uint32_t dep = 0;
+#pragma unroll
+      for (int kk = 0; kk < VPL; ++kk) dep |= x[kk].x | x[kk].y | x[kk].z | x[kk].w;
+      asm volatile("" ::"r"(dep));
     }
     __syncwarp();
-    // refill this slot with the chunk STAGES ahead
-    if (pc.valid) {
-      ChunkInfo pi = cur_take(pc, W, units, nsplit, nvec);
+    if (ps.valid) {
+      int64_t r2, pv0; int pnv, pk; bool pse, pue;
+      ps.take(r2, pv0, pnv, pk, pse, pue, W, units, lg, nvec);
       if (lane == 0) {
         fence_proxy_async_smem();
-        mbar_arrive_expect_tx(&bars[slot], (uint32_t)pi.nv * 16u);
-        bulk_g2s_hint(ring + (size_t)slot * CH_BYTES, p.logits + pi.row * p.ld_bytes + pi.v0 * 16,
-                      (uint32_t)pi.nv * 16u, &bars[slot], pol);
+        mbar_arrive_expect_tx(&bars[slot], (uint32_t)pnv * 16u);
+        bulk_g2s_hint(ring + (size_t)slot * CH_BYTES, p.logits + r2 * p.ld_bytes + pv0 * 16, (uint32_t)pnv * 16u,
+                      &bars[slot], pol);
       }
     }
     if (++slot == STAGES) { slot = 0; phase ^= 1u; }
 
-    if (ci.seg_end) {
+    const int tail_idx = (tail_elems && v0 + nv == nvec) ? nv - 1 : -1;
+    if (IS_BF16) {
+      if (nv == CH_VEC && tail_idx < 0) chunk_bf16<true>(x, nv, lane, c2, a, bad, -1, tail_keep);
+      else chunk_bf16<false>(x, nv, lane, c2, a, bad, tail_idx, tail_keep);
+    } else {
+      if (nv == CH_VEC && tail_idx < 0) chunk_f32<true>(x, nv, lane, c2, a, bad, -1, tail_keep);
+      else chunk_f32<false>(x, nv, lane, c2, a, bad, tail_idx, tail_keep);
+    }
+
+    if (seg_end) {
       // --- canonical segment reduction: lanes -> one (M, S, U)
       const float sl = ((a.s[0].x + a.s[0].y) + (a.s[1].x + a.s[1].y)) + ((a.s[2].x + a.s[2].y) + (a.s[3].x + a.s[3].y));
       const float ul = ((a.u[0].x + a.u[0].y) + (a.u[1].x + a.u[1].y)) + ((a.u[2].x + a.u[2].y) + (a.u[3].x + a.u[3].y));
       const uint32_t wbad = warp_or(bad);
       Part seg;
       if (__any_sync(0xffffffffu, isnan(ul) || isnan(sl)) && !wbad) {
-        seg = segment_slow<Tin>(p, ci.row, ci.k, lane);      // -inf logits in the segment
+        seg = segment_slow<Tin>(p, row, k, lane);      // -inf logits in the segment
       } else {
         const float M = warp_max_f(a.m);
         const double dm = (double)a.m - (double)M;
@@ -492,37 +507,37 @@ fwd_sweep_kernel(const FwdParams p) {
       if (nsplit == 1) {
         rowp = part_fold(rowp, seg);
       } else if (lane == 0) {
-        const int64_t idx = ci.row * KSEG + ci.k;
+        const int64_t idx = row * KSEG + k;
         p.part_m[idx] = (float)seg.m;
         p.part_s[idx] = seg.s;
         p.part_u[idx] = seg.u;
       }
-      if (ci.unit_end) {
+      if (unit_end) {
         const uint32_t rbits = warp_or(bad);
         bad = 0;
         if (nsplit == 1) {
-          row_epilogue(p, ci.row, rowp, rbits, IS_BF16, lane);
+          row_epilogue(p, row, rowp, rbits, IS_BF16, lane);
           rowp = {-INFINITY, 0.0, 0.0};
         } else {
           // last-arriving warp of the row folds the KSEG partials in order
           __threadfence();
           uint32_t prev = 0;
-          if (lane == 0) prev = atomicAdd(&p.row_cnt[ci.row], 1u);
+          if (lane == 0) prev = atomicAdd(&p.row_cnt[row], 1u);
           prev = __shfl_sync(0xffffffffu, prev, 0);
           if (lane == 0) status_or(p.status, rbits);
           if (prev == (uint32_t)(nsplit - 1)) {
             __threadfence();
             Part R = {-INFINITY, 0.0, 0.0};
-            for (int k = 0; k < KSEG; ++k) {
-              if (seg_begin(nvec, k + 1) == seg_begin(nvec, k)) continue;
-              const int64_t idx = ci.row * KSEG + k;
+            for (int kk = 0; kk < KSEG; ++kk) {
+              if (seg_begin(nvec, kk + 1) == seg_begin(nvec, kk)) continue;
+              const int64_t idx = row * KSEG + kk;
               Part q;
               q.m = (double)__ldcg(&p.part_m[idx]);
               q.s = __ldcg(&p.part_s[idx]);
               q.u = __ldcg(&p.part_u[idx]);
               R = part_fold(R, q);
             }
-            row_epilogue(p, ci.row, R, 0u, IS_BF16, lane);
+            row_epilogue(p, row, R, 0u, IS_BF16, lane);
           }
         }
       }
@@ -584,7 +599,7 @@ static cudaError_t launch_fwd_sweep_t(const FwdParams& p, int num_sms, cudaStrea
   e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, WARPS * 32, smem);
   if (e != cudaSuccess) return e;
   if (per_sm < 1) per_sm = 1;
-  const int64_t units = p.T_loc * p.nsplit;
+  const int64_t units = p.T_loc << p.lg_nsplit;
   int64_t grid = (int64_t)num_sms * per_sm;
   const int64_t need = (units + WARPS - 1) / WARPS;
   if (grid > need) grid = need;

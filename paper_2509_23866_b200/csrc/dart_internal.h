@@ -17,7 +17,7 @@ namespace dart {
 #define DART_BWD_WARPS 8
 #endif
 #ifndef DART_BWD_STAGES
-#define DART_BWD_STAGES 3
+#define DART_BWD_STAGES 4
 #endif
 constexpr int FWD_WARPS = DART_FWD_WARPS;
 constexpr int FWD_STAGES = DART_FWD_STAGES;
@@ -60,7 +60,7 @@ struct FwdParams {
   float *lse, *logp, *H, *ell, *dell, *lse2, *aux_w, *aux_kl;
   uint8_t* aux_flags;
   uint32_t* status;
-  int nsplit;
+  int lg_nsplit;  // rows are split over 2^lg_nsplit warps (small T_loc)
   float* part_m;
   double *part_s, *part_u;
   uint32_t* row_cnt;

@@ -20,7 +20,7 @@ from typing import Optional
 import torch
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libdart_loss.so")
+LIB_PATH = os.environ.get("DART_LIB_PATH") or os.path.join(_HERE, "libdart_loss.so")   # override: tuning builds
 
 # enums (include/dart_loss.h)
 DART_OK, DART_ERR_INVALID_ARG, DART_ERR_UNSUPPORTED, DART_ERR_CUDA, DART_ERR_WORKSPACE = range(5)

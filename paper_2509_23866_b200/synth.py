@@ -67,6 +67,7 @@ class Batch:
     logp_rollout: torch.Tensor  # fp32 [T]
     logp_ref: torch.Tensor      # fp32 [T]
     name: str = ""
+    logits_store: Optional[torch.Tensor] = None   # [T, ld] storage of `logits` (padded rows)
 
     def oracle_dict(self, rows=None, logits=True):
         """numpy float64 view for the oracle (exact conversion from bf16/fp32)."""
@@ -225,4 +226,4 @@ def make_batch(name, seed=0, device="cpu", real_reward=False, chunk_rows=2048,
     logp_roll = torch.clamp(logp_old + torch.from_numpy(d_roll).to(dev), max=0.0)
     logp_ref = torch.clamp(logp + d_ref, max=0.0)
     return Batch(layout=layout, V=V, logits=logits, target=target, logp_old=logp_old,
-                 logp_rollout=logp_roll, logp_ref=logp_ref, name=name)
+                 logp_rollout=logp_roll, logp_ref=logp_ref, name=name, logits_store=logits_store)
