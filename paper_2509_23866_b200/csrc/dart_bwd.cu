@@ -290,10 +290,15 @@ bwd_sweep_kernel(const BwdParams p) {
       const uint8_t* sp = ring + (size_t)slot * CH_BYTES;
       const float2 cc2 = make_float2(c2, c2), nl = make_float2(nl2, nl2), ng = make_float2(-g, -g);
       uint4 x[VPL];
+      if (nv == CH_VEC) {
 #pragma unroll
-      for (int k = 0; k < VPL; ++k) {
-        const int vi = lane + 32 * k;
-        x[k] = (vi < nv) ? lds128(sp + vi * 16) : make_uint4(0u, 0u, 0u, 0u);
+        for (int k = 0; k < VPL; ++k) x[k] = lds128(sp + (lane + 32 * k) * 16);
+      } else {
+#pragma unroll
+        for (int k = 0; k < VPL; ++k) {
+          const int vi = lane + 32 * k;
+          x[k] = (vi < nv) ? lds128(sp + vi * 16) : make_uint4(0u, 0u, 0u, 0u);
+        }
       }
       // consume every loaded word before the slot is handed back to the copy
       // engine (forces the LDS results to have landed: WAR across proxies)
@@ -306,8 +311,7 @@ bwd_sweep_kernel(const BwdParams p) {
       if (pc.valid) {
         const int64_t pv0 = pc.c * CH_VEC;
         const int64_t pnv = min((int64_t)CH_VEC, p.nvec - pv0);
-        if (lane == 0) {
-          fence_proxy_async_smem();
+        if (lane == 0) {  // read-then-async-write: the reads completed (values consumed above)
           mbar_arrive_expect_tx(&bars[slot], (uint32_t)pnv * 16u);
           bulk_g2s_hint(ring + (size_t)slot * CH_BYTES, p.logits + pc.t * p.ld_bytes + pv0 * 16,
                         (uint32_t)pnv * 16u, &bars[slot], pol);

@@ -129,52 +129,54 @@ __device__ __forceinline__ int64_t seg_begin(int64_t nvec, int k) {
 
 // Work stream of one warp: units u = wid, wid+W, ...; unit = (row, part);
 // part p covers segments [p*KSEG/nsplit, (p+1)*KSEG/nsplit) (nsplit = 2^lg).
+// Row-relative vector indices are 32-bit (rows < 2^31 vectors); the common
+// step (next chunk in the same segment) is a few integer ops, transitions are
+// out of line.
 struct Stream {
-  int64_t u, row, v, vend;
-  int32_t k, kend;
+  int64_t u, row;
+  int32_t v, vend, k, kend;
   bool valid;
-
-  __device__ __forceinline__ void set_unit(int64_t uu, int64_t units, int lg, int64_t nvec) {
-    u = uu;
-    valid = uu < units;
-    if (!valid) return;
-    row = uu >> lg;
-    const int part = (int)(uu & ((1 << lg) - 1));
-    k = (part * KSEG) >> lg;
-    kend = ((part + 1) * KSEG) >> lg;
-    v = seg_begin(nvec, k);
-    vend = seg_begin(nvec, k + 1);
-    while (v == vend && k + 1 < kend) { ++k; vend = seg_begin(nvec, k + 1); }  // skip empty segments
-  }
-  // take the next chunk [v0, v0+nv) of this stream and advance
-  __device__ __forceinline__ void take(int64_t& row_o, int64_t& v0, int& nv, int& k_o, bool& seg_end,
-                                       bool& unit_end, int64_t W, int64_t units, int lg, int64_t nvec) {
-    row_o = row;
-    v0 = v;
-    const int64_t rem = vend - v;
-    nv = (int)(rem < CH_VEC ? rem : CH_VEC);
-    k_o = k;
-    v += nv;
-    seg_end = (v == vend);
-    unit_end = false;
-    if (seg_end) {
-      int kk = k + 1;
-      int64_t ve = vend;
-      while (kk < kend) {
-        ve = seg_begin(nvec, kk + 1);
-        if (ve > v) break;
-        ++kk;
-      }
-      if (kk >= kend) {
-        unit_end = true;
-        set_unit(u + W, units, lg, nvec);
-      } else {
-        k = kk;
-        vend = ve;
-      }
-    }
-  }
 };
+
+__device__ __forceinline__ void stream_set_unit(Stream& s, int64_t uu, int64_t units, int lg, int64_t nvec) {
+  s.u = uu;
+  s.valid = uu < units;
+  if (!s.valid) return;
+  s.row = uu >> lg;
+  const int part = (int)(uu & ((1 << lg) - 1));
+  int k = (part * KSEG) >> lg;
+  s.kend = ((part + 1) * KSEG) >> lg;
+  s.v = (int32_t)seg_begin(nvec, k);
+  int32_t ve = (int32_t)seg_begin(nvec, k + 1);
+  while (s.v == ve && k + 1 < s.kend) { ++k; ve = (int32_t)seg_begin(nvec, k + 1); }  // skip empty segments
+  s.k = k;
+  s.vend = ve;
+}
+
+// called when the chunk just taken ended segment s.k: move to the next
+// non-empty segment of the unit or to the next unit; returns unit_end
+__device__ __forceinline__ bool stream_next_segment(Stream& s, int64_t W, int64_t units, int lg, int64_t nvec) {
+  int kk = s.k + 1;
+  int32_t ve = s.vend;
+  while (kk < s.kend) {
+    ve = (int32_t)seg_begin(nvec, kk + 1);
+    if (ve > s.v) break;
+    ++kk;
+  }
+  if (kk >= s.kend) {
+    stream_set_unit(s, s.u + W, units, lg, nvec);
+    return true;
+  }
+  s.k = kk;
+  s.vend = ve;
+  return false;
+}
+
+// Lazy running max (log2 units): a lane rescales only when a chunk's max
+// exceeds its reference by more than LAZY_M.  The shift then sits up to LAZY_M
+// below the true max, so u = sum e (x-m) mixes signs; the extra fp32 error in
+// H is ~LAZY_M * eps relative -- 2 keeps it far below the 1e-5 bar (64 did not).
+constexpr float LAZY_M = 2.0f;
 
 // per-lane online state (log2 domain)
 struct LaneAcc {
@@ -241,8 +243,9 @@ __device__ __forceinline__ void chunk_bf16(uint4 (&x)[VPL], int nv, int lane, fl
   }
   const float cmr = fmax_nan(bf16lo(mx), bf16hi(mx));
   if (!(cmr < INFINITY)) bad |= DART_STATUS_NONFINITE_LOGIT;      // NaN or +inf
-  const float cm = fmaxf(cmr * c2, a.m);
-  if (__any_sync(0xffffffffu, cm > a.m)) acc_rescale(a, cm);
+  // lazy running max (see LAZY_M)
+  const float cm = cmr * c2;
+  if (__any_sync(0xffffffffu, cm > a.m + LAZY_M)) acc_rescale(a, (cm > a.m + LAZY_M) ? cm : a.m);
   const float2 cc = make_float2(c2, c2), nm = make_float2(-a.m, -a.m);
 #pragma unroll
   for (int k = 0; k < VPL; ++k) {
@@ -290,8 +293,9 @@ __device__ __forceinline__ void chunk_f32(const uint4 (&xr)[VPL], int nv, int la
     cmr = fmax_nan(cmr, x[k].w);
   }
   if (!(cmr < INFINITY)) bad |= DART_STATUS_NONFINITE_LOGIT;
-  const float cm = fmaxf(cmr * c2, a.m);
-  if (__any_sync(0xffffffffu, cm > a.m)) acc_rescale(a, cm);
+  // lazy running max (see LAZY_M)
+  const float cm = cmr * c2;
+  if (__any_sync(0xffffffffu, cm > a.m + LAZY_M)) acc_rescale(a, (cm > a.m + LAZY_M) ? cm : a.m);
   const float2 cc = make_float2(c2, c2), nm = make_float2(-a.m, -a.m);
 #pragma unroll
   for (int k = 0; k < VPL; ++k) {
@@ -392,6 +396,36 @@ __device__ void row_epilogue(const FwdParams& p, int64_t row, Part R, uint32_t b
   }
 }
 
+// Issue the bulk copy of the producer stream's next chunk into `slot` and advance it.
+__device__ __forceinline__ void issue_next(Stream& ps, uint64_t* bars, uint8_t* ring, int slot, const FwdParams& p,
+                                           int64_t W, int64_t units, int lg, int64_t nvec, int lane, uint64_t pol) {
+  const int nv = min(CH_VEC, ps.vend - ps.v);
+  if (lane == 0) {
+    mbar_arrive_expect_tx(&bars[slot], (uint32_t)nv * 16u);
+    bulk_g2s_hint(ring + (size_t)slot * CH_BYTES, p.logits + ps.row * p.ld_bytes + (int64_t)ps.v * 16,
+                  (uint32_t)nv * 16u, &bars[slot], pol);
+  }
+  ps.v += nv;
+  if (ps.v == ps.vend) stream_next_segment(ps, W, units, lg, nvec);
+}
+
+// Hand the slot back to the copy engine once every lane holds its vectors in
+// registers (the OR consumes each loaded word, so the LDS results have landed
+// before the async-proxy write is issued), and refill it STAGES chunks ahead.
+template <int STAGES>
+__device__ __forceinline__ void release_refill(const uint4 (&x)[VPL], uint64_t* bars, uint8_t* ring, int slot,
+                                               Stream& ps, const FwdParams& p, int64_t W, int64_t units, int lg,
+                                               int64_t nvec, int lane, uint64_t pol) {
+  uint32_t dep = 0;
+#pragma unroll
+  for (int kk = 0; kk < VPL; ++kk) dep |= x[kk].x | x[kk].y | x[kk].z | x[kk].w;
+  asm volatile("" ::"r"(dep));
+  __syncwarp();
+  // (no fence.proxy.async needed: this is a read-then-async-write hazard and
+  // every read has completed -- its value is in a register -- before the issue)
+  if (ps.valid) issue_next(ps, bars, ring, slot, p, W, units, lg, nvec, lane, pol);
+}
+
 // ============================================================== K1
 template <typename Tin, int WARPS, int STAGES>
 __global__ void __launch_bounds__(WARPS * 32)
@@ -424,18 +458,13 @@ fwd_sweep_kernel(const FwdParams p) {
   const uint64_t pol = policy_evict_first();
 
   Stream cs, ps;
-  cs.set_unit(wid, units, lg, nvec);
+  stream_set_unit(cs, wid, units, lg, nvec);
   ps = cs;
   // prologue: fill the ring
 #pragma unroll 1
   for (int s = 0; s < STAGES; ++s) {
     if (!ps.valid) break;
-    int64_t r, v0; int nv, k; bool se, ue;
-    ps.take(r, v0, nv, k, se, ue, W, units, lg, nvec);
-    if (lane == 0) {
-      mbar_arrive_expect_tx(&bars[s], (uint32_t)nv * 16u);
-      bulk_g2s_hint(ring + (size_t)s * CH_BYTES, p.logits + r * p.ld_bytes + v0 * 16, (uint32_t)nv * 16u, &bars[s], pol);
-    }
+    issue_next(ps, bars, ring, s, p, W, units, lg, nvec, lane, pol);
   }
 
   int slot = 0;
@@ -447,45 +476,36 @@ fwd_sweep_kernel(const FwdParams p) {
 
 #pragma unroll 1
   while (cs.valid) {
-    int64_t row, v0; int nv, k; bool seg_end, unit_end;
-    cs.take(row, v0, nv, k, seg_end, unit_end, W, units, lg, nvec);
+    const int64_t row = cs.row;
+    const int32_t v0 = cs.v;
+    const int nv = min(CH_VEC, cs.vend - cs.v);
+    const int k = cs.k;
+    cs.v += nv;
+    const bool seg_end = (cs.v == cs.vend);
+    bool unit_end = false;
+    if (seg_end) unit_end = stream_next_segment(cs, W, units, lg, nvec);
     mbar_wait(&bars[slot], phase);
     const uint8_t* sp = ring + (size_t)slot * CH_BYTES;
-    // registers <- slot, then hand the slot straight back to the copy engine so
-    // STAGES chunks stay in flight while this one is being reduced
-    uint4 x[VPL];
+    const int tail_idx = (tail_elems && (int64_t)v0 + nv == nvec) ? nv - 1 : -1;
+    if (nv == CH_VEC && tail_idx < 0) {
+      uint4 x[VPL];
 #pragma unroll
-    for (int kk = 0; kk < VPL; ++kk) {
-      const int vi = lane + 32 * kk;
-      x[kk] = (vi < nv) ? lds128(sp + vi * 16) : make_uint4(0u, 0u, 0u, 0u);
-    }
-    {
-      uint32_t dep = 0;
-#pragma unroll
-      for (int kk = 0; kk < VPL; ++kk) dep |= x[kk].x | x[kk].y | x[kk].z | x[kk].w;
-      asm volatile("" ::"r"(dep));
-    }
-    __syncwarp();
-    if (ps.valid) {
-      int64_t r2, pv0; int pnv, pk; bool pse, pue;
-      ps.take(r2, pv0, pnv, pk, pse, pue, W, units, lg, nvec);
-      if (lane == 0) {
-        fence_proxy_async_smem();
-        mbar_arrive_expect_tx(&bars[slot], (uint32_t)pnv * 16u);
-        bulk_g2s_hint(ring + (size_t)slot * CH_BYTES, p.logits + r2 * p.ld_bytes + pv0 * 16, (uint32_t)pnv * 16u,
-                      &bars[slot], pol);
-      }
-    }
-    if (++slot == STAGES) { slot = 0; phase ^= 1u; }
-
-    const int tail_idx = (tail_elems && v0 + nv == nvec) ? nv - 1 : -1;
-    if (IS_BF16) {
-      if (nv == CH_VEC && tail_idx < 0) chunk_bf16<true>(x, nv, lane, c2, a, bad, -1, tail_keep);
-      else chunk_bf16<false>(x, nv, lane, c2, a, bad, tail_idx, tail_keep);
+      for (int kk = 0; kk < VPL; ++kk) x[kk] = lds128(sp + (lane + 32 * kk) * 16);
+      release_refill<STAGES>(x, bars, ring, slot, ps, p, W, units, lg, nvec, lane, pol);
+      if (IS_BF16) chunk_bf16<true>(x, nv, lane, c2, a, bad, -1, tail_keep);
+      else chunk_f32<true>(x, nv, lane, c2, a, bad, -1, tail_keep);
     } else {
-      if (nv == CH_VEC && tail_idx < 0) chunk_f32<true>(x, nv, lane, c2, a, bad, -1, tail_keep);
+      uint4 x[VPL];
+#pragma unroll
+      for (int kk = 0; kk < VPL; ++kk) {
+        const int vi = lane + 32 * kk;
+        x[kk] = (vi < nv) ? lds128(sp + vi * 16) : make_uint4(0u, 0u, 0u, 0u);
+      }
+      release_refill<STAGES>(x, bars, ring, slot, ps, p, W, units, lg, nvec, lane, pol);
+      if (IS_BF16) chunk_bf16<false>(x, nv, lane, c2, a, bad, tail_idx, tail_keep);
       else chunk_f32<false>(x, nv, lane, c2, a, bad, tail_idx, tail_keep);
     }
+    if (++slot == STAGES) { slot = 0; phase ^= 1u; }
 
     if (seg_end) {
       // --- canonical segment reduction: lanes -> one (M, S, U)
