@@ -72,10 +72,11 @@ WsLayout ws_layout(const dart_batch* b, const dart_meta* m) {
   L.aux_w = take(T * 4);
   L.aux_kl = take(T * 4);
   L.aux_flags = take(T);
-  L.gs = take(T * 4);
+  L.rec = take(T * 16);
   L.step_stats = take(S_loc * NSTAT * 8);
   L.step_cost = take((S_loc + 1) * 8);
   L.step_scale = take(S_loc * 8);
+  L.step_chunk = take((S_loc + 1) * 8);
   L.split_alloc = T > 0 && T <= (size_t)SPLIT_MAX_ROWS;
   if (L.split_alloc) {
     L.part_m = take(T * KSEG * 4);
@@ -353,14 +354,19 @@ dart_status dart_loss_bwd(const dart_batch* b, const dart_meta* m, const dart_cf
   pp.step_ell = f->step_ell; pp.step_stats = at<double>(ws, L.step_stats);
   pp.step_scale = at<double>(ws, L.step_scale);
   pp.step_cost = at<int64_t>(ws, L.step_cost);
+  pp.step_chunk = at<int64_t>(ws, L.step_chunk);
   pp.stats = stats;
   DART_TRY(launch_bwd_prep(pp, s));
 
   if (b->T_loc > 0) {
-    GsParams gp;
-    gp.T_loc = b->T_loc; gp.tok_step = at<int32_t>(ws, L.tok_step); gp.step_scale = pp.step_scale;
-    gp.dell = f->dell; gp.invT = (double)c->inv_temperature; gp.gs = at<float>(ws, L.gs);
-    DART_TRY(launch_gs(gp, s));
+    RowRecParams rp;
+    rp.T_loc = b->T_loc; rp.V = b->V; rp.ld_bytes = b->ld * (int64_t)es;
+    rp.is_bf16 = b->logits_dtype == DART_BF16;
+    rp.logits = static_cast<const uint8_t*>(b->logits);
+    rp.tok_step = at<int32_t>(ws, L.tok_step); rp.target = b->target; rp.step_scale = pp.step_scale;
+    rp.dell = f->dell; rp.lse2 = at<float>(ws, L.lse2); rp.invT = (double)c->inv_temperature;
+    rp.rec = at<int4>(ws, L.rec);
+    DART_TRY(launch_rowrec(rp, s));
 
     BwdParams bp;
     bp.logits = static_cast<const uint8_t*>(b->logits);
@@ -369,13 +375,12 @@ dart_status dart_loss_bwd(const dart_batch* b, const dart_meta* m, const dart_cf
     bp.dlogits = static_cast<uint8_t*>(dlogits);
     bp.ldg_bytes = ldg * (int64_t)esize(grad_dtype);
     bp.c2 = (float)((double)c->inv_temperature * LOG2E_D);
-    bp.target = b->target;
-    bp.lse2 = at<float>(ws, L.lse2);
-    bp.gs = gp.gs;
+    bp.rec = rp.rec;
     bp.step_tok_off = m->step_tok_off;
     bp.tok_begin = b->tok_begin; bp.step_begin = b->step_begin; bp.S_loc = b->S_loc;
     bp.keep = keep;
     bp.step_cost = pp.step_cost;
+    bp.step_chunk = pp.step_chunk;
     bp.zero_fill = pp.zero_fill;
     rec(2, s);
     DART_TRY(launch_bwd_sweep(bp, b->logits_dtype == DART_BF16, grad_dtype == DART_BF16, sm_count(), s));

@@ -5,7 +5,7 @@
 //                        Q11), the local loss partial sum_{kept s} c_s sum ell
 //                        and statistics (fp64), and the prefix of per-step
 //                        chunk costs that balances the sweep across warps.
-//   K4a gs_kernel        per local row: g_t = c_s * dell_t * inv_temperature.
+//   K4a rowrec_kernel    per local row: {g_t = c_s dell_t invT, -lse2_t, y_t, z_{t,y}}.
 //   K4  bwd_sweep        THE SECOND HOT LOOP: for rows of kept steps, re-read
 //                        the logits (bulk copies into a per-warp ring) and
 //                        write dL/dz_v = g_t (delta_{v,y} - p_v) rounded to
@@ -31,14 +31,16 @@ __global__ void __launch_bounds__(1024) bwd_prep_kernel(BwdPrepParams p) {
   double tot[NV];
 #pragma unroll
   for (int i = 0; i < NV; ++i) tot[i] = 0.0;  // meaningful in thread 0 only
-  if (tid == 0) { s_carry = 0; p.step_cost[0] = 0; }
+  __shared__ long long wsum2[32];
+  __shared__ long long s_carry2;
+  if (tid == 0) { s_carry = 0; p.step_cost[0] = 0; s_carry2 = 0; p.step_chunk[0] = 0; }
   __syncthreads();
   for (int64_t base = 0; base < p.S_loc; base += blockDim.x) {
     const int64_t s = base + tid;
     double v[NV];
 #pragma unroll
     for (int i = 0; i < NV; ++i) v[i] = 0.0;
-    long long cost = 0;
+    long long cost = 0, nchunks = 0;
     if (s < p.S_loc) {
       const int64_t sg = p.step_begin + s;
       const int64_t n = p.step_tok_off[sg + 1] - p.step_tok_off[sg];
@@ -47,6 +49,7 @@ __global__ void __launch_bounds__(1024) bwd_prep_kernel(BwdPrepParams p) {
       if (kept) c = step_mode ? inv_norm / (double)n : inv_norm;
       p.step_scale[s] = c;
       cost = (long long)n * p.nch * (kept ? 2 : (p.zero_fill ? 1 : 0));
+      nchunks = (kept || p.zero_fill) ? (long long)n * p.nch : 0;
       const double* st = p.step_stats + s * NSTAT;
       v[1] = (double)n;          // n_tok
       v[9] = st[6];              // sum_H (all tokens)
@@ -63,13 +66,14 @@ __global__ void __launch_bounds__(1024) bwd_prep_kernel(BwdPrepParams p) {
       }
     }
     // --- inclusive block scan of cost
-    long long x = cost;
+    long long x = cost, x2 = nchunks;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
       const long long y = __shfl_up_sync(0xffffffffu, x, o);
-      if (lane >= o) x += y;
+      const long long y2 = __shfl_up_sync(0xffffffffu, x2, o);
+      if (lane >= o) { x += y; x2 += y2; }
     }
-    if (lane == 31) wsum[warp] = x;
+    if (lane == 31) { wsum[warp] = x; wsum2[warp] = x2; }
     // --- fixed-order reduction of v
 #pragma unroll
     for (int i = 0; i < NV; ++i) v[i] = warp_sum_d(v[i]);
@@ -80,16 +84,23 @@ __global__ void __launch_bounds__(1024) bwd_prep_kernel(BwdPrepParams p) {
     __syncthreads();
     if (warp == 0) {
       long long w = (lane < (int)(blockDim.x >> 5)) ? wsum[lane] : 0;
+      long long w2 = (lane < (int)(blockDim.x >> 5)) ? wsum2[lane] : 0;
 #pragma unroll
       for (int o = 1; o < 32; o <<= 1) {
         const long long y = __shfl_up_sync(0xffffffffu, w, o);
-        if (lane >= o) w += y;
+        const long long y2 = __shfl_up_sync(0xffffffffu, w2, o);
+        if (lane >= o) { w += y; w2 += y2; }
       }
       wsum[lane] = w;  // inclusive prefix of warp totals
+      wsum2[lane] = w2;
     }
     __syncthreads();
     const long long before = s_carry + (warp > 0 ? wsum[warp - 1] : 0);
-    if (s < p.S_loc) p.step_cost[s + 1] = before + x;
+    const long long before2 = s_carry2 + (warp > 0 ? wsum2[warp - 1] : 0);
+    if (s < p.S_loc) {
+      p.step_cost[s + 1] = before + x;
+      p.step_chunk[s + 1] = before2 + x2;
+    }
     if (tid == 0) {
       const int nw = blockDim.x >> 5;
       for (int w = 0; w < nw; ++w)
@@ -97,7 +108,10 @@ __global__ void __launch_bounds__(1024) bwd_prep_kernel(BwdPrepParams p) {
         for (int i = 0; i < NV; ++i) tot[i] += red[w][i];
     }
     __syncthreads();
-    if (tid == 0) s_carry += wsum[(blockDim.x >> 5) - 1];
+    if (tid == 0) {
+      s_carry += wsum[(blockDim.x >> 5) - 1];
+      s_carry2 += wsum2[(blockDim.x >> 5) - 1];
+    }
     __syncthreads();
   }
   if (tid == 0) {
@@ -117,75 +131,87 @@ __global__ void __launch_bounds__(1024) bwd_prep_kernel(BwdPrepParams p) {
 }
 
 // ============================================================== K4a
-__global__ void gs_kernel(GsParams p) {
+// Per local row: the 16-byte record the sweep needs -- g_t = c_s dell_t invT,
+// -lse2_t, y_t and z_{t,y} -- so a warp fetches one LDG.128 per row.
+__global__ void rowrec_kernel(RowRecParams p) {
   const int64_t nthreads = (int64_t)gridDim.x * blockDim.x;
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < p.T_loc; t += nthreads) {
-    p.gs[t] = (float)(p.step_scale[p.tok_step[t]] * (double)p.dell[t] * p.invT);
+    const float g = (float)(p.step_scale[p.tok_step[t]] * (double)p.dell[t] * p.invT);
+    int32_t y = p.target[t];
+    float zy = 0.f;
+    if (y >= 0 && y < p.V) {
+      const uint8_t* rp = p.logits + t * p.ld_bytes;
+      zy = p.is_bf16 ? __uint_as_float(((uint32_t)(*reinterpret_cast<const uint16_t*>(rp + 2 * (int64_t)y))) << 16)
+                     : *reinterpret_cast<const float*>(rp + 4 * (int64_t)y);
+    } else {
+      y = -1;
+    }
+    int4 r;
+    r.x = __float_as_int(g);
+    r.y = __float_as_int(-p.lse2[t]);
+    r.z = y;
+    r.w = __float_as_int(zy);
+    reinterpret_cast<int4*>(p.rec)[t] = r;
   }
 }
 
 // ============================================================== K4
-// Cursor over the warp's chunk range [x0, x1) in cost units.  A chunk of a
-// kept step costs 2 (read + write), of a masked step 1 (write) or 0 (skipped).
-struct BCur {
-  int64_t s;       // local step
-  int64_t t, tend; // local row, end row of the step
-  int64_t c;       // chunk within row
-  int64_t start;   // cost at the start of this chunk
-  int uc;          // unit cost of the step
+// Work split: each CTA owns a contiguous, cost-balanced range of chunks
+// (kept-step chunk = 2: read + write; masked = 1: write only, or absent when
+// zero_fill is off), and its warps interleave over it (warp w takes chunks
+// w, w+WARPS, ...).  Every SM thus streams ONE contiguous read region and ONE
+// write region at a time -- far fewer concurrent DRAM streams than a
+// warp-per-range split -- while still running WARPS independent rings.
+struct OCur {
+  int64_t j, jend;  // chunk ordinal (in the local chunk sequence) and the warp's end
+  int64_t s;        // local step
+  int64_t t, tend;  // local row, end row of the step
+  int32_t c;        // chunk within the row
   bool kept, valid;
 };
 
-__device__ __forceinline__ void bcur_set_step(BCur& b, const BwdParams& p, int64_t s) {
-  // skip zero-cost steps
-  while (s < p.S_loc && p.step_cost[s + 1] == p.step_cost[s]) ++s;
-  b.s = s;
-  if (s >= p.S_loc) { b.valid = false; return; }
+__device__ __forceinline__ void ocur_seek(OCur& o, const BwdParams& p, int64_t j) {
+  o.j = j;
+  o.valid = j < o.jend;
+  if (!o.valid) return;
+  // last s with step_chunk[s] <= j (empty steps skipped automatically)
+  const int64_t s = upper_bound_i64(p.step_chunk, 0, p.S_loc + 1, j) - 1;
+  o.s = s;
   const int64_t sg = p.step_begin + s;
-  b.t = p.step_tok_off[sg] - p.tok_begin;
-  b.tend = p.step_tok_off[sg + 1] - p.tok_begin;
-  b.c = 0;
-  b.start = p.step_cost[s];
-  b.kept = p.keep[sg] != 0;
-  b.uc = b.kept ? 2 : 1;
+  const int64_t off = j - p.step_chunk[s];
+  const int64_t t0 = p.step_tok_off[sg] - p.tok_begin;
+  o.tend = p.step_tok_off[sg + 1] - p.tok_begin;
+  o.t = t0 + off / p.nch;
+  o.c = (int32_t)(off % p.nch);
+  o.kept = p.keep[sg] != 0;
 }
 
-__device__ __forceinline__ void bcur_seek(BCur& b, const BwdParams& p, int64_t x0, int64_t x1) {
+__device__ __forceinline__ void ocur_advance(OCur& o, const BwdParams& p, int stride) {
+  o.j += stride;
+  if (o.j >= o.jend) { o.valid = false; return; }
+  o.c += stride;
+  while (o.c >= p.nch) { o.c -= (int32_t)p.nch; ++o.t; }
+  if (o.t >= o.tend) ocur_seek(o, p, o.j);
+}
+
+// producer: next chunk of a kept step (masked steps are jumped over whole)
+__device__ __forceinline__ void ocur_to_kept(OCur& o, const BwdParams& p, int stride) {
+  while (o.valid && !o.kept) {
+    const int64_t nxt = p.step_chunk[o.s + 1];
+    const int64_t k = (nxt - o.j + stride - 1) / stride;
+    ocur_seek(o, p, o.j + k * stride);
+  }
+}
+
+// first chunk ordinal whose start cost is >= x
+__device__ __forceinline__ int64_t ordinal_at_cost(const BwdParams& p, int64_t x) {
   const int64_t total = p.step_cost[p.S_loc];
-  b.valid = false;
-  if (x0 >= total || x0 >= x1) return;
-  const int64_t s = upper_bound_i64(p.step_cost, 0, p.S_loc + 1, x0) - 1;
-  b.valid = true;
-  bcur_set_step(b, p, s);
-  if (!b.valid) return;
-  const int64_t off = x0 - b.start;
-  const int64_t j = (off + b.uc - 1) / b.uc;  // first chunk starting at or after x0
-  const int64_t nj = (b.tend - b.t) * p.nch;
-  if (j >= nj) {
-    bcur_set_step(b, p, b.s + 1);
-  } else {
-    b.t += j / p.nch;
-    b.c = j % p.nch;
-    b.start += j * b.uc;
-  }
-  b.valid = b.valid && b.s < p.S_loc && b.start < x1;
-}
-
-__device__ __forceinline__ void bcur_next(BCur& b, const BwdParams& p, int64_t x1) {
-  b.start += b.uc;
-  if (++b.c == p.nch) {
-    b.c = 0;
-    if (++b.t == b.tend) bcur_set_step(b, p, b.s + 1);
-  }
-  b.valid = b.valid && b.s < p.S_loc && b.start < x1;
-}
-
-// advance to the next chunk of a kept step (skipping masked steps whole)
-__device__ __forceinline__ void bcur_to_kept(BCur& b, const BwdParams& p, int64_t x1) {
-  while (b.valid && !b.kept) {
-    bcur_set_step(b, p, b.s + 1);
-    b.valid = b.valid && b.s < p.S_loc && b.start < x1;
-  }
+  if (x >= total) return p.step_chunk[p.S_loc];
+  const int64_t s = upper_bound_i64(p.step_cost, 0, p.S_loc + 1, x) - 1;
+  const int uc = p.keep[p.step_begin + s] ? 2 : 1;
+  const int64_t off = (x - p.step_cost[s] + uc - 1) / uc;
+  const int64_t n = p.step_chunk[s + 1] - p.step_chunk[s];
+  return off >= n ? p.step_chunk[s + 1] : p.step_chunk[s] + off;
 }
 
 __device__ __forceinline__ void store_vals_bf16(uint8_t* dst, const float* v, int nvalid, int EPV) {
@@ -216,6 +242,20 @@ __device__ __forceinline__ void store_vals_f32(uint8_t* dst, const float* v, int
   }
 }
 
+template <typename Tin, int WARPS, int STAGES>
+__device__ __forceinline__ void bwd_issue(OCur& pc, const BwdParams& p, uint64_t* bars, uint8_t* ring, int slot,
+                                          int lane, uint64_t pol) {
+  const int64_t v0 = (int64_t)pc.c * CH_VEC;
+  const int64_t nv = min((int64_t)CH_VEC, p.nvec - v0);
+  if (lane == 0) {
+    mbar_arrive_expect_tx(&bars[slot], (uint32_t)nv * 16u);
+    bulk_g2s_hint(ring + (size_t)slot * CH_BYTES, p.logits + pc.t * p.ld_bytes + v0 * 16, (uint32_t)nv * 16u,
+                  &bars[slot], pol);
+  }
+  ocur_advance(pc, p, WARPS);
+  ocur_to_kept(pc, p, WARPS);
+}
+
 template <typename Tin, typename Tout, int WARPS, int STAGES>
 __global__ void __launch_bounds__(WARPS * 32)
 bwd_sweep_kernel(const BwdParams p) {
@@ -232,60 +272,49 @@ bwd_sweep_kernel(const BwdParams p) {
   }
   __syncwarp();
 
-  const int64_t W = (int64_t)gridDim.x * WARPS;
-  const int64_t wid = (int64_t)blockIdx.x * WARPS + warp;
+  // this CTA's contiguous, cost-balanced chunk range [J0, J1)
   const int64_t total = p.step_cost[p.S_loc];
-  // total <= T_loc * nch * 2 (~1e8 at 2M rows) and W ~ 1e3-1e5: no int64 overflow
-  const int64_t x0 = (total * wid) / W;
-  const int64_t x1 = (total * (wid + 1)) / W;
+  const int64_t nb = gridDim.x;
+  const int64_t J0 = ordinal_at_cost(p, (total * (int64_t)blockIdx.x) / nb);
+  const int64_t J1 = ordinal_at_cost(p, (total * ((int64_t)blockIdx.x + 1)) / nb);
   const int tail_elems = (int)(p.V % EPV);
   const float c2 = p.c2;
   const uint64_t pol = policy_evict_first();
+  const int4* rec = reinterpret_cast<const int4*>(p.rec);
 
-  BCur cc;
-  bcur_seek(cc, p, x0, x1);
-  BCur pc = cc;
-  bcur_to_kept(pc, p, x1);
+  OCur cc;
+  cc.jend = J1;
+  ocur_seek(cc, p, J0 + warp);
+  OCur pc = cc;
+  ocur_to_kept(pc, p, WARPS);
 #pragma unroll 1
   for (int s = 0; s < STAGES; ++s) {
     if (!pc.valid) break;
-    const int64_t v0 = pc.c * CH_VEC;
-    const int64_t nv = min((int64_t)CH_VEC, p.nvec - v0);
-    if (lane == 0) {
-      mbar_arrive_expect_tx(&bars[s], (uint32_t)nv * 16u);
-      bulk_g2s_hint(ring + (size_t)s * CH_BYTES, p.logits + pc.t * p.ld_bytes + v0 * 16, (uint32_t)nv * 16u,
-                    &bars[s], pol);
-    }
-    bcur_next(pc, p, x1);
-    bcur_to_kept(pc, p, x1);
+    bwd_issue<Tin, WARPS, STAGES>(pc, p, bars, ring, s, lane, pol);
   }
 
   int slot = 0;
   uint32_t phase = 0;
-  int64_t cur_t = -1;
-  float g = 0.f, nl2 = 0.f, zy = 0.f;
-  int32_t y = -1;
+  int64_t cur_t = -1, pre_t = -1;
+  int4 cur = make_int4(0, 0, -1, 0), pre = make_int4(0, 0, -1, 0);
 
 #pragma unroll 1
   while (cc.valid) {
     const int64_t t = cc.t;
-    const int64_t v0 = cc.c * CH_VEC;
+    const int64_t v0 = (int64_t)cc.c * CH_VEC;
     const int nv = (int)min((int64_t)CH_VEC, p.nvec - v0);
     uint8_t* orow = p.dlogits + t * p.ldg_bytes;
     if (cc.kept) {
       if (t != cur_t) {
+        cur = (t == pre_t) ? pre : rec[t];
         cur_t = t;
-        g = p.gs[t];
-        nl2 = -p.lse2[t];
-        y = p.target[t];
-        if (y >= 0 && y < p.V) {
-          const uint8_t* rp = p.logits + t * p.ld_bytes;
-          zy = (sizeof(Tin) == 2) ? __uint_as_float(((uint32_t)(*reinterpret_cast<const uint16_t*>(rp + 2 * (int64_t)y))) << 16)
-                                  : *reinterpret_cast<const float*>(rp + 4 * (int64_t)y);
-        } else {
-          y = -1;
+        if (t + 1 < p.T_loc) {       // prefetch the next row's record (hidden behind this row)
+          pre = rec[t + 1];
+          pre_t = t + 1;
         }
       }
+      const float g = __int_as_float(cur.x), nl2 = __int_as_float(cur.y), zy = __int_as_float(cur.w);
+      const int32_t y = cur.z;
       mbar_wait(&bars[slot], phase);
       const uint8_t* sp = ring + (size_t)slot * CH_BYTES;
       const float2 cc2 = make_float2(c2, c2), nl = make_float2(nl2, nl2), ng = make_float2(-g, -g);
@@ -301,24 +330,13 @@ bwd_sweep_kernel(const BwdParams p) {
         }
       }
       // consume every loaded word before the slot is handed back to the copy
-      // engine (forces the LDS results to have landed: WAR across proxies)
+      // engine (read-then-async-write: the reads have completed)
       uint32_t dep = 0;
 #pragma unroll
       for (int k = 0; k < VPL; ++k) dep |= x[k].x | x[k].y | x[k].z | x[k].w;
       asm volatile("" ::"r"(dep));
       __syncwarp();
-      // the slot's data is in registers: refill it now (overlaps the math below)
-      if (pc.valid) {
-        const int64_t pv0 = pc.c * CH_VEC;
-        const int64_t pnv = min((int64_t)CH_VEC, p.nvec - pv0);
-        if (lane == 0) {  // read-then-async-write: the reads completed (values consumed above)
-          mbar_arrive_expect_tx(&bars[slot], (uint32_t)pnv * 16u);
-          bulk_g2s_hint(ring + (size_t)slot * CH_BYTES, p.logits + pc.t * p.ld_bytes + pv0 * 16,
-                        (uint32_t)pnv * 16u, &bars[slot], pol);
-        }
-        bcur_next(pc, p, x1);
-        bcur_to_kept(pc, p, x1);
-      }
+      if (pc.valid) bwd_issue<Tin, WARPS, STAGES>(pc, p, bars, ring, slot, lane, pol);
       if (++slot == STAGES) { slot = 0; phase ^= 1u; }
 #pragma unroll
       for (int k = 0; k < VPL; ++k) {
@@ -381,7 +399,7 @@ bwd_sweep_kernel(const BwdParams p) {
         }
       }
     }
-    bcur_next(cc, p, x1);
+    ocur_advance(cc, p, WARPS);
   }
 }
 
@@ -391,11 +409,11 @@ cudaError_t launch_bwd_prep(const BwdPrepParams& p, cudaStream_t st) {
   return cudaGetLastError();
 }
 
-cudaError_t launch_gs(const GsParams& p, cudaStream_t st) {
+cudaError_t launch_rowrec(const RowRecParams& p, cudaStream_t st) {
   if (p.T_loc <= 0) return cudaSuccess;
   int64_t blocks = (p.T_loc + 255) / 256;
   if (blocks > 8192) blocks = 8192;
-  gs_kernel<<<(unsigned)blocks, 256, 0, st>>>(p);
+  rowrec_kernel<<<(unsigned)blocks, 256, 0, st>>>(p);
   return cudaGetLastError();
 }
 

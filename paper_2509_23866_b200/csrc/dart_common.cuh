@@ -27,10 +27,11 @@ constexpr double LN2_D = 0.6931471805599453094172;
 // ---------------------------------------------------------------- workspace
 // Sub-buffers (256 B aligned), identical layout in every call of one pass.
 struct WsLayout {
-  size_t tok_adv, tok_step, lse2, aux_w, aux_kl, aux_flags, gs;         // [T_loc]
+  size_t tok_adv, tok_step, lse2, aux_w, aux_kl, aux_flags, rec;        // [T_loc] (rec: 16 B)
   size_t step_stats;                                                    // [S_loc * NSTAT] f64
   size_t step_cost;                                                     // [S_loc+1] i64
   size_t step_scale;                                                    // [S_loc] f64
+  size_t step_chunk;                                                    // [S_loc+1] i64
   size_t part_m, part_s, part_u, row_cnt;                               // split mode [T_loc*KSEG]
   size_t H_glob;                                                        // [S] f32
   size_t grp_traj;                                                      // [G+1] i64 (trajectory CSR of groups)

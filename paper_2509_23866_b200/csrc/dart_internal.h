@@ -114,17 +114,22 @@ struct BwdPrepParams {
   const double* step_ell;
   const double* step_stats;
   double* step_scale;    // [S_loc]
-  int64_t* step_cost;    // [S_loc+1]
+  int64_t* step_cost;    // [S_loc+1] prefix of chunk costs (kept 2, masked 1 or 0)
+  int64_t* step_chunk;   // [S_loc+1] prefix of chunks that need work
   void* stats;           // dart_stats*
 };
 
-struct GsParams {
-  int64_t T_loc;
+struct RowRecParams {
+  int64_t T_loc, V, ld_bytes;
+  int is_bf16;
+  const uint8_t* logits;
   const int32_t* tok_step;
+  const int32_t* target;
   const double* step_scale;
   const float* dell;
+  const float* lse2;
   double invT;
-  float* gs;
+  void* rec;  // int4 [T_loc]: {g, -lse2, y, z_y}
 };
 
 struct BwdParams {
@@ -133,13 +138,12 @@ struct BwdParams {
   uint8_t* dlogits;
   int64_t ldg_bytes;
   float c2;
-  const int32_t* target;
-  const float* lse2;
-  const float* gs;
+  const void* rec;              // int4 [T_loc] row records (K4a)
   const int64_t* step_tok_off;  // global CSR
   int64_t tok_begin, step_begin, S_loc;
   const uint8_t* keep;          // [S] global
   const int64_t* step_cost;     // [S_loc+1] prefix of chunk costs
+  const int64_t* step_chunk;    // [S_loc+1] prefix of chunk counts
   int zero_fill;
 };
 
@@ -151,7 +155,7 @@ cudaError_t launch_unpack(const UnpackParams& p, cudaStream_t st);
 cudaError_t launch_select(const SelectParams& p, cudaStream_t st);
 cudaError_t launch_norm(const NormParams& p, cudaStream_t st);
 cudaError_t launch_bwd_prep(const BwdPrepParams& p, cudaStream_t st);
-cudaError_t launch_gs(const GsParams& p, cudaStream_t st);
+cudaError_t launch_rowrec(const RowRecParams& p, cudaStream_t st);
 cudaError_t launch_bwd_sweep(const BwdParams& p, bool in_bf16, bool out_bf16, int num_sms, cudaStream_t st);
 
 }  // namespace dart
