@@ -316,9 +316,9 @@ class DartLoss:
         """C1: all-gather of the per-rank step entropies (padded to S_pad)."""
         if self.world == 1:
             return
-        import torch.distributed as dist
+        from . import dist as D
         self.step_H_pad[:self.shard.S_loc].copy_(self.step_H[:self.shard.S_loc])
-        dist.all_gather_into_tensor(self.gathered, self.step_H_pad, group=self.group)
+        D.all_gather_into(self.gathered, self.step_H_pad, group=self.group)
 
     def set_gathered(self, gathered: torch.Tensor):
         """Provide the all-gathered [world * S_pad] step entropies directly
@@ -348,8 +348,8 @@ class DartLoss:
         """C2: all-reduce(SUM) of the fp64 loss / statistics partials."""
         if self.world == 1 or self.group is False:
             return
-        import torch.distributed as dist
-        dist.all_reduce(self.stats, group=self.group)
+        from . import dist as D
+        D.all_reduce(self.stats, group=self.group)
 
     def run(self, logits, target, logp_old, logp_roll, logp_ref=None):
         """One whole pass (fwd -> C1 -> select -> bwd -> C2), stream-ordered."""

@@ -43,6 +43,36 @@ def s_pad(shards):
     return max(max(s.S_loc for s in shards), 1)
 
 
+def _gloo(group=None):
+    import torch.distributed as dist
+    return dist.get_backend(group) == "gloo"
+
+
+def all_gather_into(out: torch.Tensor, inp: torch.Tensor, group=None):
+    """all_gather_into_tensor; with gloo (CPU test backend) CUDA tensors are
+    staged through host memory."""
+    import torch.distributed as dist
+    if out.is_cuda and _gloo(group):
+        o = out.cpu()
+        dist.all_gather_into_tensor(o, inp.cpu(), group=group)
+        out.copy_(o)
+    else:
+        dist.all_gather_into_tensor(out, inp, group=group)
+    return out
+
+
+def all_reduce(t: torch.Tensor, op=None, group=None):
+    import torch.distributed as dist
+    op = dist.ReduceOp.SUM if op is None else op
+    if t.is_cuda and _gloo(group):
+        c = t.cpu()
+        dist.all_reduce(c, op=op, group=group)
+        t.copy_(c)
+    else:
+        dist.all_reduce(t, op=op, group=group)
+    return t
+
+
 def gather_padded(local: torch.Tensor, S_pad: int, group=None) -> torch.Tensor:
     """C1: every rank contributes `local` (its S_loc step values) padded to
     S_pad; returns [world * S_pad] in rank order (the layout
@@ -52,12 +82,10 @@ def gather_padded(local: torch.Tensor, S_pad: int, group=None) -> torch.Tensor:
     pad = torch.zeros(S_pad, dtype=local.dtype, device=local.device)
     pad[:local.numel()].copy_(local)
     out = torch.empty(world * S_pad, dtype=local.dtype, device=local.device)
-    dist.all_gather_into_tensor(out, pad, group=group)
+    all_gather_into(out, pad, group=group)
     return out
 
 
 def reduce_stats(stats: torch.Tensor, group=None) -> torch.Tensor:
     """C2: all-reduce(SUM) of the fp64 loss / statistics partials."""
-    import torch.distributed as dist
-    dist.all_reduce(stats, group=group)
-    return stats
+    return all_reduce(stats, group=group)
