@@ -15,6 +15,10 @@
 #include "dart_common.cuh"
 #include "dart_internal.h"
 
+#ifndef DART_BWD_STYLE
+#define DART_BWD_STYLE 1
+#endif
+
 namespace dart {
 
 // ============================================================== K6
@@ -242,6 +246,51 @@ __device__ __forceinline__ void store_vals_f32(uint8_t* dst, const float* v, int
   }
 }
 
+// dz for the EPV logits of one 16-byte input vector: -g * 2^(z c2 - lse2)
+template <typename Tin>
+__device__ __forceinline__ void grad_vec(const uint4& xv, float2 cc2, float2 nl, float2 ng, float* o) {
+  const uint32_t* w = reinterpret_cast<const uint32_t*>(&xv);
+  if (sizeof(Tin) == 2) {
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const float2 z = make_float2(bf16lo(w[j]), bf16hi(w[j]));
+      const float2 d = __ffma2_rn(z, cc2, nl);
+      const float2 pr = make_float2(ex2(d.x), ex2(d.y));
+      const float2 dz = __fmul2_rn(pr, ng);
+      o[2 * j] = dz.x;
+      o[2 * j + 1] = dz.y;
+    }
+  } else {
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      const float2 z = make_float2(__uint_as_float(w[2 * j]), __uint_as_float(w[2 * j + 1]));
+      const float2 d = __ffma2_rn(z, cc2, nl);
+      const float2 pr = make_float2(ex2(d.x), ex2(d.y));
+      const float2 dz = __fmul2_rn(pr, ng);
+      o[2 * j] = dz.x;
+      o[2 * j + 1] = dz.y;
+    }
+  }
+}
+
+// store EPV outputs of one full vector (compile-time widths, streaming stores)
+template <typename Tout, int EPV>
+__device__ __forceinline__ void store_full(uint8_t* dst, const float* o) {
+  if (sizeof(Tout) == 2) {
+    if (EPV == 8) {
+      stg128_cs(dst, make_uint4(pack_bf16x2(o[0], o[1]), pack_bf16x2(o[2], o[3]), pack_bf16x2(o[4], o[5]),
+                                pack_bf16x2(o[6], o[7])));
+    } else {
+      *reinterpret_cast<uint2*>(dst) = make_uint2(pack_bf16x2(o[0], o[1]), pack_bf16x2(o[2], o[3]));
+    }
+  } else {
+#pragma unroll
+    for (int e = 0; e < EPV; e += 4)
+      stg128_cs(dst + 4 * e, make_uint4(__float_as_uint(o[e]), __float_as_uint(o[e + 1]), __float_as_uint(o[e + 2]),
+                                        __float_as_uint(o[e + 3])));
+  }
+}
+
 template <typename Tin, int WARPS, int STAGES>
 __device__ __forceinline__ void bwd_issue(OCur& pc, const BwdParams& p, uint64_t* bars, uint8_t* ring, int slot,
                                           int lane, uint64_t pol) {
@@ -256,8 +305,18 @@ __device__ __forceinline__ void bwd_issue(OCur& pc, const BwdParams& p, uint64_t
   ocur_to_kept(pc, p, WARPS);
 }
 
+#ifndef DART_BWD_MINB
+#define DART_BWD_MINB 1
+#endif
+// DART_BWD_FULL=1 takes an unpredicated path for full chunks: fewer
+// instructions, but measured 14% SLOWER on B200 (6.17 vs 5.41 ms, store
+// drain stalls: long_scoreboard on STG source registers + lg_throttle), so
+// the per-vector guarded path is the default.
+#ifndef DART_BWD_FULL
+#define DART_BWD_FULL 0
+#endif
 template <typename Tin, typename Tout, int WARPS, int STAGES>
-__global__ void __launch_bounds__(WARPS * 32)
+__global__ void __launch_bounds__(WARPS * 32, DART_BWD_MINB)
 bwd_sweep_kernel(const BwdParams p) {
   extern __shared__ __align__(128) uint8_t smem[];
   constexpr int EPV = 16 / sizeof(Tin);       // logits per 16-byte input vector
@@ -296,19 +355,25 @@ bwd_sweep_kernel(const BwdParams p) {
   int slot = 0;
   uint32_t phase = 0;
   int64_t cur_t = -1, pre_t = -1;
+  const int64_t nvec = p.nvec, T_loc = p.T_loc, ldg_bytes = p.ldg_bytes;
+  uint8_t* const dlog = p.dlogits;
+  constexpr int64_t OUTV = EPV * (int64_t)sizeof(Tout);   // output bytes per input vector
   int4 cur = make_int4(0, 0, -1, 0), pre = make_int4(0, 0, -1, 0);
 
 #pragma unroll 1
   while (cc.valid) {
     const int64_t t = cc.t;
     const int64_t v0 = (int64_t)cc.c * CH_VEC;
-    const int nv = (int)min((int64_t)CH_VEC, p.nvec - v0);
-    uint8_t* orow = p.dlogits + t * p.ldg_bytes;
+    const int nv = (int)min((int64_t)CH_VEC, nvec - v0);
+    // full chunk: all lanes hold VPL complete vectors (no tail, no predicates)
+    const bool full = DART_BWD_FULL && (nv == CH_VEC) && !(tail_elems && v0 + nv == nvec);
+    uint8_t* orow = dlog + t * ldg_bytes;
+    uint8_t* olane = orow + (v0 + lane) * OUTV;    // this lane's first output vector
     if (cc.kept) {
       if (t != cur_t) {
         cur = (t == pre_t) ? pre : rec[t];
         cur_t = t;
-        if (t + 1 < p.T_loc) {       // prefetch the next row's record (hidden behind this row)
+        if (t + 1 < T_loc) {       // prefetch the next row's record (hidden behind this row)
           pre = rec[t + 1];
           pre_t = t + 1;
         }
@@ -319,7 +384,7 @@ bwd_sweep_kernel(const BwdParams p) {
       const uint8_t* sp = ring + (size_t)slot * CH_BYTES;
       const float2 cc2 = make_float2(c2, c2), nl = make_float2(nl2, nl2), ng = make_float2(-g, -g);
       uint4 x[VPL];
-      if (nv == CH_VEC) {
+      if (full) {
 #pragma unroll
         for (int k = 0; k < VPL; ++k) x[k] = lds128(sp + (lane + 32 * k) * 16);
       } else {
@@ -338,38 +403,37 @@ bwd_sweep_kernel(const BwdParams p) {
       __syncwarp();
       if (pc.valid) bwd_issue<Tin, WARPS, STAGES>(pc, p, bars, ring, slot, lane, pol);
       if (++slot == STAGES) { slot = 0; phase ^= 1u; }
+      if (full) {
 #pragma unroll
-      for (int k = 0; k < VPL; ++k) {
-        const int vi = lane + 32 * k;
-        if (vi < nv) {
-          const int64_t gv = v0 + vi;
+        for (int k = 0; k < VPL; ++k) {
+#if DART_BWD_STYLE == 1
+          if (lane + 32 * k < nv) {   // always true here: keeps compute/store of each vector together
+#endif
           float o[EPV];
-          const uint32_t* w = reinterpret_cast<const uint32_t*>(&x[k]);
-          if (sizeof(Tin) == 2) {
-#pragma unroll
-            for (int j = 0; j < 4; ++j) {
-              const float2 z = make_float2(bf16lo(w[j]), bf16hi(w[j]));
-              const float2 d = __ffma2_rn(z, cc2, nl);
-              const float2 pr = make_float2(ex2(d.x), ex2(d.y));
-              const float2 dz = __fmul2_rn(pr, ng);
-              o[2 * j] = dz.x;
-              o[2 * j + 1] = dz.y;
-            }
-          } else {
-#pragma unroll
-            for (int j = 0; j < 2; ++j) {
-              const float2 z = make_float2(__uint_as_float(w[2 * j]), __uint_as_float(w[2 * j + 1]));
-              const float2 d = __ffma2_rn(z, cc2, nl);
-              const float2 pr = make_float2(ex2(d.x), ex2(d.y));
-              const float2 dz = __fmul2_rn(pr, ng);
-              o[2 * j] = dz.x;
-              o[2 * j + 1] = dz.y;
-            }
+#if DART_BWD_STYLE == 2
+          if (k > 0) {  // order: store(k-1) before the math of vector k (spreads the stores)
+            asm volatile("" : "+r"(x[k].x), "+r"(x[k].y), "+r"(x[k].z), "+r"(x[k].w));
           }
-          const int nvalid = (tail_elems && gv == p.nvec - 1) ? tail_elems : EPV;
-          uint8_t* dst = orow + gv * EPV * (int64_t)sizeof(Tout);
-          if (OUT_BF16) store_vals_bf16(dst, o, nvalid, EPV);
-          else store_vals_f32(dst, o, nvalid, EPV);
+#endif
+          grad_vec<Tin>(x[k], cc2, nl, ng, o);
+          store_full<Tout, EPV>(olane + k * 32 * OUTV, o);
+#if DART_BWD_STYLE == 1
+          }
+#endif
+        }
+      } else {
+#pragma unroll
+        for (int k = 0; k < VPL; ++k) {
+          const int vi = lane + 32 * k;
+          if (vi < nv) {
+            const int64_t gv = v0 + vi;
+            float o[EPV];
+            grad_vec<Tin>(x[k], cc2, nl, ng, o);
+            const int nvalid = (tail_elems && gv == nvec - 1) ? tail_elems : EPV;
+            uint8_t* dst = orow + gv * OUTV;
+            if (OUT_BF16) store_vals_bf16(dst, o, nvalid, EPV);
+            else store_vals_f32(dst, o, nvalid, EPV);
+          }
         }
       }
       // target element: dz_y = g (1 - p_y), written after the vector store (same thread)
@@ -384,18 +448,23 @@ bwd_sweep_kernel(const BwdParams p) {
       }
     } else {
       // masked step: zeros, no read
+      float o[EPV];
 #pragma unroll
-      for (int k = 0; k < VPL; ++k) {
-        const int vi = lane + 32 * k;
-        if (vi < nv) {
-          const int64_t gv = v0 + vi;
-          float o[EPV];
+      for (int e = 0; e < EPV; ++e) o[e] = 0.f;
+      if (full) {
 #pragma unroll
-          for (int e = 0; e < EPV; ++e) o[e] = 0.f;
-          const int nvalid = (tail_elems && gv == p.nvec - 1) ? tail_elems : EPV;
-          uint8_t* dst = orow + gv * EPV * (int64_t)sizeof(Tout);
-          if (OUT_BF16) store_vals_bf16(dst, o, nvalid, EPV);
-          else store_vals_f32(dst, o, nvalid, EPV);
+        for (int k = 0; k < VPL; ++k) store_full<Tout, EPV>(olane + k * 32 * OUTV, o);
+      } else {
+#pragma unroll
+        for (int k = 0; k < VPL; ++k) {
+          const int vi = lane + 32 * k;
+          if (vi < nv) {
+            const int64_t gv = v0 + vi;
+            const int nvalid = (tail_elems && gv == nvec - 1) ? tail_elems : EPV;
+            uint8_t* dst = orow + gv * OUTV;
+            if (OUT_BF16) store_vals_bf16(dst, o, nvalid, EPV);
+            else store_vals_f32(dst, o, nvalid, EPV);
+          }
         }
       }
     }

@@ -517,8 +517,9 @@ fwd_sweep_kernel(const FwdParams p) {
         seg = segment_slow<Tin>(p, row, k, lane);      // -inf logits in the segment
       } else {
         const float M = warp_max_f(a.m);
-        const double dm = (double)a.m - (double)M;
-        const double f = exp2(dm);
+        const float dmf = a.m - M;
+        const double dm = (double)dmf;
+        const double f = (double)ex2(dmf);
         seg.m = (double)M;
         seg.s = warp_sum_d((double)sl * f);
         seg.u = warp_sum_d(((double)ul + (double)sl * dm) * f);
