@@ -134,6 +134,87 @@ CONFIG_DESC = {
 }
 
 
+# ------------------------------------------------------------------ streamed arm
+def run_streamed(args):
+    """Configs whose logits exceed HBM (long-horizon 249 GB, scale sweep):
+    forward over chunks -> select -> backward over chunks, logits/dlogits in a
+    pool of P buffers (chunk c -> slot c mod P in both sweeps; the synthetic
+    slot contents are generated once, so both sweeps read identical bytes)."""
+    from paper_2509_23866_b200 import build as B
+    B.build()
+    world, rank, local = dist_setup(args)
+    if world > 1:
+        raise SystemExit("--stream-rows is single-process (per-rank streaming with a global "
+                         "normaliser is not implemented yet)")
+    from paper_2509_23866_b200 import dart, synth
+    from paper_2509_23866_b200.stream import StreamedPass
+    dev = torch.device("cuda", torch.cuda.current_device())
+    layout, V, dtype, _ = synth.config_layout(args.config, seed=args.seed)
+    cfg = dart.Config(entropy_q=args.q, beta_kl=args.beta, zero_fill_masked=0 if args.compact else 1,
+                      select_rule=dart.SEL_OFF if args.q <= 0 else dart.SEL_FLOOR)
+    sp = StreamedPass(layout, V, cfg, dev, max_rows=args.stream_rows, pool=args.pool, logits_dtype=dtype)
+    P = sp.P
+    # synthetic rows for the P pool slots (P x rows tokens, the config's value
+    # recipe); chunk c row r reads slot (c mod P) row r in both sweeps
+    rows = sp.rows
+    nstep = -(-P * rows // 64)
+    sub = synth.Layout(G=1, traj_group=np.zeros(1, np.int32), traj_reward=np.ones(1, np.float32),
+                       traj_step_off=np.array([0, nstep], np.int64),
+                       step_tok_off=np.minimum(np.arange(nstep + 1, dtype=np.int64) * 64, P * rows),
+                       step_fork=np.random.default_rng(args.seed).random(nstep) < 0.3)
+    t0 = time.time()
+    sb = synth.make_batch(args.config, seed=args.seed, device=dev, layout=sub, V=V, dtype=dtype)
+    for k in range(P):
+        sp.pool_logits[k].copy_(sb.logits[k * rows:(k + 1) * rows])
+    T = layout.T
+    idx = torch.empty(T, dtype=torch.int64, device=dev)
+    for i, c in enumerate(sp.chunks):
+        base = (i % P) * rows
+        idx[c.tok_begin:c.tok_end] = torch.arange(base, base + c.T_loc, device=dev)
+    target, lo, lr, lref = (x[idx].contiguous() for x in (sb.target, sb.logp_old, sb.logp_rollout, sb.logp_ref))
+    del sb
+    torch.cuda.synchronize()
+    log(f"streamed {args.config}: T={T} in {len(sp.chunks)} chunks of <= {sp.rows} rows, pool {P}; "
+        f"setup {time.time() - t0:.1f}s")
+    for _ in range(args.warmup):
+        sp.run(target, lo, lr, lref)
+    torch.cuda.synchronize()
+    sp.status.zero_()
+    sp.launches = 0
+    stream = torch.cuda.current_stream()
+    clk = ClockSampler(local)
+    clk.start()
+    time.sleep(0.15)
+    s0 = torch.cuda.Event(enable_timing=True)
+    s1 = torch.cuda.Event(enable_timing=True)
+    s0.record(stream)
+    for _ in range(args.steps):
+        sp.run(target, lo, lr, lref)
+    s1.record(stream)
+    torch.cuda.synchronize()
+    clocks = clk.stop()
+    sp.check_status()
+    ms = s0.elapsed_time(s1) / args.steps
+    keep = sp.keep.cpu().numpy()[:layout.S].astype(bool)
+    n = np.diff(layout.step_tok_off)
+    kept = int(n[keep].sum())
+    es = 2
+    byts = T * (es * V + 24) + kept * 2 * es * V + (0 if args.compact else (T - kept) * es * V)
+    peak, src = hbm_peak()
+    gbs = byts / (ms * 1e-3) / 1e9
+    line = {"metric": "loss fwd+bwd logit-tokens/s at V=152064 bf16, % of HBM peak, 1/2/4/8 GPU",
+            "value": T / (ms * 1e-3), "unit": "logit-tokens/s", "n_gpus": 1, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "bf16", "data": "synthetic (seeded; pooled chunk logits)",
+            "config": {"workload": args.config, "global_tokens": T, "V": V, "groups": layout.G,
+                       "steps_total": layout.S, "chunks": len(sp.chunks), "chunk_rows": sp.rows, "pool": P,
+                       "kept_token_frac": kept / T, "streamed": True},
+            "roofline": {"bound": "hbm", "kernel": "whole step (fwd+select+bwd sweeps)", "achieved": gbs,
+                         "peak": peak, "peak_source": src, "unit": "GB/s", "frac": gbs / peak, "traffic": None},
+            "gpu_launches": sp.launches, "clocks": clocks, "e2e": None, "cpu_baseline": None}
+    print(json.dumps(line), flush=True)
+
+
 # ------------------------------------------------------------------ our arm
 def run_dart(args):
     from paper_2509_23866_b200 import build as B
@@ -459,6 +540,9 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-tokens", type=int, default=1024)
+    ap.add_argument("--stream-rows", type=int, default=0,
+                    help="chunk-stream the batch with chunks of at most this many rows (configs > HBM)")
+    ap.add_argument("--pool", type=int, default=3, help="logits/dlogits pool buffers when streaming")
     ap.add_argument("--backend", default="nccl", choices=["nccl", "gloo"],
                     help="gloo: test path (ranks may share a GPU; collectives staged via host)")
     args = ap.parse_args()
@@ -467,6 +551,8 @@ def main():
         args.warmup = 3
     if args.impl == "reference":
         run_reference(args)
+    elif args.stream_rows > 0:
+        run_streamed(args)
     else:
         run_dart(args)
 

@@ -79,3 +79,13 @@ def test_shards_cover_whole_trajectories_balanced(name, world):
     for s in shards:
         if layout.N_traj >= world:
             assert abs(s.T_loc - layout.T / world) <= max_traj
+
+
+def test_chunk_layout_whole_trajectories():
+    from paper_2509_23866_b200.stream import chunk_layout
+    layout, _, _, _ = synth.config_layout("long", seed=0)
+    ch = chunk_layout(layout, 32768)
+    assert ch[0].tok_begin == 0 and ch[-1].tok_end == layout.T
+    for a, c in zip(ch, ch[1:]):
+        assert a.traj_end == c.traj_begin and a.tok_end == c.tok_begin
+    assert max(c.T_loc for c in ch) <= 32768
