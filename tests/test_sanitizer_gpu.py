@@ -1,0 +1,24 @@
+"""compute-sanitizer memcheck + racecheck over a small pass (bulk-copy rings,
+mbarriers, split-row mode, ragged vocab tails).  Full four-tool runs:
+tools/gpu_sanitize.sh, logs in profiles/r01_sanitize_*.log."""
+import os
+import shutil
+import subprocess
+import sys
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.mark.parametrize("tool", ["memcheck", "racecheck"])
+def test_compute_sanitizer_clean(tool):
+    cs = shutil.which("compute-sanitizer") or "/usr/local/cuda/bin/compute-sanitizer"
+    if not os.path.exists(cs):
+        pytest.skip("compute-sanitizer not found")
+    r = subprocess.run([cs, "--tool", tool, "--error-exitcode", "9", sys.executable,
+                        os.path.join(ROOT, "tools", "sanitize_driver.py"), "tiny", "odd", "midsplit"],
+                       cwd=ROOT, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+    assert "0 errors" in r.stdout or "0 hazards" in r.stdout
