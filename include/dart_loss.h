@@ -53,7 +53,7 @@
 extern "C" {
 #endif
 
-#define DART_ABI_VERSION 1
+#define DART_ABI_VERSION 2
 
 typedef enum {
   DART_OK = 0,
@@ -84,6 +84,18 @@ typedef enum {
 } dart_select_rule;
 /* q*n and q*(n-1) are evaluated in float64 from the float32 value of entropy_q. */
 
+/* Granularity of the importance ratio r = pi_theta / pi_old^Train and of the
+ * truncated IS weight. */
+typedef enum {
+  DART_RATIO_TOKEN = 0,  /* per token: r_t = exp(logp_t - logp_old_t), w_t = min(exp(logp_old_t - logp_roll_t), C);
+                            ell_t = -w_t min(r_t A, clip(r_t) A) + beta k3_t                  (default) */
+  DART_RATIO_STEP = 1    /* per step (the literal pi(a|h,s) of Eq. 1/2): r_s = exp(sum_{t in s} logp_t - logp_old_t),
+                            w_s = min(exp(sum_t logp_old_t - logp_roll_t), C);
+                            ell_s = -w_s min(r_s A, clip(r_s) A) + beta sum_{t in s} k3_t, and
+                            L = sum_{kept s} inv_norm * ell_s (no 1/n_s factor in any mode);
+                            out.ell[t] holds ell_s / n_s and step_ell[s] holds ell_s */
+} dart_ratio_level;
+
 /* Device status bits (OR-accumulated into *status). */
 #define DART_STATUS_NONFINITE_LOGIT (1u << 0) /* NaN or +inf logit in a row */
 #define DART_STATUS_TARGET_RANGE    (1u << 1) /* target outside [0, V) */
@@ -108,6 +120,7 @@ typedef struct {
   int32_t select_rule;    /* dart_select_rule */
   int32_t zero_fill_masked; /* 1: dense dlogits (masked rows written as zeros);
                                0: masked rows are left untouched                   */
+  int32_t ratio_level;    /* dart_ratio_level */
 } dart_cfg;
 
 /* GLOBAL batch metadata, replicated on every rank (device pointers). */

@@ -51,6 +51,9 @@ SEL_CEIL = 1
 SEL_LINEAR = 2
 SEL_OFF = 3
 
+RATIO_TOKEN = 0     # r, w per token (default)
+RATIO_STEP = 1      # r, w per step on sum_t log pi(y_t) (PAPER.md:124/257 pi(a|h,s))
+
 
 # --------------------------------------------------------------------------
 # Metadata helpers (pure indexing, no method arithmetic)
@@ -285,8 +288,10 @@ def token_loss(logp, logp_old, logp_roll, logp_ref, A, cfg):
 # a6. Normalisation of the expectation over D  (PAPER.md:255 E over D; token
 #     aggregation unstated -- SURVEY Q11: default token-mean over kept tokens)
 # --------------------------------------------------------------------------
-def step_weights(keep, step_tok_off, mode):
-    """Per-step multiplier c_s so that L = sum_s c_s * sum_{t in s} ell_t."""
+def step_weights(keep, step_tok_off, mode, per_step_loss=False):
+    """Per-step multiplier c_s so that L = sum_s c_s * sum_{t in s} ell_t.
+    per_step_loss: the loss term is already one number per step (step-ratio
+    mode), so the step-mean modes drop their 1/n_s factor."""
     off = np.asarray(step_tok_off, dtype=np.int64)
     n = (off[1:] - off[:-1]).astype(np.float64)
     keep = np.asarray(keep).astype(bool)
@@ -300,13 +305,13 @@ def step_weights(keep, step_tok_off, mode):
     elif mode == NORM_STEP_MEAN_KEPT:
         N = float(np.sum(keep))
         if N > 0:
-            c[keep] = 1.0 / (N * n[keep])
+            c[keep] = 1.0 / (N * (1.0 if per_step_loss else n[keep]))
     elif mode == NORM_TOKEN_MEAN_ALL:
         if T > 0:
             c[keep] = 1.0 / T
     elif mode == NORM_STEP_MEAN_ALL:
         if S > 0:
-            c[keep] = 1.0 / (S * n[keep])
+            c[keep] = 1.0 / (S * (1.0 if per_step_loss else n[keep]))
     elif mode == NORM_SUM:
         c[keep] = 1.0
     else:
@@ -319,7 +324,8 @@ def step_weights(keep, step_tok_off, mode):
 # --------------------------------------------------------------------------
 DEFAULT_CFG = dict(eps_low=0.2, eps_high=0.28, is_cap=1.0, beta_kl=0.1,
                    entropy_q=0.2, inv_temperature=1.0, adv_eps=0.0,
-                   norm_mode=NORM_TOKEN_MEAN_KEPT, select_rule=SEL_FLOOR)
+                   norm_mode=NORM_TOKEN_MEAN_KEPT, select_rule=SEL_FLOOR,
+                   ratio_level=RATIO_TOKEN)
 # (PAPER.md:575 eps_low 0.2, eps_high 0.28, beta 0.1, C 1; PAPER.md:578
 #  temperature 1.0; PAPER.md:235/264 the 0.2 quantile)
 
@@ -383,12 +389,39 @@ def loss_pass(batch, cfg, keep_override=None, want_grad=True, rows=None):
     r = np.empty(T)
     clipped = np.zeros(T, dtype=bool)
     kl = np.empty(T)
-    for t in range(T):
-        ell[t], dell[t], w[t], r[t], clipped[t], kl[t] = token_loss(
-            logp[t], lo[t], lr[t], lref[t], A_tok[t], cfg)
+    trunc = np.zeros(T, dtype=bool)
+    step_ratio = cfg.get("ratio_level", RATIO_TOKEN) == RATIO_STEP
+    if not step_ratio:
+        for t in range(T):
+            ell[t], dell[t], w[t], r[t], clipped[t], kl[t] = token_loss(
+                logp[t], lo[t], lr[t], lref[t], A_tok[t], cfg)
+            trunc[t] = math.exp(lo[t] - lr[t]) >= cfg["is_cap"]
+    else:
+        # step-level ratio and IS weight on the step's sequence log-probability
+        # log pi(a|h,s) = sum_{t in s} log pi(y_t)
+        beta = cfg["beta_kl"]
+        for s_ in range(S):
+            toks = np.arange(step_tok_off[s_], step_tok_off[s_ + 1])
+            A_s = A_tok[toks[0]]
+            log_r = float(np.sum(logp[toks] - lo[toks]))
+            log_w = float(np.sum(lo[toks] - lr[toks]))
+            r_s = math.exp(log_r)
+            w_s = min(math.exp(log_w), cfg["is_cap"])
+            sur = surrogate(r_s, A_s, cfg["eps_low"], cfg["eps_high"])
+            dsur = surrogate_dlogp(r_s, A_s, cfg["eps_low"], cfg["eps_high"])   # d/d(log r_s)
+            kls = np.array([kl_k3(logp[t], lref[t]) if beta != 0.0 else 0.0 for t in toks])
+            ell_s = -w_s * sur + beta * float(np.sum(kls))
+            clip_s = not (r_s * A_s <= clip(r_s, 1.0 - cfg["eps_low"], 1.0 + cfg["eps_high"]) * A_s)
+            for j, t in enumerate(toks):
+                # d ell_s / d logp_t: d log r_s / d logp_t = 1
+                dk = kl_k3_dlogp(logp[t], lref[t]) if beta != 0.0 else 0.0
+                dell[t] = -w_s * dsur + beta * dk
+                ell[t] = ell_s / len(toks)
+                w[t], r[t], clipped[t], kl[t] = w_s, r_s, clip_s, kls[j]
+                trunc[t] = math.exp(log_w) >= cfg["is_cap"]
 
     # 6. normalisation and loss
-    c_step = step_weights(keep, step_tok_off, cfg["norm_mode"])
+    c_step = step_weights(keep, step_tok_off, cfg["norm_mode"], per_step_loss=step_ratio)
     c_tok = c_step[t_step]
     loss = float(np.sum(c_tok * ell))
 
@@ -403,7 +436,7 @@ def loss_pass(batch, cfg, keep_override=None, want_grad=True, rows=None):
         loss=loss, n_tok=float(T), n_kept_tok=float(np.sum(n[keep.astype(bool)])),
         n_kept_step=float(np.sum(keep)),
         sum_clip=float(np.sum(clipped[kt])),
-        sum_trunc=float(np.sum(np.exp(lo[kt] - lr[kt]) >= cfg["is_cap"])),
+        sum_trunc=float(np.sum(trunc[kt])),
         sum_w=float(np.sum(w[kt])), sum_adv=float(np.sum(A_tok[kt])),
         sum_adv2=float(np.sum(A_tok[kt] ** 2)), sum_H=float(np.sum(H)),
         sum_kl=float(np.sum(kl[kt])))

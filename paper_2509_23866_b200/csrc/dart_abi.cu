@@ -107,6 +107,7 @@ bool cfg_ok(const dart_cfg* c) {
   if (!(c->adv_eps >= 0.f) || !std::isfinite(c->adv_eps)) return false;
   if (c->norm_mode < DART_NORM_TOKEN_MEAN_KEPT || c->norm_mode > DART_NORM_SUM) return false;
   if (c->select_rule < DART_SEL_FLOOR || c->select_rule > DART_SEL_OFF) return false;
+  if (c->ratio_level != DART_RATIO_TOKEN && c->ratio_level != DART_RATIO_STEP) return false;
   return true;
 }
 
@@ -273,8 +274,11 @@ dart_status dart_loss_fwd(const dart_batch* b, const dart_meta* m, const dart_cf
     StepReduceParams sp;
     sp.T_loc = b->T_loc; sp.tok_begin = b->tok_begin; sp.step_begin = b->step_begin; sp.S_loc = b->S_loc;
     sp.step_tok_off = m->step_tok_off;
-    sp.H = o->tok_entropy; sp.ell = o->ell;
+    sp.H = o->tok_entropy; sp.ell = o->ell; sp.dell = o->dell;
     sp.aux_w = fp.aux_w; sp.aux_kl = fp.aux_kl; sp.tok_adv = fp.tok_adv; sp.aux_flags = fp.aux_flags;
+    sp.ratio_level = c->ratio_level;
+    sp.logp = o->logp; sp.logp_old = b->logp_old; sp.logp_roll = b->logp_rollout; sp.logp_ref = b->logp_ref;
+    sp.eps_low = c->eps_low; sp.eps_high = c->eps_high; sp.is_cap = c->is_cap; sp.beta = c->beta_kl;
     sp.step_entropy = o->step_entropy; sp.step_ell = o->step_ell;
     sp.step_stats = at<double>(ws, L.step_stats);
     DART_TRY(launch_step_reduce(sp, s));
@@ -350,6 +354,7 @@ dart_status dart_loss_bwd(const dart_batch* b, const dart_meta* m, const dart_cf
   BwdPrepParams pp;
   pp.T_loc = b->T_loc; pp.tok_begin = b->tok_begin; pp.step_begin = b->step_begin; pp.S_loc = b->S_loc;
   pp.nch = nch; pp.norm_mode = c->norm_mode; pp.zero_fill = c->zero_fill_masked ? 1 : 0;
+  pp.ratio_level = c->ratio_level;
   pp.step_tok_off = m->step_tok_off; pp.keep = keep; pp.norm = norm;
   pp.step_ell = f->step_ell; pp.step_stats = at<double>(ws, L.step_stats);
   pp.step_scale = at<double>(ws, L.step_scale);

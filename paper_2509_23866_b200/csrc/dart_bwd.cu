@@ -31,7 +31,10 @@ __global__ void __launch_bounds__(1024) bwd_prep_kernel(BwdPrepParams p) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const dart_norm* nrm = reinterpret_cast<const dart_norm*>(p.norm);
   const double inv_norm = nrm->inv_norm;
-  const bool step_mode = (p.norm_mode == DART_NORM_STEP_MEAN_KEPT || p.norm_mode == DART_NORM_STEP_MEAN_ALL);
+  // per-step 1/n_s factor of the step-mean modes; in step-ratio mode the loss
+  // term is already per step (ell_s), so no 1/n_s in any mode
+  const bool step_mode = p.ratio_level != DART_RATIO_STEP &&
+                         (p.norm_mode == DART_NORM_STEP_MEAN_KEPT || p.norm_mode == DART_NORM_STEP_MEAN_ALL);
   double tot[NV];
 #pragma unroll
   for (int i = 0; i < NV; ++i) tot[i] = 0.0;  // meaningful in thread 0 only

@@ -568,17 +568,24 @@ fwd_sweep_kernel(const FwdParams p) {
 
 // ============================================================== K2
 // One warp per local step; fixed-order per-lane sums + xor butterfly.
+// Step-ratio mode (DART_RATIO_STEP): the ratio, IS weight
+// and surrogate are taken on the step's sequence log-probability
+// sum_t log pi(y_t) (the literal pi(a|h,s) of PAPER.md:124, 257); the per-token
+// d ell / d logp_t = -w_s A r_s act_s + beta (1 - e^{d_t}) is rewritten here.
 __global__ void step_reduce_kernel(StepReduceParams p) {
   const int lane = threadIdx.x & 31;
   const int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const bool step_ratio = p.ratio_level == DART_RATIO_STEP;
   for (int64_t s = w; s < p.S_loc; s += nw) {
     const int64_t sg = p.step_begin + s;
     int64_t t0 = p.step_tok_off[sg] - p.tok_begin;
     int64_t t1 = p.step_tok_off[sg + 1] - p.tok_begin;
     t0 = max(t0, (int64_t)0);
     t1 = min(t1, p.T_loc);
+    const int64_t n = t1 - t0;
     double sH = 0, sE = 0, sw = 0, sclip = 0, strunc = 0, sA = 0, sA2 = 0, skl = 0;
+    double sdl = 0, sdw = 0;  // step ratio: sum(logp - logp_old), sum(logp_old - logp_roll)
     for (int64_t t = t0 + lane; t < t1; t += 32) {
       sH += (double)p.H[t];
       sE += (double)p.ell[t];
@@ -590,6 +597,10 @@ __global__ void step_reduce_kernel(StepReduceParams p) {
       sA += A;
       sA2 += A * A;
       skl += (double)p.aux_kl[t];
+      if (step_ratio) {
+        sdl += (double)p.logp[t] - (double)p.logp_old[t];
+        sdw += (double)p.logp_old[t] - (double)p.logp_roll[t];
+      }
     }
     sH = warp_sum_d(sH);
     sE = warp_sum_d(sE);
@@ -599,8 +610,35 @@ __global__ void step_reduce_kernel(StepReduceParams p) {
     sA = warp_sum_d(sA);
     sA2 = warp_sum_d(sA2);
     skl = warp_sum_d(skl);
+    if (step_ratio && n > 0) {
+      sdl = warp_sum_d(sdl);
+      sdw = warp_sum_d(sdw);
+      const double A = (double)p.tok_adv[t0];              // one trajectory per step
+      const double r = exp(sdl);
+      const double ratio = exp(sdw);
+      const double wt = fmin(ratio, p.is_cap);
+      const bool trunc = ratio >= p.is_cap;
+      const double lo_c = 1.0 - p.eps_low, hi_c = 1.0 + p.eps_high;
+      const double rc = fmin(fmax(r, lo_c), hi_c);
+      const double sur = fmin(r * A, rc * A);
+      const bool act = (A > 0.0) ? (r <= hi_c) : ((A < 0.0) ? (r >= lo_c) : true);
+      const double ell_s = -wt * sur + p.beta * skl;
+      const double dsur = -wt * (act ? A * r : 0.0);
+      const uint8_t flags = (uint8_t)((act ? 0u : 1u) | (trunc ? 2u : 0u));
+      for (int64_t t = t0 + lane; t < t1; t += 32) {
+        double dkl = 0.0;
+        if (p.beta != 0.0) dkl = 1.0 - exp((double)p.logp_ref[t] - (double)p.logp[t]);
+        p.dell[t] = (float)(dsur + p.beta * dkl);
+        p.ell[t] = (float)(ell_s / (double)n);
+        p.aux_w[t] = (float)wt;
+        p.aux_flags[t] = flags;
+      }
+      sE = ell_s;
+      sw = wt * (double)n;
+      sclip = act ? 0.0 : (double)n;
+      strunc = trunc ? (double)n : 0.0;
+    }
     if (lane == 0) {
-      const int64_t n = t1 - t0;
       p.step_entropy[s] = n > 0 ? (float)(sH / (double)n) : __int_as_float(0x7fc00000);
       p.step_ell[s] = sE;
       double* st = p.step_stats + s * NSTAT;

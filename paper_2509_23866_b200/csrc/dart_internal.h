@@ -69,11 +69,16 @@ struct FwdParams {
 struct StepReduceParams {
   int64_t T_loc, tok_begin, step_begin, S_loc;
   const int64_t* step_tok_off;
-  const float *H, *ell, *aux_w, *aux_kl, *tok_adv;
-  const uint8_t* aux_flags;
+  const float *H, *aux_kl, *tok_adv;
+  float *ell, *dell, *aux_w;       // rewritten per token in step-ratio mode
+  uint8_t* aux_flags;
   float* step_entropy;
   double* step_ell;
   double* step_stats;
+  // step-level ratio (DART_RATIO_STEP)
+  int ratio_level;
+  const float *logp, *logp_old, *logp_roll, *logp_ref;
+  double eps_low, eps_high, is_cap, beta;
 };
 
 struct SelectParams {
@@ -107,7 +112,7 @@ struct UnpackParams {
 
 struct BwdPrepParams {
   int64_t T_loc, tok_begin, step_begin, S_loc, nch;  // nch = chunks per row
-  int norm_mode, zero_fill;
+  int norm_mode, zero_fill, ratio_level;
   const int64_t* step_tok_off;
   const uint8_t* keep;   // [S] global
   const void* norm;      // dart_norm*

@@ -31,7 +31,8 @@ STATUS_BITS = {
     1 << 0: "NONFINITE_LOGIT", 1 << 1: "TARGET_RANGE", 1 << 2: "ROW_ALL_NEGINF",
     1 << 3: "NONFINITE_LOGP", 1 << 4: "EMPTY", 1 << 5: "BAD_CSR", 1 << 6: "TARGET_NEGINF",
 }
-ABI_VERSION = 1
+ABI_VERSION = 2
+RATIO_TOKEN, RATIO_STEP = 0, 1
 
 
 class dart_cfg(ctypes.Structure):
@@ -39,7 +40,7 @@ class dart_cfg(ctypes.Structure):
                 ("beta_kl", ctypes.c_float), ("entropy_q", ctypes.c_float),
                 ("inv_temperature", ctypes.c_float), ("adv_eps", ctypes.c_float),
                 ("norm_mode", ctypes.c_int32), ("select_rule", ctypes.c_int32),
-                ("zero_fill_masked", ctypes.c_int32)]
+                ("zero_fill_masked", ctypes.c_int32), ("ratio_level", ctypes.c_int32)]
 
 
 class dart_meta(ctypes.Structure):
@@ -154,11 +155,12 @@ class Config:
     norm_mode: int = NORM_TOKEN_MEAN_KEPT
     select_rule: int = SEL_FLOOR
     zero_fill_masked: int = 1
+    ratio_level: int = RATIO_TOKEN
 
     def c(self):
         return dart_cfg(self.eps_low, self.eps_high, self.is_cap, self.beta_kl, self.entropy_q,
                         self.inv_temperature, self.adv_eps, self.norm_mode, self.select_rule,
-                        self.zero_fill_masked)
+                        self.zero_fill_masked, self.ratio_level)
 
     def as_f32(self):
         """The values the library actually sees (float32-rounded), for the oracle."""

@@ -46,7 +46,8 @@ def test_sm100a_cubin_inside():
 
 
 def test_version_and_status_strings(L):
-    assert L.dart_abi_version() == 1
+    from paper_2509_23866_b200 import dart
+    assert L.dart_abi_version() == dart.ABI_VERSION == 2
     for c in range(5):
         assert L.dart_status_str(c).startswith(b"DART_")
     assert L.dart_status_str(99) == b"DART_UNKNOWN_STATUS"
@@ -86,7 +87,8 @@ def test_invalid_arguments_rejected_without_launch(L):
     b = dart.dart_batch.from_buffer_copy(batch); b.logp_ref = None          # beta > 0 needs logp_ref
     assert _fwd(L, dart, cfg, meta, b, out) == E
     for field, val in (("eps_low", 0.0), ("eps_high", 1.0), ("is_cap", 0.0), ("beta_kl", -1.0),
-                       ("entropy_q", 1.0), ("inv_temperature", 0.0), ("norm_mode", 9), ("select_rule", -1)):
+                       ("entropy_q", 1.0), ("inv_temperature", 0.0), ("norm_mode", 9), ("select_rule", -1),
+                       ("ratio_level", 2)):
         c = dart.dart_cfg.from_buffer_copy(cfg)
         setattr(c, field, val)
         assert _fwd(L, dart, c, meta, batch, out) == E, field

@@ -413,10 +413,11 @@ def _random_batch(rng, V, G=2, beta=0.1):
 @pytest.mark.parametrize("mode", [O.NORM_TOKEN_MEAN_KEPT, O.NORM_STEP_MEAN_KEPT, O.NORM_SUM,
                                   O.NORM_TOKEN_MEAN_ALL, O.NORM_STEP_MEAN_ALL])
 @pytest.mark.parametrize("invT", [1.0, 0.7])
-def test_p10_finite_differences(mode, invT):
+@pytest.mark.parametrize("ratio", [O.RATIO_TOKEN, O.RATIO_STEP])
+def test_p10_finite_differences(mode, invT, ratio):
     rng = np.random.default_rng(10 + mode)
     b = _random_batch(rng, V=7)
-    cfg = dict(entropy_q=0.3, beta_kl=0.1, is_cap=1.0, norm_mode=mode, inv_temperature=invT)
+    cfg = dict(entropy_q=0.3, beta_kl=0.1, is_cap=1.0, norm_mode=mode, inv_temperature=invT, ratio_level=ratio)
     out = O.loss_pass(b, cfg)
     keep = out["keep"]
     h = 1e-6
@@ -465,6 +466,56 @@ def test_p10_gradient_matches_torch_autograd():
         assert abs(L.item() - out["loss"]) < 1e-13
         for t, dz in out["dz"].items():
             assert np.allclose(z.grad[t].numpy(), dz, rtol=1e-12, atol=1e-15), (trial, t)
+
+
+def test_step_ratio_gradient_matches_torch_autograd():
+    """Step-level ratio: autograd of an independent float64
+    torch expression with per-step sequence log-ratios."""
+    rng = np.random.default_rng(21)
+    for trial in range(5):
+        b = _random_batch(rng, V=int(rng.integers(3, 30)), G=3)
+        cfg = dict(entropy_q=0.2, beta_kl=float(rng.choice([0.0, 0.1])), is_cap=float(rng.choice([1.0, 2.0])),
+                   ratio_level=O.RATIO_STEP, norm_mode=int(rng.integers(0, 5)))
+        out = O.loss_pass(b, cfg)
+        c = {**O.DEFAULT_CFG, **cfg}
+        z = torch.tensor(b["logits"], dtype=torch.float64, requires_grad=True)
+        logp = torch.log_softmax(z, -1).gather(1, torch.tensor(b["target"])[:, None])[:, 0]
+        lo, lr, lref = (torch.tensor(b[k]) for k in ("logp_old", "logp_rollout", "logp_ref"))
+        off = b["step_tok_off"]
+        L = torch.zeros((), dtype=torch.float64)
+        c_step = O.step_weights(out["keep"], off, c["norm_mode"], per_step_loss=True)
+        for s_ in range(len(off) - 1):
+            sl = slice(off[s_], off[s_ + 1])
+            A = float(out["A_tok"][off[s_]])
+            r = torch.exp(torch.sum(logp[sl] - lo[sl]))
+            w = torch.clamp(torch.exp(torch.sum(lo[sl] - lr[sl])), max=c["is_cap"])
+            sur = torch.minimum(r * A, torch.clamp(r, 1 - c["eps_low"], 1 + c["eps_high"]) * A)
+            d = lref[sl] - logp[sl]
+            L = L + c_step[s_] * (-w * sur + c["beta_kl"] * torch.sum(torch.exp(d) - d - 1))
+        L.backward()
+        assert abs(L.item() - out["loss"]) < 1e-13 * max(1.0, abs(L.item()))
+        for t, dz in out["dz"].items():
+            assert np.allclose(z.grad[t].numpy(), dz, rtol=1e-11, atol=1e-15), (trial, t)
+
+
+def test_step_ratio_p9_closed_form(golden):
+    """P9 example in step-ratio mode: step 0 = {t0, t1} of the success
+    (A = sqrt2): log r = -0.1 + 0.3 = 0.2 (inside the clip range), log w =
+    0 - 0.5; step 1 = {t2} (A = -1/sqrt2): r = 1, w = min(e^0.2, 1) = 1;
+    step 2 masked (q = 0.5)."""
+    g = golden("p9_worked_example.json")
+    run = g["run"]
+    b = _p9_batch(g, run["d_old"], run["d_roll"])
+    l0 = -math.exp(-0.5) * math.exp(0.2) * math.sqrt(2)
+    l1 = 1 / math.sqrt(2)
+    out = O.loss_pass(b, dict(entropy_q=run["q"], beta_kl=0.0, is_cap=1.0, ratio_level=O.RATIO_STEP))
+    assert abs(out["loss"] - (l0 + l1) / 3) < 1e-14              # token-mean: N_keep_tok = 3
+    out = O.loss_pass(b, dict(entropy_q=run["q"], beta_kl=0.0, is_cap=1.0, ratio_level=O.RATIO_STEP,
+                              norm_mode=O.NORM_STEP_MEAN_KEPT))
+    assert abs(out["loss"] - (l0 + l1) / 2) < 1e-14              # step-mean: N_keep_step = 2
+    # every token of step 0 gets the same surrogate gradient -w A r
+    assert abs(out["dell"][0] - out["dell"][1]) < 1e-15
+    assert abs(out["dell"][0] - (-math.exp(-0.5) * math.sqrt(2) * math.exp(0.2))) < 1e-14
 
 
 def test_p11_uniform_row_gradient():

@@ -210,3 +210,85 @@ def test_single_config_full_size_sampled():
     ell_all = dl.ell.cpu().numpy().astype(np.float64)
     L_chk = np.sum(ell_all[tok_keep]) * nd["inv_norm"]
     assert abs(st["loss"] - L_chk) <= 1e-9 * np.sum(np.abs(ell_all[tok_keep])) * nd["inv_norm"] + 1e-15
+
+
+def test_all_groups_skipped_gives_zero_loss_and_grads():
+    b = synth.make_batch("small_multi", seed=5)
+    b.layout.traj_reward = np.ones_like(b.layout.traj_reward)      # sigma_R = 0 everywhere (SURVEY Q9)
+    cfg = dart.Config()
+    dl = run_gpu(b, cfg)
+    dl.check_status()
+    assert int(dl.group_ok[:b.layout.G].sum()) == 0
+    assert int(dl.keep[:b.layout.S].sum()) == 0
+    nd = dl.norm_dict()
+    assert nd["n_keep_tok"] == 0 and nd["inv_norm"] == 0.0
+    assert dl.stats_dict()["loss"] == 0.0
+    assert torch.count_nonzero(dl.dlogits) == 0
+    compare(dl, b, cfg)
+
+
+@pytest.mark.parametrize("q", [0.0, 0.5, 0.99])
+def test_single_step_groups_and_extreme_q(q):
+    # every trajectory has one step; groups of 1..3 trajectories (n = 1 -> kept)
+    layout, _, _, _ = synth.config_layout("grid6x3x1x5@700", seed=2)
+    b = synth.make_batch("grid", seed=2, layout=layout, V=700, dtype=torch.float32, real_reward=True)
+    cfg = dart.Config(entropy_q=q)
+    dl = run_gpu(b, cfg)
+    dl.check_status()
+    compare(dl, b, cfg)
+
+
+def test_virtual_rank_with_empty_shard():
+    """More ranks than trajectories: some shards are empty (T_loc = 0)."""
+    from paper_2509_23866_b200 import dist as D
+    b = synth.make_batch("tiny", seed=1)
+    cfg = dart.Config(is_cap=2.0)
+    ref = run_gpu(b, cfg)
+    shards = D.shard_layout(b.layout, 6)              # 4 trajectories over 6 ranks
+    assert any(s.T_loc == 0 for s in shards)
+    dev = torch.device("cuda")
+    dls = []
+    for sh in shards:
+        dl = dart.DartLoss(b.layout, sh, b.V, cfg, dev, logits_dtype=torch.float32, grad_dtype=torch.float32,
+                           group=False, world_shards=shards)
+        sl = slice(sh.tok_begin, sh.tok_end)
+        dl.forward(b.logits[sl].to(dev).contiguous(), b.target[sl].to(dev).contiguous(),
+                   b.logp_old[sl].to(dev).contiguous(), b.logp_rollout[sl].to(dev).contiguous(),
+                   b.logp_ref[sl].to(dev).contiguous())
+        dls.append(dl)
+    gathered = torch.zeros(len(shards) * dls[0].S_pad, device=dev)
+    for r, (dl, sh) in enumerate(zip(dls, shards)):
+        gathered[r * dls[0].S_pad: r * dls[0].S_pad + sh.S_loc] = dl.step_H[:sh.S_loc]
+    loss = 0.0
+    for dl, sh in zip(dls, shards):
+        dl.set_gathered(gathered)
+        dl.select()
+        dl.backward()
+    torch.cuda.synchronize()
+    for dl, sh in zip(dls, shards):
+        dl.check_status()
+        assert torch.equal(dl.keep[:b.layout.S], ref.keep[:b.layout.S])
+        if sh.T_loc:
+            assert torch.equal(dl.dlogits, ref.dlogits[sh.tok_begin:sh.tok_end])
+        loss += dl.stats_dict()["loss"]
+    assert abs(loss - ref.stats_dict()["loss"]) <= 1e-12 * abs(ref.stats_dict()["loss"]) + 1e-15
+
+
+@pytest.mark.parametrize("norm", NORMS)
+@pytest.mark.parametrize("beta", [0.0, 0.1])
+def test_step_level_ratio(norm, beta):
+    """SURVEY §8(f) #2: step-level (sequence) ratio and IS weight."""
+    b = synth.make_batch("small_multi", seed=6, real_reward=True)
+    cfg = dart.Config(ratio_level=dart.RATIO_STEP, norm_mode=norm, beta_kl=beta, is_cap=1.5)
+    dl = run_gpu(b, cfg)
+    dl.check_status()
+    compare(dl, b, cfg)
+
+
+def test_step_level_ratio_mid():
+    b = synth.make_batch("mid", seed=2)
+    cfg = dart.Config(ratio_level=dart.RATIO_STEP)
+    dl = run_gpu(b, cfg)
+    dl.check_status()
+    rng = np.random.default_rng(3)
+    compare(dl, b, cfg, rows=sorted(rng.choice(b.layout.T, 12, replace=False).tolist()))
