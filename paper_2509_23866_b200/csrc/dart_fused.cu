@@ -1,0 +1,489 @@
+// dart_fused.cu -- SURVEY §8(f) NEXT #1: single-read fused loss + gradient
+// when the step mask is known in advance (sm_100a).
+//
+// In a verl-style trainer the old-policy pass (a no-grad forward of theta_old,
+// which Eq. 1's denominator needs anyway) can run
+// dart_loss_fwd + dart_select_steps and so fix the high-entropy mask
+// before the update pass.  The update pass then needs, per kept
+// row, only lse (for log pi(y) and p) and the gradient: one read of the row
+// from HBM and one write of its gradient -- 4V bytes instead of 6V.
+//
+// K7 fused_sweep: one CTA per row at a time.  A producer warp streams every
+// kept row twice through a shared ring of 4 KB bulk-copy slots: pass 1
+// (evict-last L2 policy) feeds the online max / sum, pass 2 (evict-first)
+// feeds the gradient.  Pass 2 re-reads the row about one row-time later,
+// while it is still resident in the 126 MB L2 (148 CTAs x ~2 rows in flight
+// ~ 90 MB), so HBM sees each kept row read once.  Consumer warp w takes the
+// chunks j = w, w + NC, ... of each pass (a per-row order, so results do not
+// depend on how rows are distributed); the row reduction is a fixed fold over
+// the consumer warps.  Rows of masked steps are written as zeros, unread.
+#include "dart_common.cuh"
+#include "dart_internal.h"
+
+namespace dart {
+
+#ifndef DART_FU_NC
+#define DART_FU_NC 8
+#endif
+#ifndef DART_FU_SW
+#define DART_FU_SW 3
+#endif
+#ifndef DART_FU_CTAS
+#define DART_FU_CTAS 2
+#endif
+// two CTAs per SM (each 8 consumer warps + 1 producer, 96 KB ring): while one
+// CTA sits in its row barrier / epilogue / L2-fed pass 2, the other streams
+// its next row from HBM
+constexpr int FU_NC = DART_FU_NC;         // consumer warps
+constexpr int FU_SW = DART_FU_SW;         // ring slots per consumer warp
+constexpr int FU_SLOTS = FU_NC * FU_SW;   // ring slots of CH_BYTES
+// Each consumer warp owns FU_SW slots: a warp then never waits on a slot more
+// than one phase ahead of the producer (a shared ring let a fast warp alias
+// an older mbarrier phase -- parity waits -- and read stale data).
+constexpr int FU_THREADS = (FU_NC + 1) * 32;
+
+struct FusedShared {
+  uint64_t full[FU_SLOTS];
+  uint64_t empty[FU_SLOTS];
+  double part_s[2][FU_NC];
+  float part_m[2][FU_NC];
+  float row_g[2], row_nl2[2];
+};
+
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void named_bar_sync(int id, int count) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
+}
+
+template <typename Tin>
+__device__ __forceinline__ void unpack(const uint4& xv, float* z) {
+  const uint32_t* w = reinterpret_cast<const uint32_t*>(&xv);
+  if (sizeof(Tin) == 2) {
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      z[2 * j] = bf16lo(w[j]);
+      z[2 * j + 1] = bf16hi(w[j]);
+    }
+  } else {
+#pragma unroll
+    for (int j = 0; j < 4; ++j) z[j] = __uint_as_float(w[j]);
+  }
+}
+
+template <typename Tin>
+__device__ __forceinline__ float load_logit_g(const uint8_t* row, int64_t y) {
+  if (sizeof(Tin) == 2) return __uint_as_float(((uint32_t)(*reinterpret_cast<const uint16_t*>(row + 2 * y))) << 16);
+  return *reinterpret_cast<const float*>(row + 4 * y);
+}
+
+// first local row whose start cost is >= x (costs per step: kept 2, masked 1 or 0)
+__device__ __forceinline__ int64_t fu_row_at_cost(const FusedParams& p, int64_t x) {
+  const int64_t total = p.step_cost[p.S_loc];
+  if (x >= total) return p.T_loc;
+  const int64_t s = upper_bound_i64(p.step_cost, 0, p.S_loc + 1, x) - 1;
+  const int64_t sg = p.step_begin + s;
+  const int64_t t0 = p.step_tok_off[sg] - p.tok_begin, t1 = p.step_tok_off[sg + 1] - p.tok_begin;
+  const int64_t per_row = (p.keep[sg] ? 2 : 1) * p.nch;
+  const int64_t off = (x - p.step_cost[s] + per_row - 1) / per_row;
+  return min(t0 + off, t1);
+}
+
+// 32-byte per-row record, built by fused_rec_kernel before the sweep: every
+// per-token input the row epilogue needs that does not depend on lse, so the
+// epilogue itself is a handful of float ops on prefetched registers.
+struct __align__(16) FusedRec {
+  int32_t y;        // target (-1 if out of range)
+  float zy;         // z_{t,y}
+  float lo;         // logp_old
+  float w;          // truncated IS weight min(exp(lo - lr), C)
+  float A;          // advantage of the row's trajectory
+  float lref;       // logp_ref (0 if beta == 0)
+  float c;          // per-step loss weight c_s (0: masked step)
+  uint32_t flags;   // bit0 kept step, bit1 truncated (ratio >= C), bits 8.. status bits
+};
+
+__global__ void fused_rec_kernel(FusedParams p, FusedRec* rec) {
+  const int64_t nthreads = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < p.T_loc; t += nthreads) {
+    FusedRec r;
+    uint32_t bits = 0;
+    const int32_t y = p.target[t];
+    const uint8_t* row = p.logits + t * p.ld_bytes;
+    if (y < 0 || y >= p.V) { bits |= DART_STATUS_TARGET_RANGE; r.y = -1; r.zy = __int_as_float(0x7fc00000); }
+    else { r.y = y; r.zy = p.is_bf16 ? load_logit_g<__nv_bfloat16>(row, y) : load_logit_g<float>(row, y); }
+    if (r.zy == -INFINITY) bits |= DART_STATUS_TARGET_NEGINF;
+    const double lo = p.logp_old[t], lr = p.logp_roll[t];
+    const double lref = (p.beta != 0.0) ? (double)p.logp_ref[t] : 0.0;
+    if (!isfinite(lo) || !isfinite(lr) || !isfinite(lref)) bits |= DART_STATUS_NONFINITE_LOGP;
+    const double ratio = exp(lo - lr);
+    r.lo = (float)lo;
+    r.w = (float)fmin(ratio, p.is_cap);
+    r.A = p.tok_adv[t];
+    r.lref = (float)lref;
+    const int32_t sl = p.tok_step[t];
+    const bool kept = p.keep[p.step_begin + sl] != 0;
+    r.c = (float)p.step_scale[sl];
+    r.flags = (kept ? 1u : 0u) | (ratio >= p.is_cap ? 2u : 0u) | (kept ? (bits << 8) : 0u);
+    reinterpret_cast<FusedRec*>(rec)[t] = r;
+  }
+}
+
+// row epilogue (token-level ratio): writes the
+// per-token outputs and returns g = c_s * dell * invT
+__device__ float fused_epilogue(const FusedParams& p, int64_t t, const FusedRec& rc, double Mr, double L2s) {
+  uint32_t bits = rc.flags >> 8;
+  if (Mr <= (double)(NEG_CLAMP * p.c2)) bits |= DART_STATUS_ROW_ALL_NEGINF;
+  const double lse2 = Mr + L2s;
+  const float logp = (float)(((double)rc.zy * (double)p.c2 - Mr - L2s) * LN2_D);
+  const float r = expf(logp - rc.lo);
+  const float A = rc.A;
+  const float lo_c = (float)(1.0 - p.eps_low), hi_c = (float)(1.0 + p.eps_high);
+  const float rcl = fminf(fmaxf(r, lo_c), hi_c);
+  const float sur = fminf(r * A, rcl * A);
+  const bool act = (A > 0.f) ? (r <= hi_c) : ((A < 0.f) ? (r >= lo_c) : true);
+  float kl = 0.f, dkl = 0.f;
+  if (p.beta != 0.0) {
+    const float d = rc.lref - logp;
+    const float ed = expf(d);
+    kl = (ed - d) - 1.f;
+    dkl = 1.f - ed;
+  }
+  const float beta = (float)p.beta;
+  const float ell = -rc.w * sur + beta * kl;
+  const float dell = -rc.w * (act ? A * r : 0.f) + beta * dkl;
+  p.lse[t] = (float)(lse2 * LN2_D);
+  p.logp[t] = logp;
+  p.ell[t] = ell;
+  p.dell[t] = dell;
+  p.aux_w[t] = rc.w;
+  p.aux_kl[t] = kl;
+  p.aux_flags[t] = (uint8_t)((act ? 0u : 1u) | (rc.flags & 2u));
+  status_or(p.status, bits);
+  return rc.c * dell * (float)p.invT;
+}
+
+template <typename Tin, typename Tout>
+__global__ void __launch_bounds__(FU_THREADS, DART_FU_CTAS) fused_sweep_kernel(const FusedParams p) {
+  extern __shared__ __align__(128) uint8_t smem[];
+  uint8_t* ring = smem;
+  FusedShared& sh = *reinterpret_cast<FusedShared*>(smem + (size_t)FU_SLOTS * CH_BYTES);
+  constexpr int EPV = 16 / sizeof(Tin);
+  constexpr bool OUT_BF16 = sizeof(Tout) == 2;
+  constexpr int64_t OUTV = EPV * (int64_t)sizeof(Tout);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < FU_SLOTS; ++s) {
+      mbar_init(&sh.full[s], 1);
+      mbar_init(&sh.empty[s], FU_NC > 0 ? 1 : 1);
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
+
+  // this CTA's contiguous, cost-balanced row range [ra, rb)
+  const int64_t total = p.step_cost[p.S_loc];
+  const int64_t nb = gridDim.x;
+  const int64_t ra = fu_row_at_cost(p, (total * (int64_t)blockIdx.x) / nb);
+  const int64_t rb = fu_row_at_cost(p, (total * ((int64_t)blockIdx.x + 1)) / nb);
+  const int64_t nvec = p.nvec, nch = p.nch;
+  const float c2 = p.c2;
+  const int tail_elems = (int)(p.V % EPV);
+
+  if (warp == FU_NC) {
+    // ===================== producer (one lane) =====================
+    if (lane == 0) {
+      uint64_t pol_last, pol_first;
+      asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol_last));
+      asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol_first));
+      int64_t nrow = 0;   // kept rows issued so far
+      for (int64_t t = ra; t < rb; ++t) {
+        if (!(reinterpret_cast<const FusedRec*>(p.rec)[t].flags & 1u)) continue;
+        const uint8_t* row = p.logits + t * p.ld_bytes;
+        for (int pass = 0; pass < 2; ++pass) {
+          for (int64_t j = 0; j < nch; ++j) {
+            const int w = (int)(j % FU_NC);
+            const int64_t cw = (nch - w + FU_NC - 1) / FU_NC;          // chunks of warp w per pass
+            const int64_t idx = (2 * nrow + pass) * cw + j / FU_NC;      // warp w's chunk ordinal
+            const int slot = w * FU_SW + (int)(idx % FU_SW);
+            const uint32_t use = (uint32_t)(idx / FU_SW);
+            if (use > 0) mbar_wait(&sh.empty[slot], (use - 1) & 1u);
+            const int64_t v0 = j * CH_VEC;
+            const uint32_t nv = (uint32_t)min((int64_t)CH_VEC, nvec - v0);
+            mbar_arrive_expect_tx(&sh.full[slot], nv * 16u);
+            bulk_g2s_hint(ring + (size_t)slot * CH_BYTES, row + v0 * 16, nv * 16u, &sh.full[slot],
+                          pass == 0 ? pol_last : pol_first);
+          }
+        }
+        ++nrow;
+      }
+    }
+    return;
+  }
+
+  // ===================== consumers (FU_NC warps) =====================
+  const FusedRec* recs = reinterpret_cast<const FusedRec*>(p.rec);
+  const int64_t cw = (nch - warp + FU_NC - 1) / FU_NC;   // this warp's chunks per pass
+  int64_t nrow = 0;  // kept rows consumed so far
+  int par = 0;       // mailbox parity
+  FusedRec nxt;
+  if (ra < rb) nxt = recs[ra];
+  for (int64_t t = ra; t < rb; ++t) {
+    const FusedRec rc = nxt;
+    if (t + 1 < rb) nxt = recs[t + 1];      // prefetch: hidden behind this row
+    uint8_t* orow = p.dlogits + t * p.ldg_bytes;
+    if (!(rc.flags & 1u)) {
+      if (!p.zero_fill) continue;
+      // masked step: zeros, no read; consumer warps split the row
+      for (int64_t vi = (int64_t)warp * 32 + lane; vi < nvec; vi += FU_NC * 32) {
+        const int nvalid = (tail_elems && vi == nvec - 1) ? tail_elems : EPV;
+        uint8_t* dst = orow + vi * OUTV;
+        if (nvalid == EPV) {
+          if (OUT_BF16 && EPV == 8) stg128_cs(dst, make_uint4(0u, 0u, 0u, 0u));
+          else if (OUT_BF16) *reinterpret_cast<uint2*>(dst) = make_uint2(0u, 0u);
+          else
+            for (int e = 0; e < EPV; e += 4) stg128_cs(dst + 4 * e, make_uint4(0u, 0u, 0u, 0u));
+        } else {
+          for (int e = 0; e < nvalid; ++e) {
+            if (OUT_BF16) reinterpret_cast<__nv_bfloat16*>(dst)[e] = __float2bfloat16_rn(0.f);
+            else reinterpret_cast<float*>(dst)[e] = 0.f;
+          }
+        }
+      }
+      continue;
+    }
+    // ---------------- pass 1: online max / sum over this warp's chunks
+    float m = NEG_CLAMP * c2;
+    float2 s01 = make_float2(0.f, 0.f), s23 = make_float2(0.f, 0.f);
+    uint32_t bad = 0;
+    for (int64_t j = warp; j < nch; j += FU_NC) {
+      const int64_t idx = 2 * nrow * cw + j / FU_NC;
+      const int slot = warp * FU_SW + (int)(idx % FU_SW);
+      mbar_wait(&sh.full[slot], (uint32_t)((idx / FU_SW) & 1));
+      const uint8_t* sp = ring + (size_t)slot * CH_BYTES;
+      const int64_t v0 = j * CH_VEC;
+      const int nv = (int)min((int64_t)CH_VEC, nvec - v0);
+      uint4 x[VPL];
+#pragma unroll
+      for (int q = 0; q < VPL; ++q) {
+        const int vi = lane + 32 * q;
+        x[q] = (vi < nv) ? lds128(sp + vi * 16) : make_uint4(0u, 0u, 0u, 0u);
+      }
+      uint32_t dep = 0;
+#pragma unroll
+      for (int q = 0; q < VPL; ++q) dep |= x[q].x | x[q].y | x[q].z | x[q].w;
+      asm volatile("" ::"r"(dep));
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&sh.empty[slot]);   // slot back to the producer
+      const bool tail_chunk = tail_elems && v0 + nv == nvec;
+      if (sizeof(Tin) == 2 && nv == CH_VEC && !tail_chunk) {
+        // fast path: packed bf16x2 max, one unpack per pair; -inf logits give
+        // 2^-inf = 0 and there is no 0*inf term (no entropy in this pass)
+        uint32_t mx = 0xff80ff80u;
+#pragma unroll
+        for (int q = 0; q < VPL; ++q) {
+          mx = bmax2_nan(mx, x[q].x);
+          mx = bmax2_nan(mx, x[q].y);
+          mx = bmax2_nan(mx, x[q].z);
+          mx = bmax2_nan(mx, x[q].w);
+        }
+        const float cmr = fmax_nan(bf16lo(mx), bf16hi(mx));
+        if (!(cmr < INFINITY)) bad |= DART_STATUS_NONFINITE_LOGIT;
+        const float cms = cmr * c2;
+        if (cms > m + 2.0f) {   // lazy running max (LAZY_M = 2, as in the fwd sweep)
+          const float sc = ex2(m - cms);
+          s01 = __fmul2_rn(s01, make_float2(sc, sc));
+          s23 = __fmul2_rn(s23, make_float2(sc, sc));
+          m = cms;
+        }
+        const float2 cc = make_float2(c2, c2), nm = make_float2(-m, -m);
+#pragma unroll
+        for (int q = 0; q < VPL; ++q) {
+          const float2 d0 = __ffma2_rn(make_float2(bf16lo(x[q].x), bf16hi(x[q].x)), cc, nm);
+          const float2 d1 = __ffma2_rn(make_float2(bf16lo(x[q].y), bf16hi(x[q].y)), cc, nm);
+          const float2 d2 = __ffma2_rn(make_float2(bf16lo(x[q].z), bf16hi(x[q].z)), cc, nm);
+          const float2 d3 = __ffma2_rn(make_float2(bf16lo(x[q].w), bf16hi(x[q].w)), cc, nm);
+          s01 = __fadd2_rn(s01, make_float2(ex2(d0.x), ex2(d0.y)));
+          s23 = __fadd2_rn(s23, make_float2(ex2(d1.x), ex2(d1.y)));
+          s01 = __fadd2_rn(s01, make_float2(ex2(d2.x), ex2(d2.y)));
+          s23 = __fadd2_rn(s23, make_float2(ex2(d3.x), ex2(d3.y)));
+        }
+        continue;
+      }
+      float cm = -INFINITY;
+#pragma unroll
+      for (int q = 0; q < VPL; ++q) {
+        const int vi = lane + 32 * q;
+        if (vi < nv) {
+          float z[EPV];
+          unpack<Tin>(x[q], z);
+#pragma unroll
+          for (int e = 0; e < EPV; ++e) {
+            if (tail_chunk && vi == nv - 1 && e >= tail_elems) z[e] = NEG_CLAMP;
+            cm = fmax_nan(cm, z[e]);
+          }
+        }
+      }
+      if (!(cm < INFINITY)) bad |= DART_STATUS_NONFINITE_LOGIT;
+      const float cms = fmaxf(cm, NEG_CLAMP) * c2;
+      if (cms > m + 2.0f) {
+        const float sc = ex2(m - cms);
+        s01 = __fmul2_rn(s01, make_float2(sc, sc));
+        s23 = __fmul2_rn(s23, make_float2(sc, sc));
+        m = cms;
+      }
+      const float2 cc = make_float2(c2, c2), nm = make_float2(-m, -m);
+#pragma unroll
+      for (int q = 0; q < VPL; ++q) {
+        const int vi = lane + 32 * q;
+        if (vi < nv) {
+          float z[EPV];
+          unpack<Tin>(x[q], z);
+#pragma unroll
+          for (int e = 0; e < EPV; ++e) {
+            if (tail_chunk && vi == nv - 1 && e >= tail_elems) z[e] = NEG_CLAMP;
+            z[e] = fmaxf(z[e], NEG_CLAMP);   // -inf logits contribute exp -> 0
+          }
+#pragma unroll
+          for (int e = 0; e < EPV; e += 4) {
+            const float2 d0 = __ffma2_rn(make_float2(z[e], z[e + 1]), cc, nm);
+            const float2 d1 = __ffma2_rn(make_float2(z[e + 2], z[e + 3]), cc, nm);
+            s01 = __fadd2_rn(s01, make_float2(ex2(d0.x), ex2(d0.y)));
+            s23 = __fadd2_rn(s23, make_float2(ex2(d1.x), ex2(d1.y)));
+          }
+        }
+      }
+    }
+    // warp partial (fixed lane fold) -> mailbox
+    {
+      const float M = warp_max_f(m);
+      const float sl = (s01.x + s01.y) + (s23.x + s23.y);
+      const double sd = warp_sum_d((double)sl * (double)ex2(m - M));
+      bad = warp_or(bad);
+      if (lane == 0) {
+        sh.part_m[par][warp] = M;
+        sh.part_s[par][warp] = sd;
+        if (bad) status_or(p.status, bad);
+      }
+    }
+    named_bar_sync(1, FU_NC * 32);
+    // ---------------- row epilogue (warp 0), broadcast through shared memory
+    if (warp == 0 && lane == 0) {
+      double Mr = -INFINITY, Sr = 0.0;
+      for (int w = 0; w < FU_NC; ++w) {        // fixed fold over the consumer warps
+        const double Mw = (double)sh.part_m[par][w];
+        const double Sw = sh.part_s[par][w];
+        if (Sw == 0.0) continue;
+        if (Mr == -INFINITY) { Mr = Mw; Sr = Sw; continue; }
+        const double mn = fmax(Mr, Mw);
+        Sr = Sr * (double)ex2((float)(Mr - mn)) + Sw * (double)ex2((float)(Mw - mn));
+        Mr = mn;
+      }
+      const double L2s = log2(Sr);
+      sh.row_g[par] = fused_epilogue(p, t, rc, Mr, L2s);
+      sh.row_nl2[par] = (float)(-(Mr + L2s));
+    }
+    named_bar_sync(1, FU_NC * 32);
+    const float g = sh.row_g[par], nl2 = sh.row_nl2[par];
+    const int32_t y = rc.y;
+    const float zy = rc.zy;
+    // ---------------- pass 2: gradient over this warp's chunks
+    const float2 cc2 = make_float2(c2, c2), nl = make_float2(nl2, nl2), ng = make_float2(-g, -g);
+    for (int64_t j = warp; j < nch; j += FU_NC) {
+      const int64_t idx = (2 * nrow + 1) * cw + j / FU_NC;
+      const int slot = warp * FU_SW + (int)(idx % FU_SW);
+      mbar_wait(&sh.full[slot], (uint32_t)((idx / FU_SW) & 1));
+      const uint8_t* sp = ring + (size_t)slot * CH_BYTES;
+      const int64_t v0 = j * CH_VEC;
+      const int nv = (int)min((int64_t)CH_VEC, nvec - v0);
+      uint4 x[VPL];
+#pragma unroll
+      for (int q = 0; q < VPL; ++q) {
+        const int vi = lane + 32 * q;
+        x[q] = (vi < nv) ? lds128(sp + vi * 16) : make_uint4(0u, 0u, 0u, 0u);
+      }
+      uint32_t dep = 0;
+#pragma unroll
+      for (int q = 0; q < VPL; ++q) dep |= x[q].x | x[q].y | x[q].z | x[q].w;
+      asm volatile("" ::"r"(dep));
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&sh.empty[slot]);
+#pragma unroll
+      for (int q = 0; q < VPL; ++q) {
+        const int vi = lane + 32 * q;
+        if (vi < nv) {
+          const int64_t gv = v0 + vi;
+          float z[EPV], o[EPV];
+          unpack<Tin>(x[q], z);
+#pragma unroll
+          for (int e = 0; e < EPV; e += 2) {
+            const float2 d = __ffma2_rn(make_float2(z[e], z[e + 1]), cc2, nl);
+            const float2 dz = __fmul2_rn(make_float2(ex2(d.x), ex2(d.y)), ng);
+            o[e] = dz.x;
+            o[e + 1] = dz.y;
+          }
+          const int nvalid = (tail_elems && gv == nvec - 1) ? tail_elems : EPV;
+          uint8_t* dst = orow + gv * OUTV;
+          if (nvalid == EPV) {
+            if (OUT_BF16 && EPV == 8) {
+              stg128_cs(dst, make_uint4(pack_bf16x2(o[0], o[1]), pack_bf16x2(o[2], o[3]), pack_bf16x2(o[4], o[5]),
+                                        pack_bf16x2(o[6], o[7])));
+            } else if (OUT_BF16) {
+              *reinterpret_cast<uint2*>(dst) = make_uint2(pack_bf16x2(o[0], o[1]), pack_bf16x2(o[2], o[3]));
+            } else {
+#pragma unroll
+              for (int e = 0; e < EPV; e += 4)
+                stg128_cs(dst + 4 * e, make_uint4(__float_as_uint(o[e]), __float_as_uint(o[e + 1]),
+                                                  __float_as_uint(o[e + 2]), __float_as_uint(o[e + 3])));
+            }
+          } else {
+            for (int e = 0; e < nvalid; ++e) {
+              if (OUT_BF16) reinterpret_cast<__nv_bfloat16*>(dst)[e] = __float2bfloat16_rn(o[e]);
+              else reinterpret_cast<float*>(dst)[e] = o[e];
+            }
+          }
+        }
+      }
+      // target element: g (1 - p_y), rewritten by its owning lane after the vector store
+      if (y >= 0 && y < p.V) {
+        const int64_t yv = y / EPV;
+        if (yv >= v0 && yv < v0 + nv && lane == (int)((yv - v0) & 31)) {
+          const float py = ex2(fmaf(zy, c2, nl2));
+          const float dzy = fmaf(-g, py, g);
+          if (OUT_BF16) reinterpret_cast<__nv_bfloat16*>(orow)[y] = __float2bfloat16_rn(dzy);
+          else reinterpret_cast<float*>(orow)[y] = dzy;
+        }
+      }
+    }
+    ++nrow;
+    par ^= 1;
+  }
+}
+
+cudaError_t launch_fused_rec(const FusedParams& p, cudaStream_t st) {
+  if (p.T_loc <= 0) return cudaSuccess;
+  int64_t blocks = (p.T_loc + 255) / 256;
+  if (blocks > 8192) blocks = 8192;
+  fused_rec_kernel<<<(unsigned)blocks, 256, 0, st>>>(p, reinterpret_cast<FusedRec*>(p.rec));
+  return cudaGetLastError();
+}
+
+template <typename Tin, typename Tout>
+static cudaError_t launch_fused_t(const FusedParams& p, int num_sms, cudaStream_t st) {
+  const size_t smem = (size_t)FU_SLOTS * CH_BYTES + sizeof(FusedShared);
+  auto kern = fused_sweep_kernel<Tin, Tout>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  kern<<<(unsigned)(num_sms * DART_FU_CTAS), FU_THREADS, smem, st>>>(p);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_fused_sweep(const FusedParams& p, bool in_bf16, bool out_bf16, int num_sms, cudaStream_t st) {
+  if (in_bf16 && out_bf16) return launch_fused_t<__nv_bfloat16, __nv_bfloat16>(p, num_sms, st);
+  if (in_bf16) return launch_fused_t<__nv_bfloat16, float>(p, num_sms, st);
+  if (out_bf16) return launch_fused_t<float, __nv_bfloat16>(p, num_sms, st);
+  return launch_fused_t<float, float>(p, num_sms, st);
+}
+
+}  // namespace dart

@@ -584,10 +584,18 @@ __global__ void step_reduce_kernel(StepReduceParams p) {
     t0 = max(t0, (int64_t)0);
     t1 = min(t1, p.T_loc);
     const int64_t n = t1 - t0;
+    if (p.no_entropy && !p.keep[sg]) {   // fused mode: masked steps carry no per-token values
+      if (lane == 0) {
+        p.step_ell[s] = 0.0;
+        double* st = p.step_stats + s * NSTAT;
+        for (int i = 0; i < NSTAT; ++i) st[i] = 0.0;
+      }
+      continue;
+    }
     double sH = 0, sE = 0, sw = 0, sclip = 0, strunc = 0, sA = 0, sA2 = 0, skl = 0;
     double sdl = 0, sdw = 0;  // step ratio: sum(logp - logp_old), sum(logp_old - logp_roll)
     for (int64_t t = t0 + lane; t < t1; t += 32) {
-      sH += (double)p.H[t];
+      if (!p.no_entropy) sH += (double)p.H[t];
       sE += (double)p.ell[t];
       sw += (double)p.aux_w[t];
       const uint32_t f = p.aux_flags[t];
@@ -639,7 +647,8 @@ __global__ void step_reduce_kernel(StepReduceParams p) {
       strunc = trunc ? (double)n : 0.0;
     }
     if (lane == 0) {
-      p.step_entropy[s] = n > 0 ? (float)(sH / (double)n) : __int_as_float(0x7fc00000);
+      if (!p.no_entropy)
+        p.step_entropy[s] = n > 0 ? (float)(sH / (double)n) : __int_as_float(0x7fc00000);
       p.step_ell[s] = sE;
       double* st = p.step_stats + s * NSTAT;
       st[0] = sw; st[1] = sclip; st[2] = strunc; st[3] = sA; st[4] = sA2; st[5] = skl; st[6] = sH;

@@ -75,6 +75,9 @@ struct StepReduceParams {
   float* step_entropy;
   double* step_ell;
   double* step_stats;
+  // fused mode (dart_loss_fused): no entropy; steps with keep == 0 are skipped
+  int no_entropy;
+  const uint8_t* keep;  // [S] global, only read when no_entropy
   // step-level ratio (DART_RATIO_STEP)
   int ratio_level;
   const float *logp, *logp_old, *logp_roll, *logp_ref;
@@ -152,6 +155,30 @@ struct BwdParams {
   int zero_fill;
 };
 
+struct FusedParams {
+  const uint8_t* logits;
+  int64_t ld_bytes, V, T_loc, nvec, nch;
+  int is_bf16, zero_fill;
+  uint8_t* dlogits;
+  int64_t ldg_bytes;
+  float c2;
+  double invT, eps_low, eps_high, is_cap, beta;
+  const int32_t* target;
+  const float *logp_old, *logp_roll, *logp_ref, *tok_adv;
+  const int32_t* tok_step;
+  const double* step_scale;
+  const uint8_t* keep;          // [S] global
+  const int64_t* step_cost;     // [S_loc+1]
+  const int64_t* step_tok_off;  // global CSR
+  int64_t tok_begin, step_begin, S_loc;
+  float *lse, *logp, *ell, *dell, *aux_w, *aux_kl;
+  uint8_t* aux_flags;
+  uint32_t* status;
+  void* rec;                    // [T_loc] 32-byte row records (fused_rec_kernel)
+};
+
+cudaError_t launch_fused_rec(const FusedParams& p, cudaStream_t st);
+cudaError_t launch_fused_sweep(const FusedParams& p, bool in_bf16, bool out_bf16, int num_sms, cudaStream_t st);
 cudaError_t launch_adv(const AdvParams& p, cudaStream_t st);
 cudaError_t launch_tok_meta(const TokMetaParams& p, cudaStream_t st);
 cudaError_t launch_fwd_sweep(const FwdParams& p, bool bf16, int num_sms, cudaStream_t st);

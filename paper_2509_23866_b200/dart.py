@@ -70,7 +70,8 @@ STATS_FIELDS = ["loss", "n_tok", "n_kept_tok", "n_kept_step", "sum_clip", "sum_t
 
 _lib = None
 
-EXPORTED = ["dart_workspace_size", "dart_loss_fwd", "dart_select_steps", "dart_loss_bwd", "dart_loss_pass",
+EXPORTED = ["dart_workspace_size", "dart_loss_fwd", "dart_select_steps", "dart_loss_bwd", "dart_loss_fused",
+            "dart_loss_pass",
             "dart_status_str", "dart_abi_version", "dart_last_launch_count", "dart_set_timing_events"]
 
 
@@ -102,6 +103,10 @@ def lib():
     L.dart_loss_bwd.argtypes = [P(dart_batch), P(dart_meta), P(dart_cfg), P(dart_fwd_out), ctypes.c_void_p,
                                 ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64,
                                 ctypes.c_void_p, ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p]
+    L.dart_loss_fused.restype = ctypes.c_int
+    L.dart_loss_fused.argtypes = [P(dart_batch), P(dart_meta), P(dart_cfg), ctypes.c_void_p, ctypes.c_void_p,
+                                  P(dart_fwd_out), ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64,
+                                  ctypes.c_void_p, ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p]
     L.dart_loss_pass.restype = ctypes.c_int
     L.dart_loss_pass.argtypes = [P(dart_batch), P(dart_meta), P(dart_cfg), P(dart_fwd_out), ctypes.c_void_p,
                                  ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int32,
@@ -345,6 +350,26 @@ class DartLoss:
                                     _ptr(self.dlogits_store), gdt, self.ldg, _ptr(self.stats), _ptr(self.ws),
                                     self.ws_bytes, ctypes.c_void_p(st)))
         self.launches += self.L.dart_last_launch_count()
+
+    def fused(self, logits, target, logp_old, logp_roll, logp_ref=None, keep=None, norm=None, stream=None):
+        """single-read loss + gradient with a step mask
+        known in advance (default: this object's keep / norm, e.g. from an
+        earlier forward + select on the old-policy logits).  One HBM read of
+        each kept row instead of two."""
+        self._check_inputs(logits, target, logp_old, logp_roll, logp_ref)
+        st = (stream or torch.cuda.current_stream(self.device)).cuda_stream
+        keep = self.keep if keep is None else keep
+        norm = self.norm if norm is None else norm
+        b = self._batch(logits, target, logp_old, logp_roll, logp_ref if self.cfg.beta_kl > 0 else None)
+        self._inputs = (b, logits, target, logp_old, logp_roll, logp_ref)
+        gdt = DART_BF16 if self.grad_dtype == torch.bfloat16 else DART_F32
+        _check(self.L.dart_loss_fused(ctypes.byref(b), ctypes.byref(self.meta.c()), ctypes.byref(self.cfg.c()),
+                                      _ptr(keep), _ptr(norm), ctypes.byref(self._fwd_out()), _ptr(self.dlogits_store),
+                                      gdt, self.ldg, _ptr(self.stats), _ptr(self.ws), self.ws_bytes,
+                                      ctypes.c_void_p(st)))
+        self.launches += self.L.dart_last_launch_count()
+        self.reduce_stats()
+        return self.dlogits
 
     def reduce_stats(self):
         """C2: all-reduce(SUM) of the fp64 loss / statistics partials."""
