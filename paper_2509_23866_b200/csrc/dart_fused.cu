@@ -34,6 +34,12 @@ namespace dart {
 // two CTAs per SM (each 8 consumer warps + 1 producer, 96 KB ring): while one
 // CTA sits in its row barrier / epilogue / L2-fed pass 2, the other streams
 // its next row from HBM
+#ifndef DART_FU_REV
+#define DART_FU_REV 0      // 1: pass 2 walks the row backwards (freshest L2 lines first)
+#endif
+#ifndef DART_FU_P1LAST
+#define DART_FU_P1LAST 1   // pass-1 bulk copies with the L2 evict_last policy
+#endif
 constexpr int FU_NC = DART_FU_NC;         // consumer warps
 constexpr int FU_SW = DART_FU_SW;         // ring slots per consumer warp
 constexpr int FU_SLOTS = FU_NC * FU_SW;   // ring slots of CH_BYTES
@@ -202,18 +208,23 @@ __global__ void __launch_bounds__(FU_THREADS, DART_FU_CTAS) fused_sweep_kernel(c
         if (!(reinterpret_cast<const FusedRec*>(p.rec)[t].flags & 1u)) continue;
         const uint8_t* row = p.logits + t * p.ld_bytes;
         for (int pass = 0; pass < 2; ++pass) {
-          for (int64_t j = 0; j < nch; ++j) {
+          for (int64_t ji = 0; ji < nch; ++ji) {
+            const int64_t j = (DART_FU_REV && pass == 1) ? nch - 1 - ji : ji;
             const int w = (int)(j % FU_NC);
             const int64_t cw = (nch - w + FU_NC - 1) / FU_NC;          // chunks of warp w per pass
-            const int64_t idx = (2 * nrow + pass) * cw + j / FU_NC;      // warp w's chunk ordinal
+            const int64_t pos = (DART_FU_REV && pass == 1) ? cw - 1 - j / FU_NC : j / FU_NC;
+            const int64_t idx = (2 * nrow + pass) * cw + pos;            // warp w's chunk ordinal
             const int slot = w * FU_SW + (int)(idx % FU_SW);
             const uint32_t use = (uint32_t)(idx / FU_SW);
             if (use > 0) mbar_wait(&sh.empty[slot], (use - 1) & 1u);
             const int64_t v0 = j * CH_VEC;
             const uint32_t nv = (uint32_t)min((int64_t)CH_VEC, nvec - v0);
             mbar_arrive_expect_tx(&sh.full[slot], nv * 16u);
-            bulk_g2s_hint(ring + (size_t)slot * CH_BYTES, row + v0 * 16, nv * 16u, &sh.full[slot],
-                          pass == 0 ? pol_last : pol_first);
+            if (pass == 0 && !DART_FU_P1LAST)
+              bulk_g2s(ring + (size_t)slot * CH_BYTES, row + v0 * 16, nv * 16u, &sh.full[slot]);
+            else
+              bulk_g2s_hint(ring + (size_t)slot * CH_BYTES, row + v0 * 16, nv * 16u, &sh.full[slot],
+                            pass == 0 ? pol_last : pol_first);
           }
         }
         ++nrow;
@@ -390,8 +401,9 @@ __global__ void __launch_bounds__(FU_THREADS, DART_FU_CTAS) fused_sweep_kernel(c
     const float zy = rc.zy;
     // ---------------- pass 2: gradient over this warp's chunks
     const float2 cc2 = make_float2(c2, c2), nl = make_float2(nl2, nl2), ng = make_float2(-g, -g);
-    for (int64_t j = warp; j < nch; j += FU_NC) {
-      const int64_t idx = (2 * nrow + 1) * cw + j / FU_NC;
+    for (int64_t ji = 0; ji < cw; ++ji) {
+      const int64_t j = DART_FU_REV ? warp + (cw - 1 - ji) * FU_NC : warp + ji * FU_NC;
+      const int64_t idx = (2 * nrow + 1) * cw + ji;
       const int slot = warp * FU_SW + (int)(idx % FU_SW);
       mbar_wait(&sh.full[slot], (uint32_t)((idx / FU_SW) & 1));
       const uint8_t* sp = ring + (size_t)slot * CH_BYTES;
