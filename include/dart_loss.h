@@ -53,7 +53,7 @@
 extern "C" {
 #endif
 
-#define DART_ABI_VERSION 2
+#define DART_ABI_VERSION 3
 
 typedef enum {
   DART_OK = 0,
@@ -96,6 +96,15 @@ typedef enum {
                             out.ell[t] holds ell_s / n_s and step_ell[s] holds ell_s */
 } dart_ratio_level;
 
+/* KL(pi_theta || pi_ref) estimator for the beta term (
+ * the estimator is unstated -- SURVEY Q10, §8(f) NEXT #4). */
+typedef enum {
+  DART_KL_K3 = 0,    /* per-token k3 from log pi_ref(y_t): e^d - d - 1, d = logp_ref - logp (default) */
+  DART_KL_EXACT = 1  /* exact full-vocabulary KL_t = sum_v p_v (log p_v - log q_v) from the reference
+                        policy's logits (batch->ref_logits, same temperature); its gradient
+                        invT p_v ((log p_v - log q_v) - KL_t) enters every element of the row */
+} dart_kl_mode;
+
 /* Device status bits (OR-accumulated into *status). */
 #define DART_STATUS_NONFINITE_LOGIT (1u << 0) /* NaN or +inf logit in a row */
 #define DART_STATUS_TARGET_RANGE    (1u << 1) /* target outside [0, V) */
@@ -121,6 +130,7 @@ typedef struct {
   int32_t zero_fill_masked; /* 1: dense dlogits (masked rows written as zeros);
                                0: masked rows are left untouched                   */
   int32_t ratio_level;    /* dart_ratio_level */
+  int32_t kl_mode;        /* dart_kl_mode */
 } dart_cfg;
 
 /* GLOBAL batch metadata, replicated on every rank (device pointers). */
@@ -148,7 +158,10 @@ typedef struct {
   const int32_t* target;       /* [T_loc] sampled token y_t in [0,V) */
   const float* logp_old;       /* [T_loc] log pi_old^Train(y_t)   (stop-grad input) */
   const float* logp_rollout;   /* [T_loc] log pi_old^Rollout(y_t) (recorded by the rollout engine) */
-  const float* logp_ref;       /* [T_loc] log pi_ref(y_t), or NULL when beta_kl == 0 */
+  const float* logp_ref;       /* [T_loc] log pi_ref(y_t), or NULL when beta_kl == 0 or kl_mode == EXACT */
+  const void* ref_logits;      /* [T_loc, ld_ref] reference-policy logits (logits_dtype), only read when
+                                  kl_mode == DART_KL_EXACT and beta_kl > 0; 16-byte aligned rows */
+  int64_t ld_ref;              /* row pitch of ref_logits in elements, >= V */
 } dart_batch;
 
 /* Forward outputs (caller-allocated device buffers). */

@@ -51,6 +51,9 @@ SEL_CEIL = 1
 SEL_LINEAR = 2
 SEL_OFF = 3
 
+KL_K3 = 0           # per-token k3 from log pi_ref(y) (default)
+KL_EXACT = 1        # exact full-vocabulary KL(pi_theta || pi_ref) from reference logits
+
 RATIO_TOKEN = 0     # r, w per token (default)
 RATIO_STEP = 1      # r, w per step on sum_t log pi(y_t) (PAPER.md:124/257 pi(a|h,s))
 
@@ -267,6 +270,20 @@ def kl_k3_dlogp(logp, logp_ref):
     return -(math.exp(d) - 1.0)        # d(e^d - d - 1)/dd * dd/dlogp, dd/dlogp = -1
 
 
+def kl_exact_row(z_row, zref_row, inv_temperature=1.0):
+    """D_KL(pi_theta || pi_ref) = sum_v p_v (log p_v - log q_v) over the whole
+    vocabulary (PAPER.md:124, 259), p = softmax(z/T), q = softmax(z_ref/T).
+    Returns (KL, log p - log q) ; terms with p_v = 0 contribute 0."""
+    lse, p = log_softmax_row(z_row, inv_temperature)
+    lse_r, q = log_softmax_row(zref_row, inv_temperature)
+    zp = np.asarray(z_row, dtype=np.float64) * float(inv_temperature)
+    zq = np.asarray(zref_row, dtype=np.float64) * float(inv_temperature)
+    with np.errstate(invalid="ignore"):
+        lpq = (zp - lse) - (zq - lse_r)                # log p_v - log q_v
+    nz = p > 0
+    return float(np.sum(p[nz] * lpq[nz])), lpq
+
+
 def token_loss(logp, logp_old, logp_roll, logp_ref, A, cfg):
     """ell_t = -w * min(rA, clip(r)A) + beta * KL_k3  -- the library minimises
     L = -J_HE (Eq. 2; SURVEY Q3 the IS weight multiplies the
@@ -391,16 +408,36 @@ def loss_pass(batch, cfg, keep_override=None, want_grad=True, rows=None):
     kl = np.empty(T)
     trunc = np.zeros(T, dtype=bool)
     step_ratio = cfg.get("ratio_level", RATIO_TOKEN) == RATIO_STEP
+    exact_kl = cfg.get("kl_mode", KL_K3) == KL_EXACT and cfg["beta_kl"] != 0.0
+    kl_ex = np.zeros(T)
+    LPQ = {}
+    if exact_kl:
+        zr = batch["ref_logits"]
+        for t in range(T):
+            kl_ex[t], lpq = kl_exact_row(z[t], zr[t], invT)
+            if want_grad and t in want_rows:
+                LPQ[t] = lpq
+        # the KL term no longer flows through log pi(y): token_loss sees beta = 0
+        cfg_tok = {**cfg, "beta_kl": 0.0}
+    else:
+        cfg_tok = cfg
     if not step_ratio:
         for t in range(T):
             ell[t], dell[t], w[t], r[t], clipped[t], kl[t] = token_loss(
-                logp[t], lo[t], lr[t], lref[t], A_tok[t], cfg)
+                logp[t], lo[t], lr[t], lref[t], A_tok[t], cfg_tok)
             trunc[t] = math.exp(lo[t] - lr[t]) >= cfg["is_cap"]
+            if exact_kl:
+                kl[t] = kl_ex[t]
+                ell[t] += cfg["beta_kl"] * kl_ex[t]
     else:
         # step-level ratio and IS weight on the step's sequence log-probability
         # log pi(a|h,s) = sum_{t in s} log pi(y_t)
         beta = cfg["beta_kl"]
         for s_ in range(S):
+            if exact_kl:
+                beta_tok = 0.0
+            else:
+                beta_tok = beta
             toks = np.arange(step_tok_off[s_], step_tok_off[s_ + 1])
             A_s = A_tok[toks[0]]
             log_r = float(np.sum(logp[toks] - lo[toks]))
@@ -409,13 +446,14 @@ def loss_pass(batch, cfg, keep_override=None, want_grad=True, rows=None):
             w_s = min(math.exp(log_w), cfg["is_cap"])
             sur = surrogate(r_s, A_s, cfg["eps_low"], cfg["eps_high"])
             dsur = surrogate_dlogp(r_s, A_s, cfg["eps_low"], cfg["eps_high"])   # d/d(log r_s)
-            kls = np.array([kl_k3(logp[t], lref[t]) if beta != 0.0 else 0.0 for t in toks])
+            kls = np.array([(kl_ex[t] if exact_kl else kl_k3(logp[t], lref[t])) if beta != 0.0 else 0.0
+                            for t in toks])
             ell_s = -w_s * sur + beta * float(np.sum(kls))
             clip_s = not (r_s * A_s <= clip(r_s, 1.0 - cfg["eps_low"], 1.0 + cfg["eps_high"]) * A_s)
             for j, t in enumerate(toks):
                 # d ell_s / d logp_t: d log r_s / d logp_t = 1
-                dk = kl_k3_dlogp(logp[t], lref[t]) if beta != 0.0 else 0.0
-                dell[t] = -w_s * dsur + beta * dk
+                dk = kl_k3_dlogp(logp[t], lref[t]) if beta_tok != 0.0 else 0.0
+                dell[t] = -w_s * dsur + beta_tok * dk
                 ell[t] = ell_s / len(toks)
                 w[t], r[t], clipped[t], kl[t] = w_s, r_s, clip_s, kls[j]
                 trunc[t] = math.exp(log_w) >= cfg["is_cap"]
@@ -449,5 +487,10 @@ def loss_pass(batch, cfg, keep_override=None, want_grad=True, rows=None):
             onehot = np.zeros(V)
             onehot[y[t]] = 1.0
             dz[t] = g * invT * (onehot - P[t]) if g != 0.0 else np.zeros(V)
+            if exact_kl and c_tok[t] != 0.0:
+                # d KL_t / d z_v = invT p_v ((log p_v - log q_v) - KL_t)
+                pk = P[t]
+                term = np.where(pk > 0, pk * (np.nan_to_num(LPQ[t], nan=0.0, posinf=0.0, neginf=0.0) - kl_ex[t]), 0.0)
+                dz[t] = dz[t] + c_tok[t] * cfg["beta_kl"] * invT * term
         out["dz"] = dz
     return out

@@ -72,7 +72,8 @@ WsLayout ws_layout(const dart_batch* b, const dart_meta* m) {
   L.aux_w = take(T * 4);
   L.aux_kl = take(T * 4);
   L.aux_flags = take(T);
-  L.rec = take(T * 16);
+  L.rec = take(T * 32);
+  L.klq = take(T * 4);
   L.step_stats = take(S_loc * NSTAT * 8);
   L.step_cost = take((S_loc + 1) * 8);
   L.step_scale = take(S_loc * 8);
@@ -109,6 +110,7 @@ bool cfg_ok(const dart_cfg* c) {
   if (c->norm_mode < DART_NORM_TOKEN_MEAN_KEPT || c->norm_mode > DART_NORM_SUM) return false;
   if (c->select_rule < DART_SEL_FLOOR || c->select_rule > DART_SEL_OFF) return false;
   if (c->ratio_level != DART_RATIO_TOKEN && c->ratio_level != DART_RATIO_STEP) return false;
+  if (c->kl_mode != DART_KL_K3 && c->kl_mode != DART_KL_EXACT) return false;
   return true;
 }
 
@@ -131,7 +133,12 @@ dart_status batch_check(const dart_batch* b, const dart_meta* m, const dart_cfg*
   if (b->step_begin < 0 || b->step_begin + b->S_loc > m->S) return DART_ERR_INVALID_ARG;
   if (b->T_loc > 0) {
     if (!b->logits || !b->target || !b->logp_old || !b->logp_rollout) return DART_ERR_INVALID_ARG;
-    if (c->beta_kl > 0.f && !b->logp_ref) return DART_ERR_INVALID_ARG;
+    if (c->beta_kl > 0.f && c->kl_mode == DART_KL_K3 && !b->logp_ref) return DART_ERR_INVALID_ARG;
+    if (c->beta_kl > 0.f && c->kl_mode == DART_KL_EXACT) {
+      if (!b->ref_logits || !aligned16(b->ref_logits) || b->ld_ref < b->V ||
+          ((size_t)b->ld_ref * esize(b->logits_dtype)) % 16 != 0)
+        return DART_ERR_INVALID_ARG;
+    }
     if (!aligned16(b->logits) || ((size_t)b->ld * esize(b->logits_dtype)) % 16 != 0) return DART_ERR_INVALID_ARG;
     if (b->S_loc < 1) return DART_ERR_INVALID_ARG;
   }
@@ -158,6 +165,8 @@ dart_status cuda_status(cudaError_t e) {
 
 // log2 of the number of warps a row is split over: only for few rows, and
 // only when every canonical segment is non-empty (rows >= KSEG chunks)
+inline bool exact_kl(const dart_cfg* c) { return c->kl_mode == DART_KL_EXACT && c->beta_kl > 0.f; }
+
 int choose_lg_nsplit(const dart_batch* b, const WsLayout& L, int64_t nvec) {
   if (!L.split_alloc || nvec < (int64_t)KSEG * CH_VEC) return 0;
   const int64_t target_units = 4LL * sm_count() * 16;
@@ -262,14 +271,18 @@ dart_status dart_loss_fwd(const dart_batch* b, const dart_meta* m, const dart_cf
     fp.aux_kl = at<float>(ws, L.aux_kl);
     fp.aux_flags = at<uint8_t>(ws, L.aux_flags);
     fp.status = o->status;
-    fp.lg_nsplit = choose_lg_nsplit(b, L, nvec);
+    fp.lg_nsplit = exact_kl(c) ? 0 : choose_lg_nsplit(b, L, nvec);
+    fp.ref_logits = static_cast<const uint8_t*>(b->ref_logits);
+    fp.ld_ref_bytes = b->ld_ref * (int64_t)es;
+    fp.klq = at<float>(ws, L.klq);
     fp.part_m = L.split_alloc ? at<float>(ws, L.part_m) : nullptr;
     fp.part_s = L.split_alloc ? at<double>(ws, L.part_s) : nullptr;
     fp.part_u = L.split_alloc ? at<double>(ws, L.part_u) : nullptr;
     fp.row_cnt = L.split_alloc ? at<uint32_t>(ws, L.row_cnt) : nullptr;
     if (fp.lg_nsplit > 0) DART_TRY_RT(cudaMemsetAsync(fp.row_cnt, 0, (size_t)b->T_loc * 4, s));
     rec(0, s);
-    DART_TRY(launch_fwd_sweep(fp, b->logits_dtype == DART_BF16, sm_count(), s));
+    if (exact_kl(c)) DART_TRY(launch_fwd_kl(fp, b->logits_dtype == DART_BF16, sm_count(), s));
+    else DART_TRY(launch_fwd_sweep(fp, b->logits_dtype == DART_BF16, sm_count(), s));
     rec(1, s);
 
     StepReduceParams sp;
@@ -278,6 +291,7 @@ dart_status dart_loss_fwd(const dart_batch* b, const dart_meta* m, const dart_cf
     sp.H = o->tok_entropy; sp.ell = o->ell; sp.dell = o->dell;
     sp.aux_w = fp.aux_w; sp.aux_kl = fp.aux_kl; sp.tok_adv = fp.tok_adv; sp.aux_flags = fp.aux_flags;
     sp.ratio_level = c->ratio_level;
+    sp.exact_kl = exact_kl(c) ? 1 : 0;
     sp.no_entropy = 0;
     sp.keep = nullptr;
     sp.logp = o->logp; sp.logp_old = b->logp_old; sp.logp_roll = b->logp_rollout; sp.logp_ref = b->logp_ref;
@@ -352,12 +366,15 @@ dart_status dart_loss_bwd(const dart_batch* b, const dart_meta* m, const dart_cf
   g_launches = 0;
   const size_t es = esize(b->logits_dtype);
   const int64_t nvec = (int64_t)((b->V * es + 15) / 16);
-  const int64_t nch = (nvec + CH_VEC - 1) / CH_VEC;
+  const bool kx = exact_kl(c);
+  const int64_t chv = kx ? CH_VEC / 2 : CH_VEC;            // exact KL: 2 KB of z + 2 KB of z_ref per slot
+  const int64_t nch = (nvec + chv - 1) / chv;
 
   BwdPrepParams pp;
   pp.T_loc = b->T_loc; pp.tok_begin = b->tok_begin; pp.step_begin = b->step_begin; pp.S_loc = b->S_loc;
   pp.nch = nch; pp.norm_mode = c->norm_mode; pp.zero_fill = c->zero_fill_masked ? 1 : 0;
   pp.ratio_level = c->ratio_level;
+  pp.kept_cost = kx ? 3 : 2;
   pp.step_tok_off = m->step_tok_off; pp.keep = keep; pp.norm = norm;
   pp.step_ell = f->step_ell; pp.step_stats = at<double>(ws, L.step_stats);
   pp.step_scale = at<double>(ws, L.step_scale);
@@ -374,7 +391,12 @@ dart_status dart_loss_bwd(const dart_batch* b, const dart_meta* m, const dart_cf
     rp.tok_step = at<int32_t>(ws, L.tok_step); rp.target = b->target; rp.step_scale = pp.step_scale;
     rp.dell = f->dell; rp.lse2 = at<float>(ws, L.lse2); rp.invT = (double)c->inv_temperature;
     rp.rec = at<int4>(ws, L.rec);
-    DART_TRY(launch_rowrec(rp, s));
+    rp.ref_logits = static_cast<const uint8_t*>(b->ref_logits);
+    rp.ld_ref_bytes = b->ld_ref * (int64_t)es;
+    rp.klq = at<float>(ws, L.klq);
+    rp.beta = c->beta_kl;
+    if (kx) DART_TRY(launch_rowrec_kl(rp, s));
+    else DART_TRY(launch_rowrec(rp, s));
 
     BwdParams bp;
     bp.logits = static_cast<const uint8_t*>(b->logits);
@@ -390,8 +412,12 @@ dart_status dart_loss_bwd(const dart_batch* b, const dart_meta* m, const dart_cf
     bp.step_cost = pp.step_cost;
     bp.step_chunk = pp.step_chunk;
     bp.zero_fill = pp.zero_fill;
+    bp.ref_logits = rp.ref_logits;
+    bp.ld_ref_bytes = rp.ld_ref_bytes;
+    bp.invT_f = c->inv_temperature;
     rec(2, s);
-    DART_TRY(launch_bwd_sweep(bp, b->logits_dtype == DART_BF16, grad_dtype == DART_BF16, sm_count(), s));
+    if (kx) DART_TRY(launch_bwd_kl(bp, b->logits_dtype == DART_BF16, grad_dtype == DART_BF16, sm_count(), s));
+    else DART_TRY(launch_bwd_sweep(bp, b->logits_dtype == DART_BF16, grad_dtype == DART_BF16, sm_count(), s));
     rec(3, s);
   }
   g_last_launches = g_launches;
@@ -403,7 +429,7 @@ dart_status dart_loss_fused(const dart_batch* b, const dart_meta* m, const dart_
                             int64_t ldg, dart_stats* stats, void* ws, size_t ws_bytes, void* stream) {
   dart_status st = batch_check(b, m, c);
   if (st != DART_OK) return st;
-  if (c->ratio_level != DART_RATIO_TOKEN) return DART_ERR_UNSUPPORTED;
+  if (c->ratio_level != DART_RATIO_TOKEN || exact_kl(c)) return DART_ERR_UNSUPPORTED;
   if (!o || !o->status) return DART_ERR_INVALID_ARG;
   if (b->T_loc > 0 && (!o->lse || !o->logp || !o->ell || !o->dell)) return DART_ERR_INVALID_ARG;
   if (b->S_loc > 0 && !o->step_ell) return DART_ERR_INVALID_ARG;
@@ -445,6 +471,7 @@ dart_status dart_loss_fused(const dart_batch* b, const dart_meta* m, const dart_
   pp.T_loc = b->T_loc; pp.tok_begin = b->tok_begin; pp.step_begin = b->step_begin; pp.S_loc = b->S_loc;
   pp.nch = nch; pp.norm_mode = c->norm_mode; pp.zero_fill = c->zero_fill_masked ? 1 : 0;
   pp.ratio_level = c->ratio_level;
+  pp.kept_cost = 2;
   pp.step_tok_off = m->step_tok_off; pp.keep = keep; pp.norm = norm;
   pp.step_ell = o->step_ell; pp.step_stats = at<double>(ws, L.step_stats);
   pp.step_scale = at<double>(ws, L.step_scale);
@@ -485,7 +512,7 @@ dart_status dart_loss_fused(const dart_batch* b, const dart_meta* m, const dart_
     sp.aux_w = fp.aux_w; sp.aux_kl = fp.aux_kl; sp.tok_adv = fp.tok_adv; sp.aux_flags = fp.aux_flags;
     sp.step_entropy = nullptr; sp.step_ell = o->step_ell;
     sp.step_stats = at<double>(ws, L.step_stats);
-    sp.no_entropy = 1; sp.keep = keep;
+    sp.no_entropy = 1; sp.keep = keep; sp.exact_kl = 0;
     sp.ratio_level = DART_RATIO_TOKEN;
     sp.logp = o->logp; sp.logp_old = b->logp_old; sp.logp_roll = b->logp_rollout; sp.logp_ref = b->logp_ref;
     sp.eps_low = c->eps_low; sp.eps_high = c->eps_high; sp.is_cap = c->is_cap; sp.beta = c->beta_kl;

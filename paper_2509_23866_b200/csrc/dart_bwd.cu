@@ -55,7 +55,7 @@ __global__ void __launch_bounds__(1024) bwd_prep_kernel(BwdPrepParams p) {
       double c = 0.0;
       if (kept) c = step_mode ? inv_norm / (double)n : inv_norm;
       p.step_scale[s] = c;
-      cost = (long long)n * p.nch * (kept ? 2 : (p.zero_fill ? 1 : 0));
+      cost = (long long)n * p.nch * (kept ? p.kept_cost : (p.zero_fill ? 1 : 0));
       nchunks = (kept || p.zero_fill) ? (long long)n * p.nch : 0;
       const double* st = p.step_stats + s * NSTAT;
       v[1] = (double)n;          // n_tok

@@ -27,7 +27,7 @@ constexpr double LN2_D = 0.6931471805599453094172;
 // ---------------------------------------------------------------- workspace
 // Sub-buffers (256 B aligned), identical layout in every call of one pass.
 struct WsLayout {
-  size_t tok_adv, tok_step, lse2, aux_w, aux_kl, aux_flags, rec;        // [T_loc] (rec: 16 B)
+  size_t tok_adv, tok_step, lse2, aux_w, aux_kl, aux_flags, rec, klq;   // [T_loc] (rec: 32 B)
   size_t step_stats;                                                    // [S_loc * NSTAT] f64
   size_t step_cost;                                                     // [S_loc+1] i64
   size_t step_scale;                                                    // [S_loc] f64

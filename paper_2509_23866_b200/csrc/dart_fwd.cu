@@ -635,7 +635,7 @@ __global__ void step_reduce_kernel(StepReduceParams p) {
       const uint8_t flags = (uint8_t)((act ? 0u : 1u) | (trunc ? 2u : 0u));
       for (int64_t t = t0 + lane; t < t1; t += 32) {
         double dkl = 0.0;
-        if (p.beta != 0.0) dkl = 1.0 - exp((double)p.logp_ref[t] - (double)p.logp[t]);
+        if (p.beta != 0.0 && !p.exact_kl) dkl = 1.0 - exp((double)p.logp_ref[t] - (double)p.logp[t]);
         p.dell[t] = (float)(dsur + p.beta * dkl);
         p.ell[t] = (float)(ell_s / (double)n);
         p.aux_w[t] = (float)wt;

@@ -61,6 +61,10 @@ struct FwdParams {
   uint8_t* aux_flags;
   uint32_t* status;
   int lg_nsplit;  // rows are split over 2^lg_nsplit warps (small T_loc)
+  // exact-KL mode (dart_kl.cu)
+  const uint8_t* ref_logits;
+  int64_t ld_ref_bytes;
+  float* klq;     // [T_loc] Q_t = ln2 (lse2 - lse2_ref) + KL_t
   float* part_m;
   double *part_s, *part_u;
   uint32_t* row_cnt;
@@ -80,6 +84,7 @@ struct StepReduceParams {
   const uint8_t* keep;  // [S] global, only read when no_entropy
   // step-level ratio (DART_RATIO_STEP)
   int ratio_level;
+  int exact_kl;         // DART_KL_EXACT: the KL gradient is per element, not through logp
   const float *logp, *logp_old, *logp_roll, *logp_ref;
   double eps_low, eps_high, is_cap, beta;
 };
@@ -116,6 +121,7 @@ struct UnpackParams {
 struct BwdPrepParams {
   int64_t T_loc, tok_begin, step_begin, S_loc, nch;  // nch = chunks per row
   int norm_mode, zero_fill, ratio_level;
+  int kept_cost;         // cost units of a kept chunk: 2 (read + write), 3 with exact KL (two reads)
   const int64_t* step_tok_off;
   const uint8_t* keep;   // [S] global
   const void* norm;      // dart_norm*
@@ -137,7 +143,12 @@ struct RowRecParams {
   const float* dell;
   const float* lse2;
   double invT;
-  void* rec;  // int4 [T_loc]: {g, -lse2, y, z_y}
+  void* rec;  // int4 [T_loc]: {g, -lse2, y, z_y}  (exact KL: 2 x float4)
+  // exact-KL mode
+  const uint8_t* ref_logits;
+  int64_t ld_ref_bytes;
+  const float* klq;
+  double beta;
 };
 
 struct BwdParams {
@@ -153,6 +164,10 @@ struct BwdParams {
   const int64_t* step_cost;     // [S_loc+1] prefix of chunk costs
   const int64_t* step_chunk;    // [S_loc+1] prefix of chunk counts
   int zero_fill;
+  // exact-KL mode
+  const uint8_t* ref_logits;
+  int64_t ld_ref_bytes;
+  float invT_f;
 };
 
 struct FusedParams {
@@ -178,6 +193,9 @@ struct FusedParams {
 };
 
 cudaError_t launch_fused_rec(const FusedParams& p, cudaStream_t st);
+cudaError_t launch_fwd_kl(const FwdParams& p, bool bf16, int num_sms, cudaStream_t st);
+cudaError_t launch_rowrec_kl(const RowRecParams& p, cudaStream_t st);
+cudaError_t launch_bwd_kl(const BwdParams& p, bool in_bf16, bool out_bf16, int num_sms, cudaStream_t st);
 cudaError_t launch_fused_sweep(const FusedParams& p, bool in_bf16, bool out_bf16, int num_sms, cudaStream_t st);
 cudaError_t launch_adv(const AdvParams& p, cudaStream_t st);
 cudaError_t launch_tok_meta(const TokMetaParams& p, cudaStream_t st);

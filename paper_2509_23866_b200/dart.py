@@ -31,8 +31,9 @@ STATUS_BITS = {
     1 << 0: "NONFINITE_LOGIT", 1 << 1: "TARGET_RANGE", 1 << 2: "ROW_ALL_NEGINF",
     1 << 3: "NONFINITE_LOGP", 1 << 4: "EMPTY", 1 << 5: "BAD_CSR", 1 << 6: "TARGET_NEGINF",
 }
-ABI_VERSION = 2
+ABI_VERSION = 3
 RATIO_TOKEN, RATIO_STEP = 0, 1
+KL_K3, KL_EXACT = 0, 1
 
 
 class dart_cfg(ctypes.Structure):
@@ -40,7 +41,8 @@ class dart_cfg(ctypes.Structure):
                 ("beta_kl", ctypes.c_float), ("entropy_q", ctypes.c_float),
                 ("inv_temperature", ctypes.c_float), ("adv_eps", ctypes.c_float),
                 ("norm_mode", ctypes.c_int32), ("select_rule", ctypes.c_int32),
-                ("zero_fill_masked", ctypes.c_int32), ("ratio_level", ctypes.c_int32)]
+                ("zero_fill_masked", ctypes.c_int32), ("ratio_level", ctypes.c_int32),
+                ("kl_mode", ctypes.c_int32)]
 
 
 class dart_meta(ctypes.Structure):
@@ -54,7 +56,7 @@ class dart_batch(ctypes.Structure):
                 ("V", ctypes.c_int64), ("ld", ctypes.c_int64), ("tok_begin", ctypes.c_int64),
                 ("step_begin", ctypes.c_int64), ("S_loc", ctypes.c_int64), ("target", ctypes.c_void_p),
                 ("logp_old", ctypes.c_void_p), ("logp_rollout", ctypes.c_void_p),
-                ("logp_ref", ctypes.c_void_p)]
+                ("logp_ref", ctypes.c_void_p), ("ref_logits", ctypes.c_void_p), ("ld_ref", ctypes.c_int64)]
 
 
 class dart_fwd_out(ctypes.Structure):
@@ -161,11 +163,12 @@ class Config:
     select_rule: int = SEL_FLOOR
     zero_fill_masked: int = 1
     ratio_level: int = RATIO_TOKEN
+    kl_mode: int = KL_K3
 
     def c(self):
         return dart_cfg(self.eps_low, self.eps_high, self.is_cap, self.beta_kl, self.entropy_q,
                         self.inv_temperature, self.adv_eps, self.norm_mode, self.select_rule,
-                        self.zero_fill_masked, self.ratio_level)
+                        self.zero_fill_masked, self.ratio_level, self.kl_mode)
 
     def as_f32(self):
         """The values the library actually sees (float32-rounded), for the oracle."""
@@ -236,7 +239,7 @@ class DartLoss:
 
     def __init__(self, layout, shard: Shard, V: int, cfg: Config, device, logits_dtype=torch.bfloat16,
                  grad_dtype=torch.bfloat16, group=None, world_shards=None, ld: Optional[int] = None,
-                 ldg: Optional[int] = None):
+                 ldg: Optional[int] = None, ld_ref: Optional[int] = None):
         self.L = lib()
         dev = torch.device(device)
         self.device = dev
@@ -245,6 +248,7 @@ class DartLoss:
         self.V = int(V)
         self.ld = int(ld) if ld is not None else self.V
         self.ldg = int(ldg) if ldg is not None else self.V
+        self.ld_ref = int(ld_ref) if ld_ref is not None else self.ld
         self.cfg = cfg
         self.group = group
         self.meta = Meta.from_layout(layout, dev)
@@ -279,17 +283,18 @@ class DartLoss:
                                           dtype=torch.int64, device=dev)
         self.gathered = torch.empty(self.world * self.S_pad, **f32) if self.world > 1 else None
         self.step_H_pad = torch.zeros(self.S_pad, **f32) if self.world > 1 else None
-        b = self._batch(None, None, None, None, None)
+        b = self._batch(None, None, None, None, None, None)
         self.ws_bytes = int(self.L.dart_workspace_size(ctypes.byref(b), ctypes.byref(self.meta.c()),
                                                        ctypes.byref(cfg.c())))
         self.ws = torch.empty(self.ws_bytes, dtype=torch.uint8, device=dev)
         self.launches = 0
 
-    def _batch(self, logits, target, logp_old, logp_roll, logp_ref):
+    def _batch(self, logits, target, logp_old, logp_roll, logp_ref, ref_logits=None):
         dt = DART_BF16 if self.logits_dtype == torch.bfloat16 else DART_F32
         s = self.shard
         return dart_batch(_ptr(logits), dt, s.T_loc, self.V, self.ld, s.tok_begin, s.step_begin, s.S_loc,
-                          _ptr(target), _ptr(logp_old), _ptr(logp_roll), _ptr(logp_ref))
+                          _ptr(target), _ptr(logp_old), _ptr(logp_roll), _ptr(logp_ref), _ptr(ref_logits),
+                          self.ld_ref)
 
     def _fwd_out(self):
         return dart_fwd_out(_ptr(self.lse), _ptr(self.logp), _ptr(self.H), _ptr(self.ell), _ptr(self.dell),
@@ -309,10 +314,22 @@ class DartLoss:
             if t.dtype != dt or not t.is_contiguous() or t.numel() != self.shard.T_loc:
                 raise DartError(f"{name} must be a contiguous {dt} [{self.shard.T_loc}] tensor")
 
-    def forward(self, logits, target, logp_old, logp_roll, logp_ref=None, stream=None):
+    def _check_ref(self, ref_logits):
+        if self.cfg.kl_mode == KL_EXACT and self.cfg.beta_kl > 0:
+            if ref_logits is None:
+                raise DartError("kl_mode=KL_EXACT needs ref_logits (the reference policy's logits)")
+            _require_cuda(ref_logits)
+            if (ref_logits.dtype != self.logits_dtype or ref_logits.shape != (self.shard.T_loc, self.V)
+                    or ref_logits.stride(1) != 1 or ref_logits.stride(0) != self.ld_ref):
+                raise DartError("ref_logits must match logits' dtype and shape, row pitch ld_ref")
+            return ref_logits
+        return None
+
+    def forward(self, logits, target, logp_old, logp_roll, logp_ref=None, ref_logits=None, stream=None):
         self._check_inputs(logits, target, logp_old, logp_roll, logp_ref)
         st = (stream or torch.cuda.current_stream(self.device)).cuda_stream
-        b = self._batch(logits, target, logp_old, logp_roll, logp_ref if self.cfg.beta_kl > 0 else None)
+        use_k3 = self.cfg.beta_kl > 0 and self.cfg.kl_mode == KL_K3
+        b = self._batch(logits, target, logp_old, logp_roll, logp_ref if use_k3 else None, self._check_ref(ref_logits))
         self._inputs = (b, logits, target, logp_old, logp_roll, logp_ref)
         _check(self.L.dart_loss_fwd(ctypes.byref(b), ctypes.byref(self.meta.c()), ctypes.byref(self.cfg.c()),
                                     ctypes.byref(self._fwd_out()), _ptr(self.ws), self.ws_bytes,
@@ -378,9 +395,9 @@ class DartLoss:
         from . import dist as D
         D.all_reduce(self.stats, group=self.group)
 
-    def run(self, logits, target, logp_old, logp_roll, logp_ref=None):
+    def run(self, logits, target, logp_old, logp_roll, logp_ref=None, ref_logits=None):
         """One whole pass (fwd -> C1 -> select -> bwd -> C2), stream-ordered."""
-        self.forward(logits, target, logp_old, logp_roll, logp_ref)
+        self.forward(logits, target, logp_old, logp_roll, logp_ref, ref_logits)
         self.gather()
         self.select()
         self.backward()

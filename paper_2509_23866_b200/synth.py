@@ -68,6 +68,7 @@ class Batch:
     logp_ref: torch.Tensor      # fp32 [T]
     name: str = ""
     logits_store: Optional[torch.Tensor] = None   # [T, ld] storage of `logits` (padded rows)
+    ref_logits: Optional[torch.Tensor] = None     # [T, V] reference-policy logits (exact-KL mode)
 
     def oracle_dict(self, rows=None, logits=True):
         """numpy float64 view for the oracle (exact conversion from bf16/fp32)."""
@@ -80,6 +81,8 @@ class Batch:
                  logp_ref=self.logp_ref.cpu().numpy().astype(np.float64))
         if logits:   # float32 holds bf16 exactly; the oracle widens each row to float64
             d["logits"] = self.logits.float().cpu().numpy()
+            if self.ref_logits is not None:
+                d["ref_logits"] = self.ref_logits.float().cpu().numpy()
         return d
 
 
@@ -174,7 +177,7 @@ def _approx_target_logp(z, y, inv_temperature):
 
 def make_batch(name, seed=0, device="cpu", real_reward=False, chunk_rows=2048,
                inv_temperature=1.0, zero_delta=False, layout=None, V=None, dtype=None,
-               pad_ld: Optional[int] = None):
+               pad_ld: Optional[int] = None, with_ref=False, ref_sigma=0.3):
     """Builds a Batch for config `name` on `device` (seeded; identical bits for
     the same (name, seed, device type))."""
     if layout is None:
@@ -225,5 +228,13 @@ def make_batch(name, seed=0, device="cpu", real_reward=False, chunk_rows=2048,
     logp_old = torch.clamp(logp + d_old, max=0.0)
     logp_roll = torch.clamp(logp_old + torch.from_numpy(d_roll).to(dev), max=0.0)
     logp_ref = torch.clamp(logp + d_ref, max=0.0)
+    ref = None
+    if with_ref:   # reference policy: the same logits perturbed by N(0, ref_sigma^2), same dtype
+        g2 = torch.Generator(device=dev)
+        g2.manual_seed(seed * 7919 + 2)
+        ref = torch.empty((T, V), dtype=dtype, device=dev)
+        for r0 in range(0, T, chunk_rows):
+            r1 = min(T, r0 + chunk_rows)
+            ref[r0:r1] = (logits[r0:r1].float() + ref_sigma * torch.randn((r1 - r0, V), generator=g2, device=dev)).to(dtype)
     return Batch(layout=layout, V=V, logits=logits, target=target, logp_old=logp_old,
-                 logp_rollout=logp_roll, logp_ref=logp_ref, name=name, logits_store=logits_store)
+                 logp_rollout=logp_roll, logp_ref=logp_ref, name=name, logits_store=logits_store, ref_logits=ref)

@@ -1,0 +1,111 @@
+"""exact full-vocabulary KL(pi_theta || pi_ref) from the
+reference policy's logits (DART_KL_EXACT): both sweeps stream z and z_ref.
+GPU vs the float64 oracle (its exact-KL path is pinned by the SPEC example,
+Gibbs, torch.kl_div, finite differences and autograd)."""
+import numpy as np
+import pytest
+import torch
+
+from oracle import dart_oracle as O
+from paper_2509_23866_b200 import dart, synth
+from tests.gpu_helpers import ATOL_ENT, ATOL_LOGP, ATOL_TOK, RTOL_ENT, RTOL_TOK, bf16_ulp, oracle_select_on
+
+pytestmark = pytest.mark.gpu
+
+
+def _run(b, cfg, grad_dtype=None):
+    dev = torch.device("cuda")
+    gd = grad_dtype or (torch.float32 if b.logits.dtype == torch.float32 else torch.bfloat16)
+    dl = dart.DartLoss(b.layout, dart.whole_shard(b.layout), b.V, cfg, dev, logits_dtype=b.logits.dtype,
+                       grad_dtype=gd)
+    dl.run(b.logits.to(dev), b.target.to(dev), b.logp_old.to(dev), b.logp_rollout.to(dev), b.logp_ref.to(dev),
+           ref_logits=b.ref_logits.to(dev))
+    torch.cuda.synchronize()
+    dl.check_status()
+    return dl
+
+
+def _check(dl, b, cfg, rows):
+    cfgf = cfg.as_f32()
+    L = b.layout
+    keep = dl.keep.cpu().numpy()[:L.S]
+    keep_same, _ = oracle_select_on(dl, b, cfgf)
+    assert np.array_equal(keep, keep_same)
+    ob = b.oracle_dict()
+    ref = O.loss_pass(ob, cfgf, keep_override=keep, rows=rows)
+    H, kl, ell = dl.H.cpu().numpy(), None, dl.ell.cpu().numpy()
+    assert np.all(np.abs(H - ref["H"]) <= RTOL_ENT * ref["H"] + ATOL_ENT)
+    assert np.all(np.abs(dl.logp.cpu().numpy() - ref["logp"]) <= ATOL_LOGP)
+    r = ref["r"]
+    ok = ~((np.abs(r - (1 - cfgf["eps_low"])) < 1e-5 * r) | (np.abs(r - (1 + cfgf["eps_high"])) < 1e-5 * r))
+    assert np.all(np.abs(ell[ok] - ref["ell"][ok]) <= RTOL_TOK * np.abs(ref["ell"][ok]) + ATOL_TOK)
+    st = dl.stats_dict()
+    scale = float(np.sum(np.abs(ref["c_tok"] * ref["ell"]))) + 1e-300
+    assert abs(st["loss"] - ref["loss"]) <= RTOL_ENT * scale + 1e-12
+    assert abs(st["sum_kl"] - ref["stats"]["sum_kl"]) <= 1e-5 * abs(ref["stats"]["sum_kl"]) + 1e-6
+    dz = dl.dlogits.float().cpu().numpy()
+    invT = cfgf["inv_temperature"]
+    for t in rows:
+        c = ref["c_tok"][t]
+        if c == 0.0:
+            assert np.all(dz[t] == 0), t
+            continue
+        if not ok[t]:
+            continue
+        _, p = O.log_softmax_row(ob["logits"][t], invT)
+        klt, lpq = O.kl_exact_row(ob["logits"][t], ob["ref_logits"][t], invT)
+        dref = ref["dz"][t]
+        # error model: 1 output ulp + dell's tolerance through |delta - p| + the fp32
+        # error of p and of (log p - log q) in the KL term
+        onehot = np.zeros_like(p)
+        onehot[ob["target"][t]] = 1.0
+        a = abs(c * invT)
+        tol = (bf16_ulp(dref) if dl.grad_dtype == torch.bfloat16 else np.abs(dref) * 2.0 ** -22)
+        tol = tol + a * (RTOL_TOK * abs(ref["dell"][t]) + ATOL_TOK) * np.abs(onehot - p)
+        tol = tol + a * 4e-6 * p * (abs(ref["dell"][t]) + cfgf["beta_kl"] * (np.abs(lpq) + klt + 1.0))
+        tol = tol + a * cfgf["beta_kl"] * p * 2e-5 * (1.0 + np.abs(lpq)) + 1e-38
+        err = np.abs(dz[t] - dref)
+        assert np.all(err <= tol), (t, np.argmax(err - tol), err.max())
+
+
+@pytest.mark.parametrize("ratio", [dart.RATIO_TOKEN, dart.RATIO_STEP])
+@pytest.mark.parametrize("norm", [dart.NORM_TOKEN_MEAN_KEPT, dart.NORM_STEP_MEAN_KEPT])
+def test_exact_kl_small(ratio, norm):
+    b = synth.make_batch("small_multi", seed=8, with_ref=True)
+    cfg = dart.Config(kl_mode=dart.KL_EXACT, beta_kl=0.2, ratio_level=ratio, norm_mode=norm)
+    dl = _run(b, cfg)
+    _check(dl, b, cfg, rows=list(range(b.layout.T)))
+
+
+def test_exact_kl_odd_vocab_bf16():
+    layout, _, _, _ = synth.config_layout("small_multi", seed=9)
+    b = synth.make_batch("small_multi", seed=9, layout=layout, V=1003, dtype=torch.bfloat16, with_ref=True)
+    cfg = dart.Config(kl_mode=dart.KL_EXACT)
+    # odd V: row pitch must be padded to 16 B for both logits and ref_logits
+    dev = torch.device("cuda")
+    ld = 1008
+    lg = torch.zeros((b.layout.T, ld), dtype=torch.bfloat16, device=dev)[:, :b.V]
+    lg.copy_(b.logits)
+    rf = torch.zeros((b.layout.T, ld), dtype=torch.bfloat16, device=dev)[:, :b.V]
+    rf.copy_(b.ref_logits)
+    dl = dart.DartLoss(b.layout, dart.whole_shard(b.layout), b.V, cfg, dev, logits_dtype=torch.bfloat16,
+                       grad_dtype=torch.bfloat16, ld=ld, ldg=ld, ld_ref=ld)
+    dl.run(lg, b.target.to(dev), b.logp_old.to(dev), b.logp_rollout.to(dev), b.logp_ref.to(dev), ref_logits=rf)
+    torch.cuda.synchronize()
+    dl.check_status()
+    _check(dl, b, cfg, rows=list(range(b.layout.T)))
+
+
+def test_exact_kl_mid_vocab():
+    b = synth.make_batch("mid", seed=3, with_ref=True)
+    cfg = dart.Config(kl_mode=dart.KL_EXACT)
+    dl = _run(b, cfg)
+    rng = np.random.default_rng(2)
+    _check(dl, b, cfg, rows=sorted(rng.choice(b.layout.T, 12, replace=False).tolist()))
+
+
+def test_exact_kl_zero_for_identical_reference():
+    b = synth.make_batch("small_multi", seed=10, with_ref=True)
+    b.ref_logits = b.logits.clone()
+    dl = _run(b, dart.Config(kl_mode=dart.KL_EXACT, beta_kl=0.5))
+    assert float(dl.stats_dict()["sum_kl"]) <= 1e-5 * b.layout.T

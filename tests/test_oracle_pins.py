@@ -565,3 +565,74 @@ def test_norm_modes_closed_form():
     c = O.step_weights(keep, off, O.NORM_SUM)
     assert np.allclose(c, [1, 0, 1, 1])
     assert np.all(O.step_weights(np.zeros(4, np.uint8), off, O.NORM_TOKEN_MEAN_KEPT) == 0)
+
+
+# ------------------------------------------------------------------ exact KL
+def test_exact_kl_spec_example_and_gibbs(golden):
+    e = golden("spec_examples.json")["kl_exact_V2"]
+    kl, _ = O.kl_exact_row(np.log(e["p_a"]), np.log(e["p_b"]))
+    assert abs(kl - e["kl"]) < e["tol"]
+    assert abs(kl - (0.9 * math.log(0.9 / 0.5) + 0.1 * math.log(0.1 / 0.5))) < 1e-15   # closed form
+    rng = np.random.default_rng(30)
+    for _ in range(300):
+        V = int(rng.integers(2, 50))
+        z, zr = rng.normal(0, 2, V), rng.normal(0, 2, V)
+        kl, _ = O.kl_exact_row(z, zr)
+        assert kl >= -1e-15                                             # Gibbs
+        ref = torch.nn.functional.kl_div(torch.log_softmax(torch.tensor(zr), 0),
+                                         torch.log_softmax(torch.tensor(z), 0), log_target=True,
+                                         reduction="sum").item()
+        assert abs(kl - ref) < 1e-12 * max(1.0, abs(ref))               # library routine
+        assert O.kl_exact_row(z, z + 3.0)[0] < 1e-13                    # shift-invariant: identical -> 0
+
+
+def _with_ref(b, rng, scale=0.3):
+    b = dict(b)
+    b["ref_logits"] = b["logits"] + rng.normal(0, scale, b["logits"].shape)
+    return b
+
+
+@pytest.mark.parametrize("ratio", [O.RATIO_TOKEN, O.RATIO_STEP])
+def test_exact_kl_finite_differences(ratio):
+    rng = np.random.default_rng(31)
+    b = _with_ref(_random_batch(rng, V=6), rng)
+    cfg = dict(entropy_q=0.3, beta_kl=0.3, is_cap=1.0, kl_mode=O.KL_EXACT, ratio_level=ratio, inv_temperature=0.8)
+    out = O.loss_pass(b, cfg)
+    h = 1e-6
+    z0 = b["logits"]
+    for t in range(z0.shape[0]):
+        for v in range(z0.shape[1]):
+            zp, zm = z0.copy(), z0.copy()
+            zp[t, v] += h
+            zm[t, v] -= h
+            Lp = O.loss_pass({**b, "logits": zp}, cfg, keep_override=out["keep"], want_grad=False)["loss"]
+            Lm = O.loss_pass({**b, "logits": zm}, cfg, keep_override=out["keep"], want_grad=False)["loss"]
+            fd = (Lp - Lm) / (2 * h)
+            an = out["dz"][t][v]
+            if min(abs(out["r"][t] - 0.8), abs(out["r"][t] - 1.28)) < 1e-4:
+                continue
+            assert abs(fd - an) <= 1e-6 * max(1e-3, abs(an)) + 1e-9, (t, v, fd, an)
+
+
+def test_exact_kl_gradient_matches_torch_autograd():
+    rng = np.random.default_rng(32)
+    for trial in range(4):
+        b = _with_ref(_random_batch(rng, V=int(rng.integers(3, 30)), G=3), rng, 0.5)
+        cfg = dict(entropy_q=0.2, beta_kl=0.1, is_cap=1.0, kl_mode=O.KL_EXACT)
+        out = O.loss_pass(b, cfg)
+        c = {**O.DEFAULT_CFG, **cfg}
+        z = torch.tensor(b["logits"], dtype=torch.float64, requires_grad=True)
+        lsm = torch.log_softmax(z, -1)
+        lsq = torch.log_softmax(torch.tensor(b["ref_logits"]), -1)
+        logp = lsm.gather(1, torch.tensor(b["target"])[:, None])[:, 0]
+        lo, lr = torch.tensor(b["logp_old"]), torch.tensor(b["logp_rollout"])
+        A = torch.tensor(out["A_tok"])
+        w = torch.clamp(torch.exp(lo - lr), max=c["is_cap"])
+        r = torch.exp(logp - lo)
+        sur = torch.minimum(r * A, torch.clamp(r, 1 - c["eps_low"], 1 + c["eps_high"]) * A)
+        kl = torch.sum(torch.exp(lsm) * (lsm - lsq), dim=-1)
+        L = torch.sum(torch.tensor(out["c_tok"]) * (-w * sur + c["beta_kl"] * kl))
+        L.backward()
+        assert abs(L.item() - out["loss"]) < 1e-13
+        for t, dz in out["dz"].items():
+            assert np.allclose(z.grad[t].numpy(), dz, rtol=1e-11, atol=1e-15), (trial, t)
