@@ -234,10 +234,11 @@ def run_dart(args):
                                  (r + 1) * layout_r.S, r * layout_r.T, (r + 1) * layout_r.T))
     me = shards[rank]
     cfg = dart.Config(entropy_q=args.q, beta_kl=args.beta, zero_fill_masked=0 if args.compact else 1,
-                      select_rule=dart.SEL_OFF if args.q <= 0 else dart.SEL_FLOOR)
+                      select_rule=dart.SEL_OFF if args.q <= 0 else dart.SEL_FLOOR,
+                      kl_mode=dart.KL_EXACT if args.kl == "exact" else dart.KL_K3)
     t0 = time.time()
     batch = synth.make_batch(args.config, seed=args.seed * 1000 + rank, device=dev, layout=layout_r, V=V,
-                             dtype=dtype)
+                             dtype=dtype, with_ref=args.kl == "exact")
     torch.cuda.synchronize()
     log(f"[rank {rank}] generated {layout_r.T} x {V} {dtype} logits in {time.time() - t0:.1f}s")
     group = None
@@ -247,6 +248,8 @@ def run_dart(args):
     dl = dart.DartLoss(glayout, me, V, cfg, dev, logits_dtype=dtype, grad_dtype=torch.bfloat16,
                        group=group, world_shards=shards)
     inputs = (batch.logits, batch.target, batch.logp_old, batch.logp_rollout, batch.logp_ref)
+    if args.kl == "exact":
+        inputs = inputs + (batch.ref_logits,)
 
     stream = torch.cuda.current_stream()
 
@@ -327,6 +330,9 @@ def run_dart(args):
     es = 2
     fwd_bytes = me.T_loc * (es * V + 24)
     bwd_bytes = kept_tok_loc * (2 * es * V) + (0 if args.compact else masked_tok_loc * es * V)
+    if args.kl == "exact":   # both sweeps also stream the reference logits
+        fwd_bytes = me.T_loc * (2 * es * V + 24)
+        bwd_bytes = kept_tok_loc * (3 * es * V) + (0 if args.compact else masked_tok_loc * es * V)
     if args.fused:   # one kernel: kept rows read once + written once, masked rows written
         fwd_bytes = 0
         bwd_bytes = kept_tok_loc * (2 * es * V + 24) + (0 if args.compact else masked_tok_loc * es * V)
@@ -353,7 +359,7 @@ def run_dart(args):
     # ---- e2e through the public API with host buffers (pinned), rank-local
     e2e = None
     if not args.no_e2e:
-        e2e = run_e2e(args, dl, batch, stream, world)
+        e2e = run_e2e(args, dl, batch, stream, world, inputs)
 
     # ---- CPU oracle baseline (rank 0, N == 1 only)
     cpu = None
@@ -366,7 +372,8 @@ def run_dart(args):
             "value": value, "unit": "logit-tokens/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "bf16", "data": "synthetic (seeded; DESIGN.md §5 recipe)",
-            "config": {"workload": args.config + (" (fused update, mask known in advance: NEXT #1)" if args.fused else ""),
+            "config": {"workload": args.config + (" (fused update, mask known in advance: NEXT #1)" if args.fused else "")
+                       + (" (exact full-vocabulary KL from reference logits: NEXT #4)" if args.kl == "exact" else ""),
                        "desc": CONFIG_DESC.get(args.config, args.config),
                        "global_tokens": T_tot, "tokens_per_gpu": me.T_loc, "V": V,
                        "groups": glayout.G, "steps_total": glayout.S, "entropy_q": args.q, "beta_kl": args.beta,
@@ -397,12 +404,11 @@ def run_dart(args):
         dist.destroy_process_group()
 
 
-def run_e2e(args, dl, batch, stream, world):
+def run_e2e(args, dl, batch, stream, world, inputs):
     """Same pass through the public API with the step's inputs copied from
     pinned host memory each step and the loss read back to the host."""
     from paper_2509_23866_b200 import dart  # noqa: F401
-    host = [t.cpu().pin_memory() for t in (batch.logits, batch.target, batch.logp_old, batch.logp_rollout,
-                                           batch.logp_ref)]
+    host = [t.cpu().pin_memory() for t in inputs]
     dev_bufs = [torch.empty_like(t, device=batch.logits.device) for t in host]
     loss_h = torch.empty(len(dl.stats), dtype=torch.float64).pin_memory()
     h2d = sum(t.numel() * t.element_size() for t in host)
@@ -523,7 +529,8 @@ def run_reference(args):
             "value": value, "unit": "logit-tokens/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": dt * 1e3, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
             "dtype": "f64", "data": "synthetic (seeded; DESIGN.md §5 recipe)",
-            "config": {"workload": args.config + (" (fused update, mask known in advance: NEXT #1)" if args.fused else ""),
+            "config": {"workload": args.config + (" (fused update, mask known in advance: NEXT #1)" if args.fused else "")
+                       + (" (exact full-vocabulary KL from reference logits: NEXT #4)" if args.kl == "exact" else ""),
                        "desc": CONFIG_DESC.get(args.config, args.config),
                        "sample_tokens": ntok},
             "cpu_baseline": {"value": value, "unit": "logit-tokens/s", "cores": 1, "kind": "oracle",
@@ -555,6 +562,8 @@ def main():
     ap.add_argument("--q", type=float, default=0.2)
     ap.add_argument("--beta", type=float, default=0.1)
     ap.add_argument("--compact", action="store_true", help="do not zero-fill masked rows")
+    ap.add_argument("--kl", default="k3", choices=["k3", "exact"],
+                    help="KL estimator: per-token k3 (default) or exact full-vocabulary KL (NEXT #4)")
     ap.add_argument("--fused", action="store_true",
                     help="time the single-read fused update with the mask known in advance (NEXT #1)")
     ap.add_argument("--no-e2e", action="store_true")
