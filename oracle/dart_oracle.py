@@ -284,6 +284,18 @@ def kl_exact_row(z_row, zref_row, inv_temperature=1.0):
     return float(np.sum(p[nz] * lpq[nz])), lpq
 
 
+def lmhead_logits(hidden, weight):
+    """Policy logits from the last hidden state, z_{t,v} = sum_k h_{t,k} W_{v,k}
+    (the LM head whose softmax is pi_theta(a|h,s) of PAPER.md:124 Eq. 1; the
+    fused variant is SURVEY §8(f) #3).  hidden [T, d], weight [V, d] (the
+    nn.Linear layout), both converted exactly to float64; the product is the
+    plain float64 matrix product -- no blocking, no rounding to bf16 (the fused
+    path never materialises bf16 logits, it keeps the fp32 accumulator)."""
+    h = np.asarray(hidden, dtype=np.float64)
+    W = np.asarray(weight, dtype=np.float64)
+    return h @ W.T
+
+
 def token_loss(logp, logp_old, logp_roll, logp_ref, A, cfg):
     """ell_t = -w * min(rA, clip(r)A) + beta * KL_k3  -- the library minimises
     L = -J_HE (Eq. 2; SURVEY Q3 the IS weight multiplies the

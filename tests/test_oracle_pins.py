@@ -636,3 +636,36 @@ def test_exact_kl_gradient_matches_torch_autograd():
         assert abs(L.item() - out["loss"]) < 1e-13
         for t, dz in out["dz"].items():
             assert np.allclose(z.grad[t].numpy(), dz, rtol=1e-11, atol=1e-15), (trial, t)
+
+
+# ------------------------------------------------------------------ LM head
+def test_lmhead_logits_brute_force_integers():
+    """z_{t,v} = sum_k h_{t,k} W_{v,k}: integer inputs make every sum exact, so
+    a pure-Python triple loop is the ground truth (catches a transposed W or a
+    dropped index)."""
+    rng = np.random.default_rng(40)
+    T, V, d = 3, 5, 7
+    h = rng.integers(-3, 4, (T, d)).astype(np.float64)
+    W = rng.integers(-3, 4, (V, d)).astype(np.float64)
+    z = O.lmhead_logits(h, W)
+    assert z.shape == (T, V)
+    for t in range(T):
+        for v in range(V):
+            acc = 0
+            for k in range(d):
+                acc += int(h[t, k]) * int(W[v, k])
+            assert z[t, v] == acc
+
+
+def test_lmhead_logits_special_cases():
+    rng = np.random.default_rng(41)
+    h = rng.normal(size=(4, 6))
+    # W = first rows of the identity: the logits are the hidden coordinates
+    assert np.array_equal(O.lmhead_logits(h, np.eye(6)[:3]), h[:, :3])
+    # a single hot row picks one coordinate; a zero W gives uniform softmax (H = log V)
+    W = np.zeros((5, 6))
+    W[2, 4] = 1.0
+    assert np.array_equal(O.lmhead_logits(h, W)[:, 2], h[:, 4])
+    z0 = O.lmhead_logits(h, np.zeros((9, 6)))
+    lse, logp, H, p = O.token_row(z0[0], 3)
+    assert abs(H - math.log(9)) < 1e-14 and abs(logp + math.log(9)) < 1e-14
