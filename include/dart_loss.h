@@ -53,7 +53,7 @@
 extern "C" {
 #endif
 
-#define DART_ABI_VERSION 3
+#define DART_ABI_VERSION 4
 
 typedef enum {
   DART_OK = 0,
@@ -250,6 +250,38 @@ dart_status dart_loss_fused(const dart_batch* batch, const dart_meta* meta, cons
                             const uint8_t* keep, const dart_norm* norm, const dart_fwd_out* out,
                             void* dlogits, int32_t grad_dtype, int64_t ldg, dart_stats* stats,
                             void* workspace, size_t ws_bytes, void* stream);
+
+/* the LM-head operand of dart_lmhead_fwd.  The
+ * policy logits are z_{t,v} = sum_k h_{t,k} W_{v,k} (the softmax of z / T is
+ * pi_theta(a|h,s), Eq. 1); they are computed on the tensor cores
+ * tile by tile and reduced in the epilogue, never written to memory.
+ * Both operands bf16, K (= d) contiguous, 16-byte aligned base, row pitch in
+ * elements with pitch*2 % 16 == 0, d % 8 == 0. */
+typedef struct {
+  const void* hidden;   /* [T_loc, ld_h] bf16: last hidden state of the local token rows */
+  const void* weight;   /* [V, ld_w] bf16: LM-head weight (the nn.Linear [out, in] layout) */
+  int64_t d;            /* hidden size (K of the contraction), >= 8 */
+  int64_t ld_h;         /* row pitch of hidden, >= d */
+  int64_t ld_w;         /* row pitch of weight, >= d */
+} dart_lmhead;
+
+/* Workspace for dart_lmhead_fwd (>= dart_workspace_size(batch, ...); the
+ * same buffer then serves dart_select_steps). */
+size_t dart_lmhead_workspace_size(const dart_lmhead* head, const dart_batch* batch, const dart_meta* meta,
+                                  const dart_cfg* cfg);
+
+/* Forward of the loss pass with the LM head fused in: identical outputs to
+ * dart_loss_fwd on the logits z = h W^T (fp32 accumulation on the tensor
+ * cores, no rounding to bf16), without the [T_loc, V] logits ever existing.
+ * batch->logits / logits_dtype / ld are ignored (may be NULL/0); V, the
+ * targets, logp_old/rollout/ref and the shard fields are used as in
+ * dart_loss_fwd.  Use: the theta_old "old log-prob" pass that produces the
+ * token entropies, step entropies and (via dart_select_steps) the step mask
+ * for dart_loss_fused.  DART_ERR_UNSUPPORTED for kl_mode == DART_KL_EXACT
+ * with beta_kl > 0.  The LM-head backward (dh, dW) is not part of ABI v4. */
+dart_status dart_lmhead_fwd(const dart_lmhead* head, const dart_batch* batch, const dart_meta* meta,
+                            const dart_cfg* cfg, const dart_fwd_out* out, void* workspace, size_t ws_bytes,
+                            void* stream);
 
 /* Single-rank convenience: fwd + select (world = 1) + bwd on one stream. */
 dart_status dart_loss_pass(const dart_batch* batch, const dart_meta* meta, const dart_cfg* cfg,

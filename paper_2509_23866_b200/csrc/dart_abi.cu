@@ -175,6 +175,48 @@ int choose_lg_nsplit(const dart_batch* b, const WsLayout& L, int64_t nvec) {
   return lg;
 }
 
+// LM-head workspace tail and argument checks
+struct LmLayout {
+  int n_mb, n_nt, n_nc;
+  size_t part_m, part_s, part_u, zy, total;
+};
+
+LmLayout lm_layout(const dart_batch* b, const dart_meta* m) {
+  LmLayout L;
+  const int64_t T = b->T_loc > 0 ? b->T_loc : 0;
+  L.n_mb = (int)((T + 127) / 128);
+  L.n_nt = (int)((b->V + 255) / 256);
+  L.n_nc = (L.n_nt + LM_NT_PER_CHUNK - 1) / LM_NT_PER_CHUNK;
+  size_t off = ws_layout(b, m).total;
+  auto take = [&](size_t bytes) {
+    const size_t o = off;
+    off += al256(bytes ? bytes : 1);
+    return o;
+  };
+  L.part_m = take((size_t)T * L.n_nc * 4);
+  L.part_s = take((size_t)T * L.n_nc * 8);
+  L.part_u = take((size_t)T * L.n_nc * 8);
+  L.zy = take((size_t)T * 4);
+  L.total = off;
+  return L;
+}
+
+dart_status lmhead_check(const dart_lmhead* h, const dart_batch* b, const dart_meta* m, const dart_cfg* c) {
+  if (!h || !b) return DART_ERR_INVALID_ARG;
+  dart_batch bb = *b;                     // the logits fields are not used on this path
+  bb.logits = h->hidden;
+  bb.logits_dtype = DART_BF16;
+  bb.ld = b->V + ((8 - b->V % 8) % 8);
+  if (c && cfg_ok(c) && exact_kl(c)) return DART_ERR_UNSUPPORTED;   // needs the reference logits
+  dart_status st = batch_check(&bb, m, c);
+  if (st != DART_OK) return st;
+  if (h->d < 8 || h->d % 8 != 0 || h->d > (1 << 20)) return DART_ERR_INVALID_ARG;
+  if (h->ld_h < h->d || h->ld_w < h->d || h->ld_h % 8 != 0 || h->ld_w % 8 != 0) return DART_ERR_INVALID_ARG;
+  if (b->T_loc > 0 && (!h->hidden || !h->weight || !aligned16(h->hidden) || !aligned16(h->weight)))
+    return DART_ERR_INVALID_ARG;
+  if (b->T_loc >= ((int64_t)1 << 31)) return DART_ERR_INVALID_ARG;
+  return DART_OK;
+}
 }  // namespace
 
 #define DART_TRY(expr)                        \
@@ -292,6 +334,99 @@ dart_status dart_loss_fwd(const dart_batch* b, const dart_meta* m, const dart_cf
     sp.aux_w = fp.aux_w; sp.aux_kl = fp.aux_kl; sp.tok_adv = fp.tok_adv; sp.aux_flags = fp.aux_flags;
     sp.ratio_level = c->ratio_level;
     sp.exact_kl = exact_kl(c) ? 1 : 0;
+    sp.no_entropy = 0;
+    sp.keep = nullptr;
+    sp.logp = o->logp; sp.logp_old = b->logp_old; sp.logp_roll = b->logp_rollout; sp.logp_ref = b->logp_ref;
+    sp.eps_low = c->eps_low; sp.eps_high = c->eps_high; sp.is_cap = c->is_cap; sp.beta = c->beta_kl;
+    sp.step_entropy = o->step_entropy; sp.step_ell = o->step_ell;
+    sp.step_stats = at<double>(ws, L.step_stats);
+    DART_TRY(launch_step_reduce(sp, s));
+  }
+  g_last_launches = g_launches;
+  return DART_OK;
+}
+
+size_t dart_lmhead_workspace_size(const dart_lmhead* h, const dart_batch* b, const dart_meta* m,
+                                  const dart_cfg* c) {
+  (void)h;
+  (void)c;
+  if (!b || !m) return 0;
+  return lm_layout(b, m).total;
+}
+
+dart_status dart_lmhead_fwd(const dart_lmhead* h, const dart_batch* b, const dart_meta* m, const dart_cfg* c,
+                            const dart_fwd_out* o, void* ws, size_t ws_bytes, void* stream) {
+  dart_status st = lmhead_check(h, b, m, c);
+  if (st != DART_OK) return st;
+  if ((st = fwd_out_check(b, m, o)) != DART_OK) return st;
+  const WsLayout L = ws_layout(b, m);
+  const LmLayout LL = lm_layout(b, m);
+  if (!ws || ws_bytes < LL.total) return DART_ERR_WORKSPACE;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  g_launches = 0;
+
+  AdvParams ap;
+  ap.G = m->G; ap.N_traj = m->N_traj; ap.S = m->S; ap.T = m->T;
+  ap.traj_group = m->traj_group; ap.traj_reward = m->traj_reward;
+  ap.traj_step_off = m->traj_step_off; ap.step_tok_off = m->step_tok_off;
+  ap.adv_eps = (double)c->adv_eps;
+  ap.adv = o->adv; ap.group_ok = o->group_ok;
+  ap.grp_traj = at<int64_t>(ws, L.grp_traj);
+  ap.status = o->status;
+  DART_TRY(launch_adv(ap, s));
+
+  TokMetaParams tp;
+  tp.S = m->S; tp.N_traj = m->N_traj; tp.T_loc = b->T_loc; tp.tok_begin = b->tok_begin;
+  tp.step_begin = b->step_begin; tp.S_loc = b->S_loc;
+  tp.traj_step_off = m->traj_step_off; tp.step_tok_off = m->step_tok_off;
+  tp.adv = o->adv;
+  tp.tok_adv = at<float>(ws, L.tok_adv);
+  tp.tok_step = at<int32_t>(ws, L.tok_step);
+  tp.status = o->status;
+  DART_TRY(launch_tok_meta(tp, s));
+
+  if (b->T_loc > 0) {
+    LmParams lp;
+    lp.T_loc = b->T_loc; lp.V = b->V; lp.K = (int)h->d;
+    lp.n_mb = LL.n_mb; lp.n_nt = LL.n_nt; lp.n_nc = LL.n_nc;
+    lp.nt_per_chunk = LM_NT_PER_CHUNK; lp.group_nc = LM_GROUP_NC;
+    lp.n_items = (int64_t)LL.n_mb * LL.n_nc;
+    lp.c2 = (float)((double)c->inv_temperature * LOG2E_D);
+    lp.target = b->target;
+    lp.part_m = at<float>(ws, LL.part_m);
+    lp.part_s = at<double>(ws, LL.part_s);
+    lp.part_u = at<double>(ws, LL.part_u);
+    lp.zy = at<float>(ws, LL.zy);
+    rec(0, s);
+    DART_TRY(launch_lmhead(h->hidden, h->ld_h, h->weight, h->ld_w, lp, sm_count(), s));
+    rec(1, s);
+
+    FwdParams fp;
+    memset(&fp, 0, sizeof(fp));
+    fp.V = b->V; fp.T_loc = b->T_loc;
+    fp.c2 = lp.c2;
+    fp.target = b->target; fp.logp_old = b->logp_old; fp.logp_roll = b->logp_rollout;
+    fp.logp_ref = b->logp_ref;
+    fp.tok_adv = at<float>(ws, L.tok_adv);
+    fp.eps_low = c->eps_low; fp.eps_high = c->eps_high; fp.is_cap = c->is_cap; fp.beta = c->beta_kl;
+    fp.lse = o->lse; fp.logp = o->logp; fp.H = o->tok_entropy; fp.ell = o->ell; fp.dell = o->dell;
+    fp.lse2 = at<float>(ws, L.lse2);
+    fp.aux_w = at<float>(ws, L.aux_w);
+    fp.aux_kl = at<float>(ws, L.aux_kl);
+    fp.aux_flags = at<uint8_t>(ws, L.aux_flags);
+    fp.status = o->status;
+    LmCombineParams cp;
+    cp.n_nc = LL.n_nc;
+    cp.part_m = lp.part_m; cp.part_s = lp.part_s; cp.part_u = lp.part_u; cp.zy = lp.zy;
+    DART_TRY(launch_lmhead_combine(fp, cp, s));
+
+    StepReduceParams sp;
+    sp.T_loc = b->T_loc; sp.tok_begin = b->tok_begin; sp.step_begin = b->step_begin; sp.S_loc = b->S_loc;
+    sp.step_tok_off = m->step_tok_off;
+    sp.H = o->tok_entropy; sp.ell = o->ell; sp.dell = o->dell;
+    sp.aux_w = fp.aux_w; sp.aux_kl = fp.aux_kl; sp.tok_adv = fp.tok_adv; sp.aux_flags = fp.aux_flags;
+    sp.ratio_level = c->ratio_level;
+    sp.exact_kl = 0;
     sp.no_entropy = 0;
     sp.keep = nullptr;
     sp.logp = o->logp; sp.logp_old = b->logp_old; sp.logp_roll = b->logp_rollout; sp.logp_ref = b->logp_ref;

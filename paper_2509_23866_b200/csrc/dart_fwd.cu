@@ -346,14 +346,12 @@ __device__ __forceinline__ float load_logit(const FwdParams& p, int64_t row, int
 
 // Row epilogue: everything per token that needs the full row (all lanes
 // compute redundantly; lane 0 writes).  Double precision: once per 152K logits.
-__device__ void row_epilogue(const FwdParams& p, int64_t row, Part R, uint32_t bits, bool is_bf16, int lane) {
-  const int32_t y = p.target[row];
+// zy: the target's logit (NaN with DART_STATUS_TARGET_RANGE already in bits
+// when y is out of range).  Shared by the logits sweep and the LM-head path.
+__device__ void row_epilogue_z(const FwdParams& p, int64_t row, Part R, uint32_t bits, float zy, int lane) {
   const double lo = p.logp_old[row], lr = p.logp_roll[row];
   const double lref = (p.beta != 0.0) ? (double)p.logp_ref[row] : 0.0;
   const double A = p.tok_adv[row];
-  float zy = __int_as_float(0x7fc00000);
-  if (y < 0 || y >= p.V) bits |= DART_STATUS_TARGET_RANGE;
-  else zy = load_logit(p, row, y, is_bf16);
   if (!isfinite(lo) || !isfinite(lr) || !isfinite(lref)) bits |= DART_STATUS_NONFINITE_LOGP;
   if (zy == -INFINITY) bits |= DART_STATUS_TARGET_NEGINF;
   if (R.m <= (double)(NEG_CLAMP * p.c2)) bits |= DART_STATUS_ROW_ALL_NEGINF;
@@ -394,6 +392,15 @@ __device__ void row_epilogue(const FwdParams& p, int64_t row, Part R, uint32_t b
     p.aux_flags[row] = (uint8_t)((act ? 0u : 1u) | (trunc ? 2u : 0u));
     status_or(p.status, bits);
   }
+}
+
+__device__ __forceinline__ void row_epilogue(const FwdParams& p, int64_t row, Part R, uint32_t bits, bool is_bf16,
+                                             int lane) {
+  const int32_t y = p.target[row];
+  float zy = __int_as_float(0x7fc00000);
+  if (y < 0 || y >= p.V) bits |= DART_STATUS_TARGET_RANGE;
+  else zy = load_logit(p, row, y, is_bf16);
+  row_epilogue_z(p, row, R, bits, zy, lane);
 }
 
 // Issue the bulk copy of the producer stream's next chunk into `slot` and advance it.
@@ -566,6 +573,31 @@ fwd_sweep_kernel(const FwdParams p) {
   }
 }
 
+// ============================================================== LM-head combine
+// fold the per-(row, vocabulary chunk) partials the tcgen05
+// LM-head kernel left (dart_lmhead.cu) in chunk order, then the same row
+// epilogue as the logits sweep.  One thread per row; deterministic.
+__global__ void lmhead_combine_kernel(FwdParams p, LmCombineParams c) {
+  const int64_t row = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (row >= p.T_loc) return;
+  Part R = {-INFINITY, 0.0, 0.0};
+  const int64_t base = row * c.n_nc;
+  for (int k = 0; k < c.n_nc; ++k) {
+    Part q;
+    q.m = (double)c.part_m[base + k];
+    q.s = c.part_s[base + k];
+    q.u = c.part_u[base + k];
+    R = part_fold(R, q);
+  }
+  const int32_t y = p.target[row];
+  uint32_t bits = 0;
+  float zy = __int_as_float(0x7fc00000);
+  if (y < 0 || y >= p.V) bits |= DART_STATUS_TARGET_RANGE;
+  else zy = c.zy[row];
+  if (!isfinite(R.m) || !isfinite(R.s) || !isfinite(R.u) || !(bits || isfinite(zy))) bits |= DART_STATUS_NONFINITE_LOGIT;
+  row_epilogue_z(p, row, R, bits, zy, 0);
+}
+
 // ============================================================== K2
 // One warp per local step; fixed-order per-lane sums + xor butterfly.
 // Step-ratio mode (DART_RATIO_STEP): the ratio, IS weight
@@ -679,6 +711,12 @@ static cudaError_t launch_fwd_sweep_t(const FwdParams& p, int num_sms, cudaStrea
 cudaError_t launch_fwd_sweep(const FwdParams& p, bool bf16, int num_sms, cudaStream_t st) {
   if (bf16) return launch_fwd_sweep_t<__nv_bfloat16, FWD_WARPS, FWD_STAGES>(p, num_sms, st);
   return launch_fwd_sweep_t<float, FWD_WARPS, FWD_STAGES>(p, num_sms, st);
+}
+
+cudaError_t launch_lmhead_combine(const FwdParams& p, const LmCombineParams& c, cudaStream_t st) {
+  if (p.T_loc <= 0) return cudaSuccess;
+  lmhead_combine_kernel<<<(unsigned)((p.T_loc + 127) / 128), 128, 0, st>>>(p, c);
+  return cudaGetLastError();
 }
 
 cudaError_t launch_adv(const AdvParams& p, cudaStream_t st) {

@@ -192,6 +192,34 @@ struct FusedParams {
   void* rec;                    // [T_loc] 32-byte row records (fused_rec_kernel)
 };
 
+// LM-head-fused forward (dart_lmhead.cu)
+constexpr int LM_NT_PER_CHUNK = 8;   // 256-column tiles per work item (one (m, s, u) partial per row)
+constexpr int LM_GROUP_NC = 4;       // vocabulary chunks per raster super-column (L2 reuse of W and h)
+
+struct LmParams {
+  int64_t T_loc, V;
+  int K;                    // hidden size d
+  int n_mb, n_nt, n_nc;     // 128-row blocks, 256-column tiles, vocabulary chunks
+  int nt_per_chunk, group_nc;
+  int64_t n_items;          // n_mb * n_nc
+  float c2;                 // inv_temperature * log2(e)
+  const int32_t* target;
+  float* part_m;            // [T_loc * n_nc]
+  double *part_s, *part_u;  // [T_loc * n_nc]
+  float* zy;                // [T_loc] fp32 target logit
+};
+
+struct LmCombineParams {
+  int n_nc;
+  const float* part_m;
+  const double *part_s, *part_u;
+  const float* zy;
+};
+
+cudaError_t launch_lmhead(const void* hidden, int64_t ld_h, const void* weight, int64_t ld_w, const LmParams& p,
+                          int num_sms, cudaStream_t st);
+cudaError_t launch_lmhead_combine(const FwdParams& p, const LmCombineParams& c, cudaStream_t st);
+
 cudaError_t launch_fused_rec(const FusedParams& p, cudaStream_t st);
 cudaError_t launch_fwd_kl(const FwdParams& p, bool bf16, int num_sms, cudaStream_t st);
 cudaError_t launch_rowrec_kl(const RowRecParams& p, cudaStream_t st);

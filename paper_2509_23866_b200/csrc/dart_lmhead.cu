@@ -1,0 +1,362 @@
+// dart_lmhead.cu -- SURVEY §8(f) NEXT #3: the LM head fused into the loss
+// pass's forward sweep.
+//
+// z_{t,v} = sum_k h_{t,k} W_{v,k} (the logits whose softmax / T is
+// pi_theta(a|h,s), Eq. 1) is computed on the 5th-generation
+// tensor cores: tcgen05.mma (bf16 x bf16 -> fp32) with both operands staged
+// into shared memory by TMA (128-byte swizzle) and the accumulator in TMEM.
+// The epilogue reads each 128 x 256 accumulator tile back with tcgen05.ld and
+// folds it straight into the per-row online softmax statistics (m, s, u) of
+// the log2 domain (the same (m, s, u) algebra as the logits sweep
+// entropy) plus the target's logit -- the [T, V] logits never touch memory.
+//
+// Work item = (128-row block mb, vocabulary chunk nc of LM_NT_PER_CHUNK
+// 256-column tiles); each item leaves one (m, s, u) partial per row, folded in
+// chunk order by lmhead_combine_kernel (dart_fwd.cu).  Persistent CTAs (one
+// per SM) walk the items in a super-column raster: LM_GROUP_NC chunks x all
+// row blocks, chunks innermost, so the ~148 concurrently active items touch
+// ~37 hidden blocks and ~4 weight chunks at a time (L2 resident).
+//
+// Warp roles (192 threads): warp 0 = TMA producer (one lane), warp 1 = TMEM
+// allocator + MMA issuer (one lane), warps 2..5 = epilogue (warp w reads TMEM
+// lanes 32*(w%4) .. +31, i.e. accumulator rows).  Pipelines: LM_STAGES smem
+// stages (full/empty mbarriers), two TMEM accumulators of 256 fp32 columns
+// (tfull/tempty), so the epilogue of tile i overlaps the MMAs of tile i+1.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include "dart_common.cuh"
+#include "dart_internal.h"
+
+namespace dart {
+namespace {
+
+constexpr int LM_BM = 128, LM_BN = 256, LM_BK = 64, LM_STAGES = 4, LM_ACC = 2;
+constexpr int LM_THREADS = 192;
+constexpr uint32_t LM_A_BYTES = LM_BM * LM_BK * 2;   // 16 KB
+constexpr uint32_t LM_B_BYTES = LM_BN * LM_BK * 2;   // 32 KB
+constexpr uint32_t LM_STAGE_BYTES = LM_A_BYTES + LM_B_BYTES;
+constexpr size_t LM_SMEM = 1024 + (size_t)LM_STAGES * LM_STAGE_BYTES + 256;
+constexpr uint32_t LM_TMEM_COLS = LM_ACC * LM_BN;     // 512: the whole TMEM of the SM
+constexpr float LM_MASKED = -1.0e30f;                 // raw logit for columns >= V
+
+// ---------------------------------------------------------------- PTX
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];" ::"r"(
+          smem_u32(dst)),
+      "l"(map), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
+      : "memory");
+}
+
+__device__ __forceinline__ void tma_prefetch_desc(const CUtensorMap* map) {
+  asm volatile("prefetch.tensormap [%0];" ::"l"(map) : "memory");
+}
+
+// Shared-memory matrix descriptor of a K-major, 128-byte-swizzled tile as TMA
+// writes it: rows of 64 bf16 (128 B) at a 128 B pitch, 8-row core groups
+// 1024 B apart (SBO), LBO unused for swizzled K-major, descriptor version 1
+// (sm_100), layout type 2 = SWIZZLE_128B.  Tiles are 1024-byte aligned, so
+// the base offset is 0.
+__device__ __forceinline__ uint64_t sw128_kmajor_desc(uint32_t saddr) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFFu);
+  d |= (uint64_t)1u << 16;
+  d |= (uint64_t)(1024u >> 4) << 32;
+  d |= (uint64_t)1u << 46;
+  d |= (uint64_t)2u << 61;
+  return d;
+}
+
+// Instruction descriptor, kind::f16: fp32 accumulator (c_format=1), bf16 A
+// and B (format 1), both K-major, N>>3 at bit 17, M>>4 at bit 24.
+constexpr uint32_t LM_IDESC = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(LM_BN >> 3) << 17) |
+                              ((uint32_t)(LM_BM >> 4) << 24);
+
+__device__ __forceinline__ void umma_bf16(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t accumulate) {
+  asm volatile(
+      "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
+      "l"(da), "l"(db), "r"(LM_IDESC), "r"(accumulate));
+}
+
+__device__ __forceinline__ void umma_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
+               : "memory");
+}
+
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+
+// 32 consecutive fp32 columns of this thread's TMEM lane (row).
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&x)[32]) {
+  uint32_t v[32];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+        "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]),
+        "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]),
+        "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 32; ++i) x[i] = __uint_as_float(v[i]);
+}
+
+// work item -> (row block, vocabulary chunk): super-columns of group_nc chunks,
+// row blocks outer, chunks inner
+__device__ __forceinline__ void lm_item(const LmParams& p, int64_t it, int& mb, int& nc) {
+  const int64_t per_sc = (int64_t)p.n_mb * p.group_nc;
+  const int sc = (int)(it / per_sc);
+  const int rem = (int)(it - (int64_t)sc * per_sc);
+  const int gn = min(p.group_nc, p.n_nc - sc * p.group_nc);
+  mb = rem / gn;
+  nc = sc * p.group_nc + rem % gn;
+}
+
+__global__ void __launch_bounds__(LM_THREADS, 1)
+    lmhead_fwd_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                      const LmParams p) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + LM_STAGES * LM_A_BYTES;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + LM_STAGES * LM_STAGE_BYTES);
+  uint64_t* empty = full + LM_STAGES;
+  uint64_t* tfull = empty + LM_STAGES;
+  uint64_t* tempty = tfull + LM_ACC;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + LM_ACC);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < LM_STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int a = 0; a < LM_ACC; ++a) {
+      mbar_init(&tfull[a], 1);
+      mbar_init(&tempty[a], 4);
+    }
+    fence_mbar_init();
+    tma_prefetch_desc(&tmA);
+    tma_prefetch_desc(&tmB);
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "r"(LM_TMEM_COLS)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const int KB = (p.K + LM_BK - 1) / LM_BK;
+
+  if (warp == 0) {
+    // ---------------------------------------------------------- TMA producer
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t ph = 0;
+      for (int64_t it = blockIdx.x; it < p.n_items; it += gridDim.x) {
+        int mb, nc;
+        lm_item(p, it, mb, nc);
+        const int nt0 = nc * p.nt_per_chunk, nt1 = min(nt0 + p.nt_per_chunk, p.n_nt);
+        for (int nt = nt0; nt < nt1; ++nt) {
+          for (int kb = 0; kb < KB; ++kb) {
+            mbar_wait(&empty[stage], ph ^ 1u);
+            mbar_arrive_expect_tx(&full[stage], LM_STAGE_BYTES);
+            tma_load_2d(sA + stage * LM_A_BYTES, &tmA, &full[stage], kb * LM_BK, mb * LM_BM);
+            tma_load_2d(sB + stage * LM_B_BYTES, &tmB, &full[stage], kb * LM_BK, nt * LM_BN);
+            if (++stage == LM_STAGES) {
+              stage = 0;
+              ph ^= 1u;
+            }
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ---------------------------------------------------------- MMA issuer
+    if (lane == 0) {
+      int stage = 0, acc = 0;
+      uint32_t ph = 0, aph = 0;
+      for (int64_t it = blockIdx.x; it < p.n_items; it += gridDim.x) {
+        int mb, nc;
+        lm_item(p, it, mb, nc);
+        const int nt0 = nc * p.nt_per_chunk, nt1 = min(nt0 + p.nt_per_chunk, p.n_nt);
+        for (int nt = nt0; nt < nt1; ++nt) {
+          mbar_wait(&tempty[acc], aph ^ 1u);
+          tc_fence_after();
+          const uint32_t d_tmem = tmem + (uint32_t)(acc * LM_BN);
+          for (int kb = 0; kb < KB; ++kb) {
+            mbar_wait(&full[stage], ph);
+            tc_fence_after();
+            const uint64_t da = sw128_kmajor_desc(smem_u32(sA + stage * LM_A_BYTES));
+            const uint64_t db = sw128_kmajor_desc(smem_u32(sB + stage * LM_B_BYTES));
+#pragma unroll
+            for (int k = 0; k < LM_BK / 16; ++k)   // UMMA_K = 16 bf16 = 32 B along the swizzled row
+              umma_bf16(d_tmem, da + (uint64_t)(2 * k), db + (uint64_t)(2 * k), (kb | k) != 0 ? 1u : 0u);
+            umma_commit(&empty[stage]);             // frees the smem stage when these MMAs retire
+            if (++stage == LM_STAGES) {
+              stage = 0;
+              ph ^= 1u;
+            }
+          }
+          umma_commit(&tfull[acc]);                 // accumulator tile complete
+          if (++acc == LM_ACC) {
+            acc = 0;
+            aph ^= 1u;
+          }
+        }
+      }
+    }
+  } else {
+    // ---------------------------------------------------------- epilogue
+    const int q = warp & 3;            // TMEM lane quarter this warp may access
+    const int r = q * 32 + lane;       // accumulator row of this thread
+    const float c2 = p.c2;
+    int acc = 0;
+    uint32_t aph = 0;
+    for (int64_t it = blockIdx.x; it < p.n_items; it += gridDim.x) {
+      int mb, nc;
+      lm_item(p, it, mb, nc);
+      const int nt0 = nc * p.nt_per_chunk, nt1 = min(nt0 + p.nt_per_chunk, p.n_nt);
+      const int64_t row = (int64_t)mb * LM_BM + r;
+      const bool valid = row < p.T_loc;
+      const int64_t y = valid ? (int64_t)p.target[row] : -1;
+      float m_run = LM_MASKED;         // running max of z*c2 (log2 units); any real logit exceeds it
+      double S = 0.0, U = 0.0;         // sum 2^(x-m), sum 2^(x-m)(x-m)
+      float zy = 0.0f;
+      for (int nt = nt0; nt < nt1; ++nt) {
+        mbar_wait(&tfull[acc], aph);
+        tc_fence_after();
+        const uint32_t tbase = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * LM_BN);
+#pragma unroll 1
+        for (int j = 0; j < LM_BN / 32; ++j) {
+          float x[32];
+          tmem_ld32(tbase + (uint32_t)(j * 32), x);
+          const int64_t col0 = (int64_t)nt * LM_BN + j * 32;
+          if (col0 + 32 > p.V) {       // vocabulary tail (TMA zero-filled columns >= V)
+            const int nv = (int)max((int64_t)0, p.V - col0);
+#pragma unroll
+            for (int i = 0; i < 32; ++i) x[i] = (i < nv) ? x[i] : LM_MASKED;
+          }
+          float mx = x[0];
+#pragma unroll
+          for (int i = 1; i < 32; ++i) mx = fmaxf(mx, x[i]);
+          const float gm = mx * c2;
+          if (gm > m_run) {              // exact rescale of (S, U) to the new max
+            const float dm = m_run - gm;
+            const double f = (double)ex2(dm);
+            U = f * (U + S * (double)dm);
+            S *= f;
+            m_run = gm;
+          }
+          float s0 = 0.f, s1 = 0.f, u0 = 0.f, u1 = 0.f;
+#pragma unroll
+          for (int i = 0; i < 32; i += 2) {
+            const float d0 = fmaf(x[i], c2, -m_run), d1 = fmaf(x[i + 1], c2, -m_run);
+            const float e0 = ex2(d0), e1 = ex2(d1);
+            s0 += e0;
+            s1 += e1;
+            u0 = fmaf(e0, d0, u0);
+            u1 = fmaf(e1, d1, u1);
+          }
+          S += (double)(s0 + s1);
+          U += (double)(u0 + u1);
+          const int64_t jy = y - col0;
+          if ((uint64_t)jy < 32u) {
+            // binary select tree on the bits of jy (a plain x[jy] would put x in local memory)
+            float t[16];
+#pragma unroll
+            for (int i = 0; i < 16; ++i) t[i] = (jy & 16) ? x[i + 16] : x[i];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) t[i] = (jy & 8) ? t[i + 8] : t[i];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) t[i] = (jy & 4) ? t[i + 4] : t[i];
+#pragma unroll
+            for (int i = 0; i < 2; ++i) t[i] = (jy & 2) ? t[i + 2] : t[i];
+            zy = (jy & 1) ? t[1] : t[0];
+          }
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&tempty[acc]);
+        if (++acc == LM_ACC) {
+          acc = 0;
+          aph ^= 1u;
+        }
+      }
+      if (valid) {
+        const int64_t idx = row * p.n_nc + nc;
+        p.part_m[idx] = m_run;
+        p.part_s[idx] = S;
+        p.part_u[idx] = U;
+        if (y >= (int64_t)nt0 * LM_BN && y < (int64_t)nt1 * LM_BN) p.zy[row] = zy;
+      }
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(LM_TMEM_COLS) : "memory");
+  }
+}
+
+// ---------------------------------------------------------------- host
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    void* ptr = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(ptr);
+  }
+  return fn;
+}
+
+// 2-D bf16 tensor map over a row-major [rows, K] matrix (K contiguous),
+// box = 64 (K) x box_rows, 128-byte swizzle, zero fill out of bounds.
+bool make_map(CUtensorMap* m, const void* base, int64_t rows, int64_t K, int64_t ld, uint32_t box_rows) {
+  auto enc = encode_fn();
+  if (!enc) return false;
+  cuuint64_t dims[2] = {(cuuint64_t)K, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)ld * 2};
+  cuuint32_t box[2] = {(cuuint32_t)LM_BK, box_rows};
+  cuuint32_t es[2] = {1, 1};
+  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, es,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
+}  // namespace
+
+cudaError_t launch_lmhead(const void* hidden, int64_t ld_h, const void* weight, int64_t ld_w, const LmParams& p,
+                          int num_sms, cudaStream_t st) {
+  if (p.T_loc <= 0 || p.n_items <= 0) return cudaSuccess;
+  CUtensorMap tmA, tmB;
+  if (!make_map(&tmA, hidden, p.T_loc, p.K, ld_h, LM_BM)) return cudaErrorInvalidValue;
+  if (!make_map(&tmB, weight, p.V, p.K, ld_w, LM_BN)) return cudaErrorInvalidValue;
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(lmhead_fwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)LM_SMEM);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  const int64_t grid = p.n_items < num_sms ? p.n_items : num_sms;
+  lmhead_fwd_kernel<<<(unsigned)grid, LM_THREADS, LM_SMEM, st>>>(tmA, tmB, p);
+  return cudaGetLastError();
+}
+
+}  // namespace dart

@@ -31,7 +31,7 @@ STATUS_BITS = {
     1 << 0: "NONFINITE_LOGIT", 1 << 1: "TARGET_RANGE", 1 << 2: "ROW_ALL_NEGINF",
     1 << 3: "NONFINITE_LOGP", 1 << 4: "EMPTY", 1 << 5: "BAD_CSR", 1 << 6: "TARGET_NEGINF",
 }
-ABI_VERSION = 3
+ABI_VERSION = 4
 RATIO_TOKEN, RATIO_STEP = 0, 1
 KL_K3, KL_EXACT = 0, 1
 
@@ -66,6 +66,11 @@ class dart_fwd_out(ctypes.Structure):
                 ("status", ctypes.c_void_p)]
 
 
+class dart_lmhead(ctypes.Structure):
+    _fields_ = [("hidden", ctypes.c_void_p), ("weight", ctypes.c_void_p), ("d", ctypes.c_int64),
+                ("ld_h", ctypes.c_int64), ("ld_w", ctypes.c_int64)]
+
+
 NORM_FIELDS = ["n_keep_tok", "n_keep_step", "n_tok", "n_step", "inv_norm"]  # 4 x i64 + f64
 STATS_FIELDS = ["loss", "n_tok", "n_kept_tok", "n_kept_step", "sum_clip", "sum_trunc", "sum_w",
                 "sum_adv", "sum_adv2", "sum_H", "sum_kl"]
@@ -73,7 +78,7 @@ STATS_FIELDS = ["loss", "n_tok", "n_kept_tok", "n_kept_step", "sum_clip", "sum_t
 _lib = None
 
 EXPORTED = ["dart_workspace_size", "dart_loss_fwd", "dart_select_steps", "dart_loss_bwd", "dart_loss_fused",
-            "dart_loss_pass",
+            "dart_loss_pass", "dart_lmhead_workspace_size", "dart_lmhead_fwd",
             "dart_status_str", "dart_abi_version", "dart_last_launch_count", "dart_set_timing_events"]
 
 
@@ -114,6 +119,11 @@ def lib():
                                  ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int32,
                                  ctypes.c_int64, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_size_t,
                                  ctypes.c_void_p]
+    L.dart_lmhead_workspace_size.restype = ctypes.c_size_t
+    L.dart_lmhead_workspace_size.argtypes = [P(dart_lmhead), P(dart_batch), P(dart_meta), P(dart_cfg)]
+    L.dart_lmhead_fwd.restype = ctypes.c_int
+    L.dart_lmhead_fwd.argtypes = [P(dart_lmhead), P(dart_batch), P(dart_meta), P(dart_cfg), P(dart_fwd_out),
+                                  ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p]
     L.dart_status_str.restype = ctypes.c_char_p
     L.dart_status_str.argtypes = [ctypes.c_int]
     L.dart_abi_version.restype = ctypes.c_int32
@@ -239,7 +249,7 @@ class DartLoss:
 
     def __init__(self, layout, shard: Shard, V: int, cfg: Config, device, logits_dtype=torch.bfloat16,
                  grad_dtype=torch.bfloat16, group=None, world_shards=None, ld: Optional[int] = None,
-                 ldg: Optional[int] = None, ld_ref: Optional[int] = None):
+                 ldg: Optional[int] = None, ld_ref: Optional[int] = None, with_grad: bool = True):
         self.L = lib()
         dev = torch.device(device)
         self.device = dev
@@ -270,8 +280,9 @@ class DartLoss:
         self.tau = torch.empty(max(layout.G, 1), **f32)
         self.norm = torch.empty(5, dtype=torch.int64, device=dev)          # dart_norm (40 B)
         self.stats = torch.empty(len(STATS_FIELDS), dtype=torch.float64, device=dev)
-        self.dlogits_store = torch.empty((T, self.ldg), dtype=grad_dtype, device=dev)
-        self.dlogits = self.dlogits_store[:, :self.V]
+        # with_grad=False: a forward-only pass (e.g. the LM-head old-log-prob pass) owns no gradient buffer
+        self.dlogits_store = torch.empty((T, self.ldg), dtype=grad_dtype, device=dev) if with_grad else None
+        self.dlogits = self.dlogits_store[:, :self.V] if with_grad else None
         # world layout for select (rank r owns global steps [rank_step_off[r], [r+1]))
         if world_shards is None:
             world_shards = [shard]
@@ -334,6 +345,39 @@ class DartLoss:
         _check(self.L.dart_loss_fwd(ctypes.byref(b), ctypes.byref(self.meta.c()), ctypes.byref(self.cfg.c()),
                                     ctypes.byref(self._fwd_out()), _ptr(self.ws), self.ws_bytes,
                                     ctypes.c_void_p(st)))
+        self.launches += self.L.dart_last_launch_count()
+
+    def forward_lmhead(self, hidden, weight, target, logp_old, logp_roll, logp_ref=None, stream=None):
+        """dart_lmhead_fwd: the forward with z = hidden @ weight.T
+        computed on the tensor cores and reduced in place -- no logits tensor.
+        hidden [T_loc, d] bf16, weight [V, d] bf16 (row pitch may exceed d; d % 8 == 0).
+        Outputs land in the same buffers as forward(); select() may follow."""
+        _require_cuda(hidden, weight, target, logp_old, logp_roll, logp_ref)
+        T = self.shard.T_loc
+        if hidden.dtype != torch.bfloat16 or weight.dtype != torch.bfloat16:
+            raise DartError("the LM-head path takes bf16 hidden states and weights")
+        if hidden.dim() != 2 or weight.dim() != 2 or hidden.shape[0] != T or weight.shape[0] != self.V \
+                or hidden.shape[1] != weight.shape[1] or hidden.stride(1) != 1 or weight.stride(1) != 1:
+            raise DartError(f"hidden [{T}, d] and weight [{self.V}, d] row-major expected, got "
+                            f"{tuple(hidden.shape)} / {tuple(weight.shape)}")
+        for name, t, dt in (("target", target, torch.int32), ("logp_old", logp_old, torch.float32),
+                            ("logp_rollout", logp_roll, torch.float32)):
+            if t.dtype != dt or not t.is_contiguous() or t.numel() != T:
+                raise DartError(f"{name} must be a contiguous {dt} [{T}] tensor")
+        st = (stream or torch.cuda.current_stream(self.device)).cuda_stream
+        use_k3 = self.cfg.beta_kl > 0 and self.cfg.kl_mode == KL_K3
+        head = dart_lmhead(_ptr(hidden), _ptr(weight), int(hidden.shape[1]), int(hidden.stride(0)),
+                           int(weight.stride(0)))
+        b = self._batch(None, target, logp_old, logp_roll, logp_ref if use_k3 else None, None)
+        need = int(self.L.dart_lmhead_workspace_size(ctypes.byref(head), ctypes.byref(b),
+                                                     ctypes.byref(self.meta.c()), ctypes.byref(self.cfg.c())))
+        if need > self.ws_bytes:
+            self.ws = torch.empty(need, dtype=torch.uint8, device=self.device)
+            self.ws_bytes = need
+        self._inputs = (b, None, target, logp_old, logp_roll, logp_ref)
+        _check(self.L.dart_lmhead_fwd(ctypes.byref(head), ctypes.byref(b), ctypes.byref(self.meta.c()),
+                                      ctypes.byref(self.cfg.c()), ctypes.byref(self._fwd_out()), _ptr(self.ws),
+                                      self.ws_bytes, ctypes.c_void_p(st)))
         self.launches += self.L.dart_last_launch_count()
 
     def gather(self):

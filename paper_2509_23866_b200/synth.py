@@ -238,3 +238,76 @@ def make_batch(name, seed=0, device="cpu", real_reward=False, chunk_rows=2048,
             ref[r0:r1] = (logits[r0:r1].float() + ref_sigma * torch.randn((r1 - r0, V), generator=g2, device=dev)).to(dtype)
     return Batch(layout=layout, V=V, logits=logits, target=target, logp_old=logp_old,
                  logp_rollout=logp_roll, logp_ref=logp_ref, name=name, logits_store=logits_store, ref_logits=ref)
+
+
+# ---------------------------------------------------------------- LM-head inputs
+@dataclasses.dataclass
+class LmBatch:
+    """Inputs of the LM-head-fused forward: `batch` carries the metadata and the
+    per-token inputs (its `logits` is None), plus hidden [T, d] and weight [V, d]."""
+    batch: Batch
+    hidden: torch.Tensor        # bf16 [T, d]
+    weight: torch.Tensor        # bf16 [V, d]
+
+
+def make_lmhead(name, d, seed=0, device="cpu", V=None, layout=None, exact=False, inv_temperature=1.0,
+                chunk_rows=2048):
+    """Seeded LM-head inputs with the logit statistics of make_batch's recipe.
+
+    realistic (exact=False): W_v ~ N(0, I/d) so |W_v| ~ 1; h_t = sigma_t eps_t +
+      b_t W_{v*_t} with eps ~ N(0, I_d) and (sigma, b, v*) drawn as in
+      make_batch (routine vs fork steps); then z_tv = h_t . W_v ~ sigma N(0,1)
+      + b [v == v*] (+ O(b / sqrt(d)) cross terms) -- the same peaked/flat
+      mix, now produced by a matrix product.  Both operands rounded to bf16.
+    exact=True: h in {-2..2}, W in {-4..4}/64 -- every partial sum of h.W is a
+      multiple of 1/64 below 2^13 in magnitude, so any fp32 summation order is
+      exact and the tensor-core logits equal the float64 ones bit for bit.
+    Targets: Gumbel-max on z / T (z from an fp32 matmul of the bf16 operands,
+    a realism helper like _approx_target_logp, not part of either side)."""
+    if layout is None:
+        layout, V0, _, _ = config_layout(name, seed)
+        V = V or V0
+    T = layout.T
+    dev = torch.device(device)
+    gen = torch.Generator(device=dev)
+    gen.manual_seed(seed * 7919 + 11)
+    rng = np.random.default_rng(seed * 31 + 17)
+    if exact:
+        hidden = torch.randint(-2, 3, (T, d), generator=gen, device=dev).to(torch.bfloat16)
+        weight = (torch.randint(-4, 5, (V, d), generator=gen, device=dev).float() / 64.0).to(torch.bfloat16)
+    else:
+        weight = (torch.randn((V, d), generator=gen, device=dev) / float(np.sqrt(d))).to(torch.bfloat16)
+        step_of_tok = np.repeat(np.arange(layout.S), np.diff(layout.step_tok_off))
+        fork_tok = layout.step_fork[step_of_tok]
+        sigma_step = np.where(layout.step_fork, rng.uniform(1.0, 4.0, layout.S), 1.0)
+        sigma = torch.from_numpy(sigma_step[step_of_tok].astype(np.float32)).to(dev)
+        b = torch.from_numpy(np.where(fork_tok, rng.uniform(0.0, 15.0, T),
+                                      rng.uniform(17.0, 30.0, T)).astype(np.float32)).to(dev)
+        vstar = torch.from_numpy(rng.integers(0, V, T)).to(dev)
+        hidden = torch.empty((T, d), dtype=torch.bfloat16, device=dev)
+        for r0 in range(0, T, chunk_rows):
+            r1 = min(T, r0 + chunk_rows)
+            h = torch.randn((r1 - r0, d), generator=gen, device=dev) * sigma[r0:r1, None]
+            h += b[r0:r1, None] * weight[vstar[r0:r1]].float()
+            hidden[r0:r1] = h.to(torch.bfloat16)
+    target = torch.empty(T, dtype=torch.int32, device=dev)
+    logp = torch.empty(T, dtype=torch.float32, device=dev)
+    wf = weight.float()
+    for r0 in range(0, T, chunk_rows):
+        r1 = min(T, r0 + chunk_rows)
+        z = hidden[r0:r1].float() @ wf.T
+        u = torch.rand(z.shape, generator=gen, device=dev, dtype=torch.float32).clamp_(1e-20, 1.0)
+        y = torch.argmax(z * inv_temperature - torch.log(-torch.log(u)), dim=1)
+        target[r0:r1] = y.to(torch.int32)
+        logp[r0:r1] = _approx_target_logp(z, y, inv_temperature)
+        del z, u
+    d_old = torch.from_numpy(rng.normal(0, 0.15, T).astype(np.float32)).to(dev)
+    mix = rng.random(T) < 0.03
+    d_roll = np.where(mix, rng.normal(0, 1.0, T), rng.normal(0, 0.02, T)).astype(np.float32)
+    d_ref = torch.from_numpy(rng.normal(0, 0.1, T).astype(np.float32)).to(dev)
+    logp_old = torch.clamp(logp + d_old, max=0.0)
+    logp_roll = torch.clamp(logp_old + torch.from_numpy(d_roll).to(dev), max=0.0)
+    logp_ref = torch.clamp(logp + d_ref, max=0.0)
+    bt = Batch(layout=layout, V=V, logits=None, target=target, logp_old=logp_old, logp_rollout=logp_roll,
+               logp_ref=logp_ref, name=name)
+    return LmBatch(batch=bt, hidden=hidden, weight=weight)

@@ -47,7 +47,7 @@ def test_sm100a_cubin_inside():
 
 def test_version_and_status_strings(L):
     from paper_2509_23866_b200 import dart
-    assert L.dart_abi_version() == dart.ABI_VERSION == 3
+    assert L.dart_abi_version() == dart.ABI_VERSION == 4
     for c in range(5):
         assert L.dart_status_str(c).startswith(b"DART_")
     assert L.dart_status_str(99) == b"DART_UNKNOWN_STATUS"
@@ -131,6 +131,32 @@ def test_workspace_size_is_host_only_and_monotone(L):
     m = dart.dart_meta.from_buffer_copy(meta); m.T = 40000
     w2 = L.dart_workspace_size(ctypes.byref(b), ctypes.byref(m), ctypes.byref(cfg))
     assert 0 < w1 < w2
+
+
+def test_lmhead_validation(L):
+    """dart_lmhead_fwd (SURVEY §8(f) #3) rejects bad LM-head operands before any launch."""
+    dart, cfg, meta, batch, out = _structs()
+    E = dart.DART_ERR_INVALID_ARG
+    fake = ctypes.c_void_p(0x100000)
+    good = dart.dart_lmhead(fake, ctypes.c_void_p(0x300000), 64, 64, 72)
+
+    def call(head, b=batch, c=cfg, ws_bytes=1 << 40):
+        return L.dart_lmhead_fwd(None if head is None else ctypes.byref(head), ctypes.byref(b), ctypes.byref(meta),
+                                 ctypes.byref(c), ctypes.byref(out), ctypes.c_void_p(0x200000), ws_bytes, None)
+    assert call(None) == E
+    for field, val in (("d", 0), ("d", 60), ("ld_h", 32), ("ld_w", 68), ("hidden", None),
+                       ("weight", ctypes.c_void_p(0x300008))):
+        h = dart.dart_lmhead.from_buffer_copy(good)
+        setattr(h, field, val)
+        assert call(h) == E, field
+    b = dart.dart_batch.from_buffer_copy(batch); b.logits = None            # logits are not needed here
+    assert call(good, b=b, ws_bytes=8) == dart.DART_ERR_WORKSPACE
+    c = dart.dart_cfg.from_buffer_copy(cfg); c.kl_mode = dart.KL_EXACT       # needs the reference logits
+    assert call(good, c=c) == dart.DART_ERR_UNSUPPORTED
+    b = dart.dart_batch.from_buffer_copy(batch); b.logits = None
+    w0 = L.dart_workspace_size(ctypes.byref(batch), ctypes.byref(meta), ctypes.byref(cfg))
+    w1 = L.dart_lmhead_workspace_size(ctypes.byref(good), ctypes.byref(b), ctypes.byref(meta), ctypes.byref(cfg))
+    assert w1 > w0
 
 
 def test_binding_refuses_cpu_tensors():
