@@ -404,6 +404,239 @@ def run_dart(args):
         dist.destroy_process_group()
 
 
+def tensor_peak():
+    try:
+        with open(PEAKS_PATH) as f:
+            j = json.load(f)
+        return float(j["bf16_tflops_sustained"]), float(j["bf16_tflops"]), "measured (MEASURED_PEAKS.json)"
+    except Exception:
+        return 2250.0, 2250.0, "fallback (B200_PROFILING.md nominal dense bf16)"
+
+
+def run_lmhead(args):
+    """the old-log-prob pass with the LM head fused in.
+    One step = dart_lmhead_fwd (z = h W^T on tcgen05 + log-softmax / entropy /
+    target log-prob in the epilogue, per-step entropies) + select, over the
+    config's tokens; the [T, V] logits never exist.  Timed beside it: the
+    unfused pipeline (cuBLAS bf16 GEMM writing the logits, then the same
+    forward + select over them)."""
+    from paper_2509_23866_b200 import build as B
+    if int(os.environ.get("RANK", "0")) == 0:
+        B.build()
+    world, rank, local = dist_setup(args)
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+    from paper_2509_23866_b200 import dart, synth
+    dev = torch.device("cuda", torch.cuda.current_device())
+    layout_r, V, _, _ = synth.config_layout(args.config, seed=args.seed)
+    glayout = global_layout(layout_r, world)
+    shards = [dart.Shard(r * layout_r.N_traj, (r + 1) * layout_r.N_traj, r * layout_r.S, (r + 1) * layout_r.S,
+                         r * layout_r.T, (r + 1) * layout_r.T) for r in range(world)]
+    me = shards[rank]
+    d = args.hidden
+    cfg = dart.Config(entropy_q=args.q, beta_kl=args.beta)
+    t0 = time.time()
+    lb = synth.make_lmhead(None, d, seed=args.seed * 1000 + rank, device=dev, layout=layout_r, V=V)
+    torch.cuda.synchronize()
+    log(f"[rank {rank}] generated hidden {layout_r.T} x {d} and W {V} x {d} in {time.time() - t0:.1f}s")
+    group = dist.group.WORLD if world > 1 else None
+    dl = dart.DartLoss(glayout, me, V, cfg, dev, group=group, world_shards=shards, with_grad=False)
+    b = lb.batch
+    inputs = (lb.hidden, lb.weight, b.target, b.logp_old, b.logp_rollout, b.logp_ref)
+    stream = torch.cuda.current_stream()
+
+    def step():
+        dl.forward_lmhead(*inputs)
+        dl.gather()
+        dl.select()
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    dl.status.zero_()
+    dl.launches = 0
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clk = ClockSampler(local)
+    clk.start()
+    time.sleep(0.15)
+    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    start.record(stream)
+    for _ in range(args.steps):
+        step()
+    end.record(stream)
+    torch.cuda.synchronize()
+    clocks = clk.stop()
+    elapsed_ms = start.elapsed_time(end)
+    launches = dl.launches
+    dl.check_status()
+    # kernel timing pass: events recorded by the library around the tcgen05 kernel
+    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(args.steps)]
+    for e in ev:
+        for x in e:
+            x.record(stream)
+    torch.cuda.synchronize()
+    for k in range(args.steps):
+        dart.set_timing_events(*ev[k])
+        step()
+    torch.cuda.synchronize()
+    dart.set_timing_events()
+    gemm_ms = statistics.mean(e[0].elapsed_time(e[1]) for e in ev)
+    ms = elapsed_ms / args.steps
+    if world > 1:
+        from paper_2509_23866_b200 import dist as D
+        t = torch.tensor([ms], dtype=torch.float64, device=dev)
+        D.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    value = glayout.T / (ms * 1e-3)
+    flops = 2.0 * me.T_loc * d * V
+    peak_s, peak_b, peak_src = tensor_peak()
+    achieved = flops / (gemm_ms * 1e-3) / 1e12
+    traffic = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+            traffic = json.load(f).get("lmhead_fwd", {}).get("dram_bytes_per_launch")
+    except Exception:
+        traffic = None
+
+    # ---- the unfused pipeline, timed beside it (cuBLAS GEMM -> bf16 logits -> same fwd + select)
+    unfused = None
+    if not args.no_unfused and rank == 0:
+        try:
+            logits = torch.empty((me.T_loc, V), dtype=torch.bfloat16, device=dev)
+            dl2 = dart.DartLoss(glayout, me, V, cfg, dev, with_grad=False)
+            k = max(3, min(args.steps, 10))
+
+            def ustep():
+                torch.matmul(lb.hidden, lb.weight.T, out=logits)
+                dl2.forward(logits, b.target, b.logp_old, b.logp_rollout, b.logp_ref)
+                dl2.select()
+            for _ in range(2):
+                ustep()
+            torch.cuda.synchronize()
+            s1, s2, s3 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
+            g_ms = []
+            s1.record(stream)
+            for _ in range(k):
+                ustep()
+            s2.record(stream)
+            torch.cuda.synchronize()
+            for _ in range(k):
+                a, c = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a.record(stream)
+                torch.matmul(lb.hidden, lb.weight.T, out=logits)
+                c.record(stream)
+                c.synchronize()
+                g_ms.append(a.elapsed_time(c))
+            u_ms = s1.elapsed_time(s2) / k
+            cub = statistics.mean(g_ms)
+            unfused = {"ms_per_step": u_ms, "tokens_per_s": me.T_loc / (u_ms * 1e-3), "cublas_gemm_ms": cub,
+                       "cublas_tflops": flops / (cub * 1e-3) / 1e12,
+                       "logits_bytes": me.T_loc * V * 2, "steps": k}
+            del logits, dl2
+            torch.cuda.empty_cache()
+        except torch.OutOfMemoryError:
+            unfused = {"skipped": "out of memory for the [T, V] bf16 logits"}
+
+    # ---- e2e: hidden states + per-token inputs from pinned host memory each step, step entropies back
+    e2e = None
+    if not args.no_e2e:
+        host = [t.cpu().pin_memory() for t in (lb.hidden, b.target, b.logp_old, b.logp_rollout, b.logp_ref)]
+        dbuf = [torch.empty_like(t, device=dev) for t in host]
+        out_h = torch.empty(me.S_loc, dtype=torch.float32).pin_memory()
+        h2d = sum(t.numel() * t.element_size() for t in host)
+
+        def one():
+            for x, hh in zip(dbuf, host):
+                x.copy_(hh, non_blocking=True)
+            dl.forward_lmhead(dbuf[0], lb.weight, *dbuf[1:])
+            dl.gather()
+            dl.select()
+            out_h.copy_(dl.step_H[:me.S_loc], non_blocking=True)
+        one()
+        torch.cuda.synchronize()
+        n = max(1, min(args.steps, args.e2e_steps))
+        a, c = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        for _ in range(n):
+            one()
+        c.record(stream)
+        torch.cuda.synchronize()
+        ems = a.elapsed_time(c) / n
+        if world > 1:
+            from paper_2509_23866_b200 import dist as D
+            t = torch.tensor([ems], dtype=torch.float64, device=dev)
+            D.all_reduce(t, op=dist.ReduceOp.MAX)
+            ems = float(t.item())
+        e2e = {"value": glayout.T / (ems * 1e-3), "unit": "tokens/s", "h2d_bytes_per_step": h2d,
+               "d2h_bytes_per_step": out_h.numel() * 4, "steps": n, "ms_per_step": ems,
+               "note": "weight stays resident (model parameter); hidden states and per-token inputs copied"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        cpu = lmhead_cpu_baseline(args, lb, cfg)
+
+    if rank == 0:
+        line = {
+            "metric": "LM-head-fused old-log-prob pass tokens/s (h W^T + log-softmax + entropy + select), "
+                      "V=152064, d=%d" % d,
+            "value": value, "unit": "tokens/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "bf16", "data": "synthetic (seeded; synth.make_lmhead recipe, DESIGN.md §9)",
+            "config": {"workload": args.config + " (LM-head-fused forward: NEXT #3)",
+                       "desc": CONFIG_DESC.get(args.config, args.config), "global_tokens": glayout.T,
+                       "tokens_per_gpu": me.T_loc, "V": V, "d": d,
+                       "l2": "inputs larger than L2 (W %.2f GB + hidden %.2f GB >> 126 MB)" % (
+                           V * d * 2 / 1e9, me.T_loc * d * 2 / 1e9),
+                       "parallelism": f"dp{world} (trajectory-sharded)"},
+            "roofline": {"bound": "tensor", "kernel": "lmhead_fwd_kernel", "achieved": achieved, "peak": peak_s,
+                         "peak_source": peak_src + " bf16_tflops_sustained (kernel inside a long step loop)",
+                         "unit": "TFLOP/s", "frac": achieved / peak_s, "frac_of_burst_peak": achieved / peak_b,
+                         "traffic": traffic, "traffic_unit": "DRAM bytes per launch (ncu); the tensor-bound kernel's operand re-reads hit L2 95%",
+                         "algorithmic_flops_per_launch": flops, "avg_launch_ms": gemm_ms},
+            "unfused_cublas_pipeline": unfused,
+            "gpu_launches": launches,
+            "clocks": clocks,
+            "e2e": e2e,
+            "cpu_baseline": cpu,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def lmhead_cpu_baseline(args, lb, cfg, rows=64):
+    """The oracle (float64 NumPy, BLAS limited to one thread) on the first
+    `rows` tokens: LM-head logits + log-softmax / entropy per token."""
+    from oracle import dart_oracle as O
+    try:
+        from threadpoolctl import threadpool_limits
+    except Exception:
+        threadpool_limits = None
+    h = lb.hidden[:rows].float().cpu().numpy()
+    W = lb.weight.float().cpu().numpy()
+    y = lb.batch.target[:rows].cpu().numpy()
+    invT = cfg.as_f32()["inv_temperature"]
+
+    def work():
+        z = O.lmhead_logits(h, W)
+        for t in range(rows):
+            O.token_row(z[t], int(y[t]), invT)
+    t0 = time.time()
+    if threadpool_limits is not None:
+        with threadpool_limits(limits=1):
+            work()
+    else:
+        work()
+    dt = time.time() - t0
+    return {"value": rows / dt, "unit": "tokens/s", "cores": 1, "kind": "oracle",
+            "sample": f"{rows} tokens: float64 h W^T (d={h.shape[1]}, V={W.shape[0]}) + per-token log-softmax / "
+                      f"entropy, NumPy with BLAS limited to 1 thread", "seconds": dt}
+
+
 def run_e2e(args, dl, batch, stream, world, inputs):
     """Same pass through the public API with the step's inputs copied from
     pinned host memory each step and the loss read back to the host."""
@@ -573,6 +806,10 @@ def main():
     ap.add_argument("--stream-rows", type=int, default=0,
                     help="chunk-stream the batch with chunks of at most this many rows (configs > HBM)")
     ap.add_argument("--pool", type=int, default=3, help="logits/dlogits pool buffers when streaming")
+    ap.add_argument("--lmhead", action="store_true",
+                    help="time the LM-head-fused old-log-prob pass (NEXT #3) instead of the loss pass")
+    ap.add_argument("--hidden", type=int, default=3584, help="hidden size d for --lmhead (Qwen2.5-7B: 3584)")
+    ap.add_argument("--no-unfused", action="store_true", help="--lmhead: skip the cuBLAS + logits comparison")
     ap.add_argument("--backend", default="nccl", choices=["nccl", "gloo"],
                     help="gloo: test path (ranks may share a GPU; collectives staged via host)")
     args = ap.parse_args()
@@ -581,6 +818,8 @@ def main():
         args.warmup = 3
     if args.impl == "reference":
         run_reference(args)
+    elif args.lmhead:
+        run_lmhead(args)
     elif args.stream_rows > 0:
         run_streamed(args)
     else:

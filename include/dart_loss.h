@@ -229,7 +229,10 @@ dart_status dart_select_steps(const float* step_entropy_gathered, const int64_t*
 /* Backward: local loss partial + statistics into *stats, then dL/dlogits for
  * the local rows: kept rows re-read once and written once, masked rows
  * written as zeros (zero_fill_masked=1) or skipped.  dlogits: [T_loc, ldg]
- * of grad_dtype, 16-byte aligned rows. */
+ * of grad_dtype, 16-byte aligned rows.
+ * dlogits == NULL: loss-only mode -- *stats (loss, counts, sums) without the
+ * gradient sweep; batch->logits / logits_dtype / ld / ref_logits and
+ * grad_dtype / ldg are then ignored (e.g. after dart_lmhead_fwd). */
 dart_status dart_loss_bwd(const dart_batch* batch, const dart_meta* meta, const dart_cfg* cfg,
                           const dart_fwd_out* fwd, const uint8_t* keep, const dart_norm* norm,
                           void* dlogits, int32_t grad_dtype, int64_t ldg, dart_stats* stats,

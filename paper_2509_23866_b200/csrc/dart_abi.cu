@@ -124,22 +124,24 @@ bool meta_ok(const dart_meta* m) {
   return true;
 }
 
-dart_status batch_check(const dart_batch* b, const dart_meta* m, const dart_cfg* c) {
+// need_logits = false: the logits fields are ignored (LM-head forward, loss-only bwd)
+dart_status batch_check(const dart_batch* b, const dart_meta* m, const dart_cfg* c, bool need_logits = true) {
   if (!b || !meta_ok(m) || !cfg_ok(c)) return DART_ERR_INVALID_ARG;
-  if (b->logits_dtype != DART_BF16 && b->logits_dtype != DART_F32) return DART_ERR_UNSUPPORTED;
-  if (b->T_loc < 0 || b->V < 1 || b->ld < b->V || b->S_loc < 0) return DART_ERR_INVALID_ARG;
+  if (need_logits && b->logits_dtype != DART_BF16 && b->logits_dtype != DART_F32) return DART_ERR_UNSUPPORTED;
+  if (b->T_loc < 0 || b->V < 1 || (need_logits && b->ld < b->V) || b->S_loc < 0) return DART_ERR_INVALID_ARG;
   if (b->V > 0x7fffffffLL) return DART_ERR_INVALID_ARG;
   if (b->tok_begin < 0 || b->tok_begin + b->T_loc > m->T) return DART_ERR_INVALID_ARG;
   if (b->step_begin < 0 || b->step_begin + b->S_loc > m->S) return DART_ERR_INVALID_ARG;
   if (b->T_loc > 0) {
-    if (!b->logits || !b->target || !b->logp_old || !b->logp_rollout) return DART_ERR_INVALID_ARG;
+    if ((need_logits && !b->logits) || !b->target || !b->logp_old || !b->logp_rollout) return DART_ERR_INVALID_ARG;
     if (c->beta_kl > 0.f && c->kl_mode == DART_KL_K3 && !b->logp_ref) return DART_ERR_INVALID_ARG;
-    if (c->beta_kl > 0.f && c->kl_mode == DART_KL_EXACT) {
+    if (need_logits && c->beta_kl > 0.f && c->kl_mode == DART_KL_EXACT) {
       if (!b->ref_logits || !aligned16(b->ref_logits) || b->ld_ref < b->V ||
           ((size_t)b->ld_ref * esize(b->logits_dtype)) % 16 != 0)
         return DART_ERR_INVALID_ARG;
     }
-    if (!aligned16(b->logits) || ((size_t)b->ld * esize(b->logits_dtype)) % 16 != 0) return DART_ERR_INVALID_ARG;
+    if (need_logits && (!aligned16(b->logits) || ((size_t)b->ld * esize(b->logits_dtype)) % 16 != 0))
+      return DART_ERR_INVALID_ARG;
     if (b->S_loc < 1) return DART_ERR_INVALID_ARG;
   }
   return DART_OK;
@@ -203,12 +205,8 @@ LmLayout lm_layout(const dart_batch* b, const dart_meta* m) {
 
 dart_status lmhead_check(const dart_lmhead* h, const dart_batch* b, const dart_meta* m, const dart_cfg* c) {
   if (!h || !b) return DART_ERR_INVALID_ARG;
-  dart_batch bb = *b;                     // the logits fields are not used on this path
-  bb.logits = h->hidden;
-  bb.logits_dtype = DART_BF16;
-  bb.ld = b->V + ((8 - b->V % 8) % 8);
   if (c && cfg_ok(c) && exact_kl(c)) return DART_ERR_UNSUPPORTED;   // needs the reference logits
-  dart_status st = batch_check(&bb, m, c);
+  dart_status st = batch_check(b, m, c, /*need_logits=*/false);
   if (st != DART_OK) return st;
   if (h->d < 8 || h->d % 8 != 0 || h->d > (1 << 20)) return DART_ERR_INVALID_ARG;
   if (h->ld_h < h->d || h->ld_w < h->d || h->ld_h % 8 != 0 || h->ld_w % 8 != 0) return DART_ERR_INVALID_ARG;
@@ -486,12 +484,13 @@ dart_status dart_select_steps(const float* gathered, const int64_t* rank_step_of
 dart_status dart_loss_bwd(const dart_batch* b, const dart_meta* m, const dart_cfg* c, const dart_fwd_out* f,
                           const uint8_t* keep, const dart_norm* norm, void* dlogits, int32_t grad_dtype,
                           int64_t ldg, dart_stats* stats, void* ws, size_t ws_bytes, void* stream) {
-  dart_status st = batch_check(b, m, c);
+  const bool loss_only = dlogits == nullptr;   // loss + statistics only: no gradient sweep, logits unused
+  dart_status st = batch_check(b, m, c, !loss_only);
   if (st != DART_OK) return st;
   if ((st = fwd_out_check(b, m, f)) != DART_OK) return st;
-  if (grad_dtype != DART_BF16 && grad_dtype != DART_F32) return DART_ERR_UNSUPPORTED;
+  if (!loss_only && grad_dtype != DART_BF16 && grad_dtype != DART_F32) return DART_ERR_UNSUPPORTED;
   if (!norm || !stats || (m->S > 0 && !keep)) return DART_ERR_INVALID_ARG;
-  if (b->T_loc > 0) {
+  if (b->T_loc > 0 && !loss_only) {
     if (!dlogits || ldg < b->V || !aligned16(dlogits) || ((size_t)ldg * esize(grad_dtype)) % 16 != 0)
       return DART_ERR_INVALID_ARG;
   }
@@ -518,7 +517,7 @@ dart_status dart_loss_bwd(const dart_batch* b, const dart_meta* m, const dart_cf
   pp.stats = stats;
   DART_TRY(launch_bwd_prep(pp, s));
 
-  if (b->T_loc > 0) {
+  if (b->T_loc > 0 && !loss_only) {
     RowRecParams rp;
     rp.T_loc = b->T_loc; rp.V = b->V; rp.ld_bytes = b->ld * (int64_t)es;
     rp.is_bf16 = b->logits_dtype == DART_BF16;

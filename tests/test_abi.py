@@ -117,7 +117,11 @@ def test_select_and_bwd_validation(L):
     assert bwd(5, 512) == dart.DART_ERR_UNSUPPORTED
     assert bwd(dart.DART_BF16, 511) == E
     assert bwd(dart.DART_BF16, 513) == E
-    assert bwd(dart.DART_BF16, 512, dl=None) == E
+    # dlogits = NULL is the loss-only mode: validation passes (ld / grad dtype ignored) up to the workspace
+    assert L.dart_loss_bwd(ctypes.byref(batch), ctypes.byref(meta), ctypes.byref(cfg), ctypes.byref(out), fake, fake,
+                           None, 5, 0, fake, ctypes.c_void_p(0x200000), 8, None) == dart.DART_ERR_WORKSPACE
+    assert L.dart_loss_bwd(ctypes.byref(batch), ctypes.byref(meta), ctypes.byref(cfg), ctypes.byref(out), fake, None,
+                           None, 5, 0, fake, ctypes.c_void_p(0x200000), 1 << 40, None) == E   # norm required
     # whole-batch convenience call requires the shard to be the whole batch
     b = dart.dart_batch.from_buffer_copy(batch); b.T_loc = 40
     assert L.dart_loss_pass(ctypes.byref(b), ctypes.byref(meta), ctypes.byref(cfg), ctypes.byref(out), fake, fake,

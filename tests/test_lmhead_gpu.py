@@ -159,3 +159,26 @@ def test_lmhead_rejects_bad_operands():
     with pytest.raises(dart.DartError):       # d = 60: rows not 16-byte multiples
         dl.forward_lmhead(lb.hidden.cuda()[:, :60], lb.weight.cuda()[:, :60], b.target.cuda(), b.logp_old.cuda(),
                           b.logp_rollout.cuda(), b.logp_ref.cuda())
+
+
+def test_lmhead_loss_only_backward_matches_oracle_loss():
+    """dart_lmhead_fwd -> select -> dart_loss_bwd(dlogits = NULL): the loss and
+    statistics of the pass without any [T, V] tensor (exact operands)."""
+    lb = synth.make_lmhead("grid4x4x3x20@3000", 256, seed=11, exact=True)
+    cfg = dart.Config(entropy_q=0.3)
+    dl, _ = run_lm(lb, cfg)
+    dl.backward()
+    torch.cuda.synchronize()
+    dl.check_status()
+    cfgf = cfg.as_f32()
+    ob = lb.batch.oracle_dict(logits=False)
+    ob["logits"] = O.lmhead_logits(lb.hidden.float().numpy(), lb.weight.float().numpy())
+    keep = dl.keep.cpu().numpy()[:lb.batch.layout.S]
+    ref = O.loss_pass(ob, cfgf, keep_override=keep, want_grad=False)
+    st = dl.stats_dict()
+    scale = float(np.sum(np.abs(ref["c_tok"] * ref["ell"]))) + 1e-300
+    assert abs(st["loss"] - ref["loss"]) <= RTOL_ENT * scale + 1e-12, (st["loss"], ref["loss"])
+    for k in ("n_tok", "n_kept_tok", "n_kept_step"):
+        assert st[k] == ref["stats"][k], k
+    for k in ("sum_w", "sum_adv", "sum_H", "sum_kl"):
+        assert abs(st[k] - ref["stats"][k]) <= 1e-5 * (abs(ref["stats"][k]) + 1.0), k
