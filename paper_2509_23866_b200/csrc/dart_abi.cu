@@ -2,6 +2,7 @@
 // validation, the workspace layout, and the kernel launch sequence.
 // Never allocates, never synchronises; every launch goes to `stream`.
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 
 #include "dart_common.cuh"
@@ -168,6 +169,15 @@ dart_status cuda_status(cudaError_t e) {
 // log2 of the number of warps a row is split over: only for few rows, and
 // only when every canonical segment is non-empty (rows >= KSEG chunks)
 inline bool exact_kl(const dart_cfg* c) { return c->kl_mode == DART_KL_EXACT && c->beta_kl > 0.f; }
+
+// dart_loss_fused kernel: 0 = L2 re-read variant (default, faster: 8.9 M
+// tokens/s), 1 = cluster / distributed-shared-memory true single read (5.9 M:
+// per-row exchange and lock-stepped phases starve MUFU);
+// env DART_FUSED_VARIANT
+int fused_variant() {
+  const char* e = getenv("DART_FUSED_VARIANT");
+  return (e && e[0] == '1') ? 1 : 0;
+}
 
 int choose_lg_nsplit(const dart_batch* b, const WsLayout& L, int64_t nvec) {
   if (!L.split_alloc || nvec < (int64_t)KSEG * CH_VEC) return 0;
@@ -634,9 +644,14 @@ dart_status dart_loss_fused(const dart_batch* b, const dart_meta* m, const dart_
     fp.aux_flags = at<uint8_t>(ws, L.aux_flags);
     fp.status = o->status;
     fp.rec = at<uint8_t>(ws, L.fused_rec);
+    fp.dbg = nullptr;
+    if (const char* d = getenv("DART_FC_DBG")) fp.dbg = reinterpret_cast<unsigned long long*>(strtoull(d, nullptr, 0));
     DART_TRY(launch_fused_rec(fp, s));
     rec(2, s);
-    DART_TRY(launch_fused_sweep(fp, fp.is_bf16, grad_dtype == DART_BF16, sm_count(), s));
+    if (fused_cluster_ok(fp) && fused_variant() == 1)
+      DART_TRY(launch_fused_cluster(fp, grad_dtype == DART_BF16, sm_count(), s));
+    else
+      DART_TRY(launch_fused_sweep(fp, fp.is_bf16, grad_dtype == DART_BF16, sm_count(), s));
     rec(3, s);
 
     StepReduceParams sp;

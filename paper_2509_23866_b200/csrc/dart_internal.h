@@ -190,6 +190,7 @@ struct FusedParams {
   uint8_t* aux_flags;
   uint32_t* status;
   void* rec;                    // [T_loc] 32-byte row records (fused_rec_kernel)
+  unsigned long long* dbg;      // timing experiments only (DART_FC_EXP == 5), else NULL
 };
 
 // LM-head-fused forward (dart_lmhead.cu)
@@ -221,6 +222,8 @@ cudaError_t launch_lmhead(const void* hidden, int64_t ld_h, const void* weight, 
 cudaError_t launch_lmhead_combine(const FwdParams& p, const LmCombineParams& c, cudaStream_t st);
 
 cudaError_t launch_fused_rec(const FusedParams& p, cudaStream_t st);
+bool fused_cluster_ok(const FusedParams& p);      // bf16 logits and a row quarter fits one row buffer
+cudaError_t launch_fused_cluster(const FusedParams& p, bool out_bf16, int num_sms, cudaStream_t st);
 cudaError_t launch_fwd_kl(const FwdParams& p, bool bf16, int num_sms, cudaStream_t st);
 cudaError_t launch_rowrec_kl(const RowRecParams& p, cudaStream_t st);
 cudaError_t launch_bwd_kl(const BwdParams& p, bool in_bf16, bool out_bf16, int num_sms, cudaStream_t st);

@@ -13,6 +13,14 @@ from tests.gpu_helpers import ATOL_ENT, ATOL_LOGP, ATOL_TOK, P_REL, RTOL_ENT, RT
 pytestmark = pytest.mark.gpu
 
 
+@pytest.fixture(params=["1", "0"], ids=["cluster", "l2reread"], autouse=True)
+def fused_variant(request, monkeypatch):
+    """Both dart_loss_fused kernels: the cluster / distributed-shared-memory
+    single read (default for bf16 logits) and the L2 re-read variant."""
+    monkeypatch.setenv("DART_FUSED_VARIANT", request.param)
+    return request.param
+
+
 def _fused_case(name, cfg, seed=0, grad_dtype=None, rows=None, **kw):
     b = synth.make_batch(name, seed=seed, **kw)
     old = run_gpu(b, cfg, grad_dtype=grad_dtype)          # old-policy pass -> mask + norm
