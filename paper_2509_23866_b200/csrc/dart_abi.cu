@@ -525,6 +525,7 @@ dart_status dart_loss_bwd(const dart_batch* b, const dart_meta* m, const dart_cf
   pp.step_cost = at<int64_t>(ws, L.step_cost);
   pp.step_chunk = at<int64_t>(ws, L.step_chunk);
   pp.stats = stats;
+  pp.no_stats = 0;
   DART_TRY(launch_bwd_prep(pp, s));
 
   if (b->T_loc > 0 && !loss_only) {
@@ -622,6 +623,7 @@ dart_status dart_loss_fused(const dart_batch* b, const dart_meta* m, const dart_
   pp.step_cost = at<int64_t>(ws, L.step_cost);
   pp.step_chunk = at<int64_t>(ws, L.step_chunk);
   pp.stats = stats;
+  pp.no_stats = b->T_loc > 0 ? 1 : 0;   // the step sums come from the sweep below; stats in the second call
   DART_TRY(launch_bwd_prep(pp, s));
 
   if (b->T_loc > 0) {
@@ -666,6 +668,7 @@ dart_status dart_loss_fused(const dart_batch* b, const dart_meta* m, const dart_
     sp.logp = o->logp; sp.logp_old = b->logp_old; sp.logp_roll = b->logp_rollout; sp.logp_ref = b->logp_ref;
     sp.eps_low = c->eps_low; sp.eps_high = c->eps_high; sp.is_cap = c->is_cap; sp.beta = c->beta_kl;
     DART_TRY(launch_step_reduce(sp, s));
+    pp.no_stats = 0;
     DART_TRY(launch_bwd_prep(pp, s));   // loss partial + statistics from the step sums
   }
   g_last_launches = g_launches;

@@ -59,8 +59,8 @@ __global__ void __launch_bounds__(1024) bwd_prep_kernel(BwdPrepParams p) {
       nchunks = (kept || p.zero_fill) ? (long long)n * p.nch : 0;
       const double* st = p.step_stats + s * NSTAT;
       v[1] = (double)n;          // n_tok
-      v[9] = st[6];              // sum_H (all tokens)
-      if (kept) {
+      if (!p.no_stats) v[9] = st[6];   // sum_H (all tokens)
+      if (kept && !p.no_stats) {
         v[0] = c * p.step_ell[s];  // loss partial
         v[2] = (double)n;
         v[3] = 1.0;
@@ -121,7 +121,7 @@ __global__ void __launch_bounds__(1024) bwd_prep_kernel(BwdPrepParams p) {
     }
     __syncthreads();
   }
-  if (tid == 0) {
+  if (tid == 0 && !p.no_stats) {
     dart_stats* o = reinterpret_cast<dart_stats*>(p.stats);
     o->loss = tot[0];
     o->n_tok = tot[1];

@@ -131,6 +131,7 @@ struct BwdPrepParams {
   int64_t* step_cost;    // [S_loc+1] prefix of chunk costs (kept 2, masked 1 or 0)
   int64_t* step_chunk;   // [S_loc+1] prefix of chunks that need work
   void* stats;           // dart_stats*
+  int no_stats;          // 1: step_scale / step_cost / step_chunk only (step sums not yet written)
 };
 
 struct RowRecParams {

@@ -13,6 +13,41 @@ for name in which:
     elif name == "midsplit":   # V = 152064, few rows -> split-row mode + bulk copies of full chunks
         layout, _, _, _ = synth.config_layout("grid1x2x2x16@152064", seed=0)
         b = synth.make_batch("x", seed=0, layout=layout, V=152064, dtype=torch.bfloat16)
+    elif name == "lmhead":   # NEXT #3: tcgen05 / TMA / TMEM kernel + combine, ragged rows and vocabulary
+        lb = synth.make_lmhead("grid2x4x3x20@3000", 256, seed=3, exact=True)
+        bb = lb.batch
+        dl = dart.DartLoss(bb.layout, dart.whole_shard(bb.layout), bb.V, dart.Config(), "cuda", with_grad=False)
+        dl.forward_lmhead(lb.hidden.cuda(), lb.weight.cuda(), bb.target.cuda(), bb.logp_old.cuda(),
+                          bb.logp_rollout.cuda(), bb.logp_ref.cuda())
+        dl.select()
+        dl.backward()
+        torch.cuda.synchronize()
+        dl.check_status()
+        print(name, "ok", dl.stats_dict()["loss"])
+        continue
+    elif name in ("fused", "fused_cluster"):   # NEXT #1 (both kernels)
+        import os
+        os.environ["DART_FUSED_VARIANT"] = "1" if name == "fused_cluster" else "0"
+        layout, _, _, _ = synth.config_layout("grid2x2x3x24@30000", seed=0)
+        b = synth.make_batch("x", seed=0, layout=layout, V=30000, dtype=torch.bfloat16)
+        old = run_gpu(b, dart.Config())
+        dl = dart.DartLoss(b.layout, dart.whole_shard(b.layout), b.V, dart.Config(), "cuda")
+        dl.fused(b.logits.cuda(), b.target.cuda(), b.logp_old.cuda(), b.logp_rollout.cuda(), b.logp_ref.cuda(),
+                 keep=old.keep, norm=old.norm)
+        torch.cuda.synchronize()
+        dl.check_status()
+        print(name, "ok", dl.stats_dict()["loss"])
+        continue
+    elif name == "klexact":  # NEXT #4
+        b = synth.make_batch("small_multi", seed=0, with_ref=True)
+        dl = dart.DartLoss(b.layout, dart.whole_shard(b.layout), b.V, dart.Config(kl_mode=dart.KL_EXACT), "cuda",
+                           logits_dtype=b.logits.dtype, grad_dtype=torch.float32 if b.logits.dtype == torch.float32 else torch.bfloat16)
+        dl.run(b.logits.cuda(), b.target.cuda(), b.logp_old.cuda(), b.logp_rollout.cuda(), b.logp_ref.cuda(),
+               b.ref_logits.cuda())
+        torch.cuda.synchronize()
+        dl.check_status()
+        print(name, "ok", dl.stats_dict()["loss"])
+        continue
     else:
         b = synth.make_batch(name, seed=0)
     dl = run_gpu(b, dart.Config(is_cap=2.0 if name.startswith("tiny") else 1.0))
