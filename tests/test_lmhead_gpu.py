@@ -182,3 +182,48 @@ def test_lmhead_loss_only_backward_matches_oracle_loss():
         assert st[k] == ref["stats"][k], k
     for k in ("sum_w", "sum_adv", "sum_H", "sum_kl"):
         assert abs(st[k] - ref["stats"][k]) <= 1e-5 * (abs(ref["stats"][k]) + 1.0), k
+
+
+def test_lmhead_sharded_equals_unsharded():
+    """Trajectory shards (virtual ranks, all-gather emulated by concatenation):
+    each row's (m, s, u) is folded by one thread in tile order and chunk order,
+    so every per-token value is bitwise the unsharded one."""
+    from paper_2509_23866_b200 import dist as D
+    lb = synth.make_lmhead("grid4x4x3x20@3000", 256, seed=13)
+    b = lb.batch
+    cfg = dart.Config()
+    ref, _ = run_lm(lb, cfg)
+    shards = D.shard_layout(b.layout, 3)
+    dls = []
+    for sh in shards:
+        dl = dart.DartLoss(b.layout, sh, b.V, cfg, "cuda", group=False, world_shards=shards, with_grad=False)
+        sl = slice(sh.tok_begin, sh.tok_end)
+        dl.forward_lmhead(lb.hidden[sl].cuda().contiguous(), lb.weight.cuda(), b.target[sl].cuda().contiguous(),
+                          b.logp_old[sl].cuda().contiguous(), b.logp_rollout[sl].cuda().contiguous(),
+                          b.logp_ref[sl].cuda().contiguous())
+        dls.append(dl)
+    S_pad = dls[0].S_pad
+    gathered = torch.zeros(len(shards) * S_pad, dtype=torch.float32, device="cuda")
+    for r, (dl, sh) in enumerate(zip(dls, shards)):
+        gathered[r * S_pad: r * S_pad + sh.S_loc] = dl.step_H[:sh.S_loc]
+    for dl in dls:
+        dl.set_gathered(gathered)
+        dl.select()
+    torch.cuda.synchronize()
+    for dl, sh in zip(dls, shards):
+        dl.check_status()
+        sl = slice(sh.tok_begin, sh.tok_end)
+        assert torch.equal(dl.keep[:b.layout.S], ref.keep[:b.layout.S])
+        for a, c in ((dl.lse, ref.lse[sl]), (dl.logp, ref.logp[sl]), (dl.H, ref.H[sl]), (dl.ell, ref.ell[sl])):
+            assert torch.equal(a, c)
+
+
+def test_lmhead_full_vocab_exact_operands():
+    """V = 152064 (594 tiles, 75 vocabulary chunks, last chunk 2 tiles) with
+    exact operands and a small d: every output against the oracle at the
+    logits sweep's tolerances."""
+    layout = synth.config_layout("grid1x2x2x40@152064")[0]          # T = 160 rows (2 blocks, ragged)
+    lb = synth.make_lmhead(None, 64, seed=17, layout=layout, V=synth.V_QWEN, exact=True)
+    cfg = dart.Config(entropy_q=0.3)
+    dl, _ = run_lm(lb, cfg)
+    compare_lm(dl, lb, cfg, exact=True)
