@@ -286,6 +286,21 @@ dart_status dart_lmhead_fwd(const dart_lmhead* head, const dart_batch* batch, co
                             const dart_cfg* cfg, const dart_fwd_out* out, void* workspace, size_t ws_bytes,
                             void* stream);
 
+/* Plain GEMM step of the LM-head backward:
+ *   C[M, N] = A[M, K] * B[N, K]^T   (c_mode STORE_F32 / STORE_BF16)
+ *   C[M, N] += A[M, K] * B[N, K]^T  (c_mode ACCUM_F32)
+ * bf16 operands, fp32 accumulation on the tensor cores.  Operand storage
+ * (device, 16-byte aligned, row pitch in elements, pitch % 8 == 0):
+ *   a_mn_major = 0: A is row-major [M, K] (lda >= K); 1: A^T is stored,
+ *   row-major [K, M] (lda >= M).  Likewise B: 0 = [N, K], 1 = [K, N].
+ * C: device, row-major [M, ldc] of fp32 (STORE_F32, ACCUM_F32) or bf16,
+ * 16-byte aligned, ldc >= N, N % 8 == 0, ldc % 8 == 0.  Asynchronous on
+ * `stream`; no workspace. */
+typedef enum { DART_GEMM_STORE_F32 = 0, DART_GEMM_STORE_BF16 = 1, DART_GEMM_ACCUM_F32 = 2 } dart_gemm_mode;
+dart_status dart_gemm_bf16(const void* A, int32_t a_mn_major, int64_t lda, const void* B, int32_t b_mn_major,
+                           int64_t ldb, void* C, int32_t c_mode, int64_t ldc, int64_t M, int64_t N, int64_t K,
+                           void* stream);
+
 /* Single-rank convenience: fwd + select (world = 1) + bwd on one stream. */
 dart_status dart_loss_pass(const dart_batch* batch, const dart_meta* meta, const dart_cfg* cfg,
                            const dart_fwd_out* fwd, uint8_t* keep, float* tau, dart_norm* norm,

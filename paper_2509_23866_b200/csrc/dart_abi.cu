@@ -675,6 +675,22 @@ dart_status dart_loss_fused(const dart_batch* b, const dart_meta* m, const dart_
   return DART_OK;
 }
 
+dart_status dart_gemm_bf16(const void* A, int32_t a_mn, int64_t lda, const void* B, int32_t b_mn, int64_t ldb,
+                           void* C, int32_t c_mode, int64_t ldc, int64_t M, int64_t N, int64_t K, void* stream) {
+  if (c_mode != DART_GEMM_STORE_F32 && c_mode != DART_GEMM_STORE_BF16 && c_mode != DART_GEMM_ACCUM_F32)
+    return DART_ERR_UNSUPPORTED;
+  const int64_t lim = (int64_t)1 << 31;
+  if (M < 1 || N < 1 || K < 1 || M >= lim || N >= lim || K >= lim) return DART_ERR_INVALID_ARG;
+  if (!A || !B || !C || !aligned16(A) || !aligned16(B) || !aligned16(C)) return DART_ERR_INVALID_ARG;
+  if (lda % 8 != 0 || ldb % 8 != 0 || ldc % 8 != 0 || N % 8 != 0 || ldc < N) return DART_ERR_INVALID_ARG;
+  if (lda < (a_mn ? M : K) || ldb < (b_mn ? N : K)) return DART_ERR_INVALID_ARG;
+  g_launches = 0;
+  DART_TRY(launch_gemm_bf16(A, a_mn != 0, lda, B, b_mn != 0, ldb, C, c_mode, ldc, M, N, K, sm_count(),
+                            static_cast<cudaStream_t>(stream)));
+  g_last_launches = g_launches;
+  return DART_OK;
+}
+
 dart_status dart_loss_pass(const dart_batch* b, const dart_meta* m, const dart_cfg* c, const dart_fwd_out* f,
                            uint8_t* keep, float* tau, dart_norm* norm, void* dlogits, int32_t grad_dtype,
                            int64_t ldg, dart_stats* stats, void* ws, size_t ws_bytes, void* stream) {

@@ -1,0 +1,253 @@
+// dart_gemm.cu -- the plain GEMM steps of the LM-head backward (SURVEY §8(f)
+// NEXT #3): C[M, N] (+)= A[M, K] * B[N, K]^T, bf16 operands, fp32 accumulation
+// on the 5th-generation tensor cores (sm_100a).
+//
+// Either operand may be K-major (row-major [rows, K]) or MN-major (row-major
+// [K, rows], i.e. the transpose is stored), so the three products of the
+// LM head need no transposed copies:
+//    logits  z  = h  W^T    A = h  [T, d] K-major,   B = W [V, d] K-major
+//    dh         = dz W      A = dz [T, V] K-major,   B = W [V, d] MN-major (N = d contiguous)
+//    dW        += dz^T h    A = dz [T, V] MN-major,  B = h [T, d] MN-major
+//
+// Same machinery as the LM-head forward kernel (dart_lmhead.cu): persistent
+// CTAs, warp 0 = TMA producer into a 4-stage ring of 128-byte-swizzled tiles
+// (K-major: one 64 x rows box; MN-major: 64 x 64 boxes 8 KB apart along MN),
+// warp 1 = TMEM allocator + tcgen05.mma issuer (M = 128, N = 256, K = 16 per
+// instruction), warps 2..5 = epilogue from two TMEM accumulators (fp32 store,
+// bf16 store or fp32 read-add-write).  Tiles are rastered in groups of
+// GM_GROUP row blocks for L2 reuse of the B panel.
+#include "dart_common.cuh"
+#include "dart_internal.h"
+#include "dart_tc.cuh"
+
+namespace dart {
+namespace {
+
+constexpr int GM_BM = 128, GM_BN = 256, GM_BK = 64, GM_STAGES = 4, GM_ACC = 2, GM_THREADS = 192;
+constexpr uint32_t GM_A_BYTES = GM_BM * GM_BK * 2;   // 16 KB
+constexpr uint32_t GM_B_BYTES = GM_BN * GM_BK * 2;   // 32 KB
+constexpr uint32_t GM_STAGE_BYTES = GM_A_BYTES + GM_B_BYTES;
+constexpr size_t GM_SMEM = 1024 + (size_t)GM_STAGES * GM_STAGE_BYTES + 256;
+constexpr uint32_t GM_TMEM_COLS = GM_ACC * GM_BN;
+constexpr int GM_GROUP = 16;                        // row blocks per raster group
+
+struct GemmParams {
+  int M, N, K;
+  int n_mt, n_nt;
+  int64_t n_tiles;
+  int c_mode;          // DART_GEMM_STORE_F32 / _STORE_BF16 / _ACCUM_F32
+  void* C;
+  int64_t ldc;         // elements
+};
+
+__device__ __forceinline__ void gm_tile(const GemmParams& p, int64_t t, int& mt, int& nt) {
+  const int64_t per_group = (int64_t)GM_GROUP * p.n_nt;
+  const int g = (int)(t / per_group);
+  const int r = (int)(t - (int64_t)g * per_group);
+  const int m0 = g * GM_GROUP;
+  const int gm = min(GM_GROUP, p.n_mt - m0);
+  mt = m0 + r % gm;
+  nt = r / gm;
+}
+
+template <bool A_MN, bool B_MN>
+__global__ void __launch_bounds__(GM_THREADS, 1)
+    gemm_bf16_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                     const GemmParams p) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + GM_STAGES * GM_A_BYTES;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + GM_STAGES * GM_STAGE_BYTES);
+  uint64_t* empty = full + GM_STAGES;
+  uint64_t* tfull = empty + GM_STAGES;
+  uint64_t* tempty = tfull + GM_ACC;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + GM_ACC);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < GM_STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int a = 0; a < GM_ACC; ++a) {
+      mbar_init(&tfull[a], 1);
+      mbar_init(&tempty[a], 4);
+    }
+    fence_mbar_init();
+    tc::tma_prefetch_desc(&tmA);
+    tc::tma_prefetch_desc(&tmB);
+  }
+  if (warp == 1) tc::tmem_alloc(tmem_slot, GM_TMEM_COLS);
+  tc::fence_before();
+  __syncthreads();
+  tc::fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const int KB = (p.K + GM_BK - 1) / GM_BK;
+
+  if (warp == 0) {
+    // ---------------------------------------------------------- TMA producer
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t ph = 0;
+      for (int64_t t = blockIdx.x; t < p.n_tiles; t += gridDim.x) {
+        int mt, nt;
+        gm_tile(p, t, mt, nt);
+        for (int kb = 0; kb < KB; ++kb) {
+          mbar_wait(&empty[stage], ph ^ 1u);
+          mbar_arrive_expect_tx(&full[stage], GM_STAGE_BYTES);
+          uint8_t* a = sA + stage * GM_A_BYTES;
+          uint8_t* b = sB + stage * GM_B_BYTES;
+          if (A_MN) {
+            tc::tma_load_2d(a, &tmA, &full[stage], mt * GM_BM, kb * GM_BK);
+            tc::tma_load_2d(a + 8192, &tmA, &full[stage], mt * GM_BM + 64, kb * GM_BK);
+          } else {
+            tc::tma_load_2d(a, &tmA, &full[stage], kb * GM_BK, mt * GM_BM);
+          }
+          if (B_MN) {
+#pragma unroll
+            for (int q = 0; q < GM_BN / 64; ++q)
+              tc::tma_load_2d(b + q * 8192, &tmB, &full[stage], nt * GM_BN + 64 * q, kb * GM_BK);
+          } else {
+            tc::tma_load_2d(b, &tmB, &full[stage], kb * GM_BK, nt * GM_BN);
+          }
+          if (++stage == GM_STAGES) {
+            stage = 0;
+            ph ^= 1u;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ---------------------------------------------------------- MMA issuer
+    if (lane == 0) {
+      constexpr uint32_t idesc = tc::idesc_bf16_f32(GM_BM, GM_BN, A_MN, B_MN);
+      constexpr uint32_t a_lbo = A_MN ? 8192u : 16u, b_lbo = B_MN ? 8192u : 16u;
+      constexpr uint64_t a_kstep = A_MN ? (2048u >> 4) : (32u >> 4);   // one K step of 16
+      constexpr uint64_t b_kstep = B_MN ? (2048u >> 4) : (32u >> 4);
+      int stage = 0, acc = 0;
+      uint32_t ph = 0, aph = 0;
+      for (int64_t t = blockIdx.x; t < p.n_tiles; t += gridDim.x) {
+        mbar_wait(&tempty[acc], aph ^ 1u);
+        tc::fence_after();
+        const uint32_t d_tmem = tmem + (uint32_t)(acc * GM_BN);
+        for (int kb = 0; kb < KB; ++kb) {
+          mbar_wait(&full[stage], ph);
+          tc::fence_after();
+          const uint64_t da = tc::smem_desc_sw128(smem_u32(sA + stage * GM_A_BYTES), a_lbo, 1024);
+          const uint64_t db = tc::smem_desc_sw128(smem_u32(sB + stage * GM_B_BYTES), b_lbo, 1024);
+#pragma unroll
+          for (int k = 0; k < GM_BK / 16; ++k)
+            tc::umma_bf16(d_tmem, da + a_kstep * k, db + b_kstep * k, idesc, (kb | k) != 0 ? 1u : 0u);
+          tc::umma_commit(&empty[stage]);
+          if (++stage == GM_STAGES) {
+            stage = 0;
+            ph ^= 1u;
+          }
+        }
+        tc::umma_commit(&tfull[acc]);
+        if (++acc == GM_ACC) {
+          acc = 0;
+          aph ^= 1u;
+        }
+      }
+    }
+  } else {
+    // ---------------------------------------------------------- epilogue
+    const int q = warp & 3;
+    const int r = q * 32 + lane;
+    int acc = 0;
+    uint32_t aph = 0;
+    for (int64_t t = blockIdx.x; t < p.n_tiles; t += gridDim.x) {
+      int mt, nt;
+      gm_tile(p, t, mt, nt);
+      mbar_wait(&tfull[acc], aph);
+      tc::fence_after();
+      const int64_t m = (int64_t)mt * GM_BM + r;
+      const uint32_t tbase = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * GM_BN);
+#pragma unroll 1
+      for (int j = 0; j < GM_BN / 32; ++j) {
+        float x[32];
+        tc::tmem_ld32(tbase + (uint32_t)(j * 32), x);
+        const int64_t n0 = (int64_t)nt * GM_BN + j * 32;
+        if (m >= p.M || n0 >= p.N) continue;
+        if (p.c_mode == DART_GEMM_STORE_BF16) {
+          __nv_bfloat16* c = reinterpret_cast<__nv_bfloat16*>(p.C) + m * p.ldc + n0;
+#pragma unroll
+          for (int i = 0; i < 32; i += 8) {
+            if (n0 + i + 8 <= p.N) {
+              *reinterpret_cast<uint4*>(c + i) = make_uint4(pack_bf16x2(x[i], x[i + 1]), pack_bf16x2(x[i + 2], x[i + 3]),
+                                                            pack_bf16x2(x[i + 4], x[i + 5]),
+                                                            pack_bf16x2(x[i + 6], x[i + 7]));
+            }
+          }
+        } else {
+          float* c = reinterpret_cast<float*>(p.C) + m * p.ldc + n0;
+#pragma unroll
+          for (int i = 0; i < 32; i += 4) {
+            if (n0 + i + 4 <= p.N) {
+              float4 v = make_float4(x[i], x[i + 1], x[i + 2], x[i + 3]);
+              if (p.c_mode == DART_GEMM_ACCUM_F32) {
+                const float4 o = *reinterpret_cast<const float4*>(c + i);
+                v.x += o.x; v.y += o.y; v.z += o.z; v.w += o.w;
+              }
+              *reinterpret_cast<float4*>(c + i) = v;
+            }
+          }
+        }
+      }
+      tc::fence_before();
+      __syncwarp();
+      if (lane == 0) tc::mbar_arrive1(&tempty[acc]);
+      if (++acc == GM_ACC) {
+        acc = 0;
+        aph ^= 1u;
+      }
+    }
+  }
+  tc::fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc::fence_after();
+    tc::tmem_dealloc(tmem, GM_TMEM_COLS);
+  }
+}
+
+template <bool A_MN, bool B_MN>
+cudaError_t launch_gemm_t(const CUtensorMap& ta, const CUtensorMap& tb, const GemmParams& p, int num_sms,
+                          cudaStream_t st) {
+  auto kern = gemm_bf16_kernel<A_MN, B_MN>;
+  static bool attr = false;   // per instantiation
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)GM_SMEM);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  const int64_t grid = p.n_tiles < num_sms ? p.n_tiles : num_sms;
+  kern<<<(unsigned)grid, GM_THREADS, GM_SMEM, st>>>(ta, tb, p);
+  return cudaGetLastError();
+}
+
+}  // namespace
+
+cudaError_t launch_gemm_bf16(const void* A, bool a_mn, int64_t lda, const void* B, bool b_mn, int64_t ldb, void* C,
+                             int c_mode, int64_t ldc, int64_t M, int64_t N, int64_t K, int num_sms, cudaStream_t st) {
+  if (M <= 0 || N <= 0) return cudaSuccess;
+  CUtensorMap ta, tb;
+  const bool ok_a = a_mn ? tc::make_map_bf16(&ta, A, K, M, lda, 64, 64) : tc::make_map_bf16(&ta, A, M, K, lda, 64, GM_BM);
+  const bool ok_b = b_mn ? tc::make_map_bf16(&tb, B, K, N, ldb, 64, 64) : tc::make_map_bf16(&tb, B, N, K, ldb, 64, GM_BN);
+  if (!ok_a || !ok_b) return cudaErrorInvalidValue;
+  GemmParams p;
+  p.M = (int)M; p.N = (int)N; p.K = (int)K;
+  p.n_mt = (int)((M + GM_BM - 1) / GM_BM);
+  p.n_nt = (int)((N + GM_BN - 1) / GM_BN);
+  p.n_tiles = (int64_t)p.n_mt * p.n_nt;
+  p.c_mode = c_mode;
+  p.C = C;
+  p.ldc = ldc;
+  if (a_mn && b_mn) return launch_gemm_t<true, true>(ta, tb, p, num_sms, st);
+  if (a_mn) return launch_gemm_t<true, false>(ta, tb, p, num_sms, st);
+  if (b_mn) return launch_gemm_t<false, true>(ta, tb, p, num_sms, st);
+  return launch_gemm_t<false, false>(ta, tb, p, num_sms, st);
+}
+
+}  // namespace dart

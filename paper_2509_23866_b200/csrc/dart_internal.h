@@ -221,6 +221,8 @@ struct LmCombineParams {
 cudaError_t launch_lmhead(const void* hidden, int64_t ld_h, const void* weight, int64_t ld_w, const LmParams& p,
                           int num_sms, cudaStream_t st);
 cudaError_t launch_lmhead_combine(const FwdParams& p, const LmCombineParams& c, cudaStream_t st);
+cudaError_t launch_gemm_bf16(const void* A, bool a_mn, int64_t lda, const void* B, bool b_mn, int64_t ldb, void* C,
+                             int c_mode, int64_t ldc, int64_t M, int64_t N, int64_t K, int num_sms, cudaStream_t st);
 
 cudaError_t launch_fused_rec(const FusedParams& p, cudaStream_t st);
 bool fused_cluster_ok(const FusedParams& p);      // bf16 logits and a row quarter fits one row buffer

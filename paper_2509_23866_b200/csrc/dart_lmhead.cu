@@ -22,11 +22,9 @@
 // lanes 32*(w%4) .. +31, i.e. accumulator rows).  Pipelines: LM_STAGES smem
 // stages (full/empty mbarriers), two TMEM accumulators of 256 fp32 columns
 // (tfull/tempty), so the epilogue of tile i overlaps the MMAs of tile i+1.
-#include <cuda.h>
-#include <cudaTypedefs.h>
-
 #include "dart_common.cuh"
 #include "dart_internal.h"
+#include "dart_tc.cuh"
 
 namespace dart {
 namespace {
@@ -40,74 +38,22 @@ constexpr size_t LM_SMEM = 1024 + (size_t)LM_STAGES * LM_STAGE_BYTES + 256;
 constexpr uint32_t LM_TMEM_COLS = LM_ACC * LM_BN;     // 512: the whole TMEM of the SM
 constexpr float LM_MASKED = -1.0e30f;                 // raw logit for columns >= V
 
-// ---------------------------------------------------------------- PTX
-__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
-}
+using tc::fence_after;
+using tc::fence_before;
+using tc::tma_load_2d;
+using tc::tma_prefetch_desc;
+using tc::tmem_ld32;
+using tc::umma_commit;
 
-__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1) {
-  asm volatile(
-      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];" ::"r"(
-          smem_u32(dst)),
-      "l"(map), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
-      : "memory");
-}
+constexpr uint32_t LM_IDESC = tc::idesc_bf16_f32(LM_BM, LM_BN, false, false);
 
-__device__ __forceinline__ void tma_prefetch_desc(const CUtensorMap* map) {
-  asm volatile("prefetch.tensormap [%0];" ::"l"(map) : "memory");
-}
-
-// Shared-memory matrix descriptor of a K-major, 128-byte-swizzled tile as TMA
-// writes it: rows of 64 bf16 (128 B) at a 128 B pitch, 8-row core groups
-// 1024 B apart (SBO), LBO unused for swizzled K-major, descriptor version 1
-// (sm_100), layout type 2 = SWIZZLE_128B.  Tiles are 1024-byte aligned, so
-// the base offset is 0.
-__device__ __forceinline__ uint64_t sw128_kmajor_desc(uint32_t saddr) {
-  uint64_t d = 0;
-  d |= (uint64_t)((saddr >> 4) & 0x3FFFu);
-  d |= (uint64_t)1u << 16;
-  d |= (uint64_t)(1024u >> 4) << 32;
-  d |= (uint64_t)1u << 46;
-  d |= (uint64_t)2u << 61;
-  return d;
-}
-
-// Instruction descriptor, kind::f16: fp32 accumulator (c_format=1), bf16 A
-// and B (format 1), both K-major, N>>3 at bit 17, M>>4 at bit 24.
-constexpr uint32_t LM_IDESC = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(LM_BN >> 3) << 17) |
-                              ((uint32_t)(LM_BM >> 4) << 24);
-
+__device__ __forceinline__ uint64_t sw128_kmajor_desc(uint32_t saddr) { return tc::smem_desc_sw128(saddr, 16, 1024); }
 __device__ __forceinline__ void umma_bf16(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t accumulate) {
-  asm volatile(
-      "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
-      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
-      "l"(da), "l"(db), "r"(LM_IDESC), "r"(accumulate));
+  tc::umma_bf16(tmem_d, da, db, LM_IDESC, accumulate);
 }
-
-__device__ __forceinline__ void umma_commit(uint64_t* bar) {
-  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
-               : "memory");
-}
-
-__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
-__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
-
-// 32 consecutive fp32 columns of this thread's TMEM lane (row).
-__device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&x)[32]) {
-  uint32_t v[32];
-  asm volatile(
-      "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
-      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
-      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
-      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
-        "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]),
-        "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]),
-        "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
-      : "r"(taddr));
-  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-#pragma unroll
-  for (int i = 0; i < 32; ++i) x[i] = __uint_as_float(v[i]);
-}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) { tc::mbar_arrive1(bar); }
+__device__ __forceinline__ void tc_fence_after() { fence_after(); }
+__device__ __forceinline__ void tc_fence_before() { fence_before(); }
 
 // work item -> (row block, vocabulary chunk): super-columns of group_nc chunks,
 // row blocks outer, chunks inner
@@ -312,42 +258,14 @@ __global__ void __launch_bounds__(LM_THREADS, 1)
   }
 }
 
-// ---------------------------------------------------------------- host
-PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
-  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
-  if (!fn) {
-    void* ptr = nullptr;
-    cudaDriverEntryPointQueryResult q;
-    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q) == cudaSuccess &&
-        q == cudaDriverEntryPointSuccess)
-      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(ptr);
-  }
-  return fn;
-}
-
-// 2-D bf16 tensor map over a row-major [rows, K] matrix (K contiguous),
-// box = 64 (K) x box_rows, 128-byte swizzle, zero fill out of bounds.
-bool make_map(CUtensorMap* m, const void* base, int64_t rows, int64_t K, int64_t ld, uint32_t box_rows) {
-  auto enc = encode_fn();
-  if (!enc) return false;
-  cuuint64_t dims[2] = {(cuuint64_t)K, (cuuint64_t)rows};
-  cuuint64_t strides[1] = {(cuuint64_t)ld * 2};
-  cuuint32_t box[2] = {(cuuint32_t)LM_BK, box_rows};
-  cuuint32_t es[2] = {1, 1};
-  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, es,
-                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  return r == CUDA_SUCCESS;
-}
-
 }  // namespace
 
 cudaError_t launch_lmhead(const void* hidden, int64_t ld_h, const void* weight, int64_t ld_w, const LmParams& p,
                           int num_sms, cudaStream_t st) {
   if (p.T_loc <= 0 || p.n_items <= 0) return cudaSuccess;
   CUtensorMap tmA, tmB;
-  if (!make_map(&tmA, hidden, p.T_loc, p.K, ld_h, LM_BM)) return cudaErrorInvalidValue;
-  if (!make_map(&tmB, weight, p.V, p.K, ld_w, LM_BN)) return cudaErrorInvalidValue;
+  if (!tc::make_map_bf16(&tmA, hidden, p.T_loc, p.K, ld_h, LM_BK, LM_BM)) return cudaErrorInvalidValue;
+  if (!tc::make_map_bf16(&tmB, weight, p.V, p.K, ld_w, LM_BK, LM_BN)) return cudaErrorInvalidValue;
   static bool attr = false;
   if (!attr) {
     cudaError_t e = cudaFuncSetAttribute(lmhead_fwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)LM_SMEM);

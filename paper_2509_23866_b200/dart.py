@@ -78,8 +78,29 @@ STATS_FIELDS = ["loss", "n_tok", "n_kept_tok", "n_kept_step", "sum_clip", "sum_t
 _lib = None
 
 EXPORTED = ["dart_workspace_size", "dart_loss_fwd", "dart_select_steps", "dart_loss_bwd", "dart_loss_fused",
-            "dart_loss_pass", "dart_lmhead_workspace_size", "dart_lmhead_fwd",
+            "dart_loss_pass", "dart_lmhead_workspace_size", "dart_lmhead_fwd", "dart_gemm_bf16",
             "dart_status_str", "dart_abi_version", "dart_last_launch_count", "dart_set_timing_events"]
+
+
+GEMM_STORE_F32, GEMM_STORE_BF16, GEMM_ACCUM_F32 = 0, 1, 2
+
+
+def gemm_bf16(A, B, C, a_mn_major=False, b_mn_major=False, mode=GEMM_STORE_F32, stream=None):
+    """C (+)= A_op @ B_op^T on the tensor cores (dart_gemm_bf16).  A_op is A
+    ([M, K]) or, with a_mn_major, A.T where A is stored [K, M]; likewise B_op
+    ([N, K] or B stored [K, N]).  C: fp32 (STORE_F32 / ACCUM_F32) or bf16 [M, N]."""
+    _require_cuda(A, B, C)
+    if A.dtype != torch.bfloat16 or B.dtype != torch.bfloat16:
+        raise DartError("gemm_bf16 takes bf16 operands")
+    if A.stride(1) != 1 or B.stride(1) != 1 or C.stride(1) != 1:
+        raise DartError("row-major operands expected")
+    M, K = (A.shape[1], A.shape[0]) if a_mn_major else (A.shape[0], A.shape[1])
+    N, Kb = (B.shape[1], B.shape[0]) if b_mn_major else (B.shape[0], B.shape[1])
+    if K != Kb or tuple(C.shape) != (M, N):
+        raise DartError(f"shape mismatch: A_op [{M}, {K}], B_op [{N}, {Kb}], C {tuple(C.shape)}")
+    st = (stream or torch.cuda.current_stream(C.device)).cuda_stream
+    _check(lib().dart_gemm_bf16(_ptr(A), int(a_mn_major), A.stride(0), _ptr(B), int(b_mn_major), B.stride(0),
+                                _ptr(C), int(mode), C.stride(0), M, N, K, ctypes.c_void_p(st)))
 
 
 class DartError(RuntimeError):
@@ -124,6 +145,10 @@ def lib():
     L.dart_lmhead_fwd.restype = ctypes.c_int
     L.dart_lmhead_fwd.argtypes = [P(dart_lmhead), P(dart_batch), P(dart_meta), P(dart_cfg), P(dart_fwd_out),
                                   ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p]
+    L.dart_gemm_bf16.restype = ctypes.c_int
+    L.dart_gemm_bf16.argtypes = [ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64, ctypes.c_void_p, ctypes.c_int32,
+                                 ctypes.c_int64, ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64, ctypes.c_int64,
+                                 ctypes.c_int64, ctypes.c_int64, ctypes.c_void_p]
     L.dart_status_str.restype = ctypes.c_char_p
     L.dart_status_str.argtypes = [ctypes.c_int]
     L.dart_abi_version.restype = ctypes.c_int32

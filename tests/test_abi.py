@@ -23,7 +23,7 @@ def L():
 def declared_functions():
     src = open(HEADER).read()
     src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
-    return sorted(set(re.findall(r"\b(dart_[a-z_]+)\s*\(", src)))
+    return sorted(set(re.findall(r"\b(dart_[a-z0-9_]+)\s*\(", src)))
 
 
 def test_header_declares_the_three_calls():
