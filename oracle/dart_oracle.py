@@ -296,6 +296,16 @@ def lmhead_logits(hidden, weight):
     return h @ W.T
 
 
+def lmhead_grads(dz, hidden, weight):
+    """Chain rule through z = h W^T (training half): given
+    dL/dz [T, V] (loss_pass's dz rows), dL/dh = dz W  [T, d] and
+    dL/dW = dz^T h  [V, d].  Plain float64 matrix products."""
+    dz = np.asarray(dz, dtype=np.float64)
+    h = np.asarray(hidden, dtype=np.float64)
+    W = np.asarray(weight, dtype=np.float64)
+    return dz @ W, dz.T @ h
+
+
 def token_loss(logp, logp_old, logp_roll, logp_ref, A, cfg):
     """ell_t = -w * min(rA, clip(r)A) + beta * KL_k3  -- the library minimises
     L = -J_HE (Eq. 2; SURVEY Q3 the IS weight multiplies the

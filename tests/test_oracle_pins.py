@@ -669,3 +669,37 @@ def test_lmhead_logits_special_cases():
     z0 = O.lmhead_logits(h, np.zeros((9, 6)))
     lse, logp, H, p = O.token_row(z0[0], 3)
     assert abs(H - math.log(9)) < 1e-14 and abs(logp + math.log(9)) < 1e-14
+
+
+def test_lmhead_grads_match_torch_autograd_through_the_head():
+    """dh = dz W and dW = dz^T h against float64 torch autograd of the whole
+    loss composed with z = h W^T (an independent derivation: torch's own
+    matmul backward and our loss written as torch ops)."""
+    rng = np.random.default_rng(42)
+    b = _random_batch(rng, V=6)
+    T = len(b["target"])
+    d = 5
+    h = rng.normal(0, 1, (T, d))
+    W = rng.normal(0, 0.7, (6, d))
+    b = dict(b)
+    b["logits"] = O.lmhead_logits(h, W)
+    cfg = dict(entropy_q=0.3, beta_kl=0.1, is_cap=1.5, inv_temperature=0.9)
+    out = O.loss_pass(b, cfg)
+    dz = np.stack([out["dz"][t] for t in range(T)])
+    dh, dW = O.lmhead_grads(dz, h, W)
+    c = {**O.DEFAULT_CFG, **cfg}
+    ht = torch.tensor(h, requires_grad=True)
+    Wt = torch.tensor(W, requires_grad=True)
+    z = ht @ Wt.T
+    logp = torch.log_softmax(z * c["inv_temperature"], -1).gather(1, torch.tensor(b["target"])[:, None])[:, 0]
+    lo, lr, lref = (torch.tensor(b[k]) for k in ("logp_old", "logp_rollout", "logp_ref"))
+    A = torch.tensor(out["A_tok"])
+    w = torch.clamp(torch.exp(lo - lr), max=c["is_cap"])
+    r = torch.exp(logp - lo)
+    sur = torch.minimum(r * A, torch.clamp(r, 1 - c["eps_low"], 1 + c["eps_high"]) * A)
+    dd = lref - logp
+    L = torch.sum(torch.tensor(out["c_tok"]) * (-w * sur + c["beta_kl"] * (torch.exp(dd) - dd - 1)))
+    L.backward()
+    assert abs(L.item() - out["loss"]) < 1e-12
+    assert np.allclose(dh, ht.grad.numpy(), rtol=1e-10, atol=1e-13)
+    assert np.allclose(dW, Wt.grad.numpy(), rtol=1e-10, atol=1e-13)
