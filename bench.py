@@ -608,6 +608,119 @@ def run_lmhead(args):
         dist.destroy_process_group()
 
 
+def run_lmhead_update(args):
+    """SURVEY §8(f) NEXT #3, training half: the update pass through the LM head
+    with the mask from the (untimed) old-log-prob pass.  One step = per chunk
+    z = h W^T, fused loss + dz, dh = dz W, dW += dz^T h (three tcgen05 GEMMs +
+    the fused sweep).  Timed beside it: cuBLAS (torch.matmul) for the three
+    products with the full [T, V] logits / gradient materialised + the same
+    fused loss kernel."""
+    from paper_2509_23866_b200 import build as B
+    B.build()
+    world, rank, local = dist_setup(args)
+    if world > 1:
+        raise SystemExit("--lmhead --update is single-GPU (chunks are virtual ranks)")
+    from paper_2509_23866_b200 import dart, lmhead, synth
+    dev = torch.device("cuda", torch.cuda.current_device())
+    layout, V, _, _ = synth.config_layout(args.config, seed=args.seed)
+    d = args.hidden
+    cfg = dart.Config(entropy_q=args.q, beta_kl=args.beta)
+    lb = synth.make_lmhead(None, d, seed=args.seed * 1000, device=dev, layout=layout, V=V)
+    b = lb.batch
+    old = dart.DartLoss(layout, dart.whole_shard(layout), V, cfg, dev, with_grad=False)
+    old.forward_lmhead(lb.hidden, lb.weight, b.target, b.logp_old, b.logp_rollout, b.logp_ref)
+    old.select()
+    torch.cuda.synchronize()
+    keep, norm = old.keep.clone(), old.norm.clone()
+    del old
+    up = lmhead.LmHeadUpdate(layout, V, d, cfg, dev, chunk_rows=args.chunk_rows)
+    dh = torch.empty((layout.T, d), dtype=torch.float32, device=dev)
+    dW = torch.empty((V, d), dtype=torch.float32, device=dev)
+    args_in = (lb.hidden, lb.weight, b.target, b.logp_old, b.logp_rollout, b.logp_ref, keep, norm)
+    stream = torch.cuda.current_stream()
+
+    def step():
+        up.run(*args_in, dh=dh, dW=dW)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    up.status.zero_()
+    up.launches = 0
+    clk = ClockSampler(local)
+    clk.start()
+    time.sleep(0.15)
+    s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s0.record(stream)
+    for _ in range(args.steps):
+        step()
+    s1.record(stream)
+    torch.cuda.synchronize()
+    clocks = clk.stop()
+    up.check_status()
+    ms = s0.elapsed_time(s1) / args.steps
+    flops = 3 * 2.0 * layout.T * d * V
+    peak_s, peak_b, peak_src = tensor_peak()
+    achieved = flops / (ms * 1e-3) / 1e12
+    launches = up.launches // args.steps
+
+    unfused = None
+    if not args.no_unfused:
+        try:
+            logits = torch.empty((layout.T, V), dtype=torch.bfloat16, device=dev)
+            dl2 = dart.DartLoss(layout, dart.whole_shard(layout), V, cfg, dev)
+            dh2 = torch.empty((layout.T, d), dtype=torch.bfloat16, device=dev)
+            dW2 = torch.empty((V, d), dtype=torch.bfloat16, device=dev)
+
+            def ustep():
+                torch.matmul(lb.hidden, lb.weight.T, out=logits)
+                g = dl2.fused(logits, b.target, b.logp_old, b.logp_rollout, b.logp_ref, keep=keep, norm=norm)
+                torch.matmul(g, lb.weight, out=dh2)
+                torch.matmul(g.T, lb.hidden, out=dW2)
+            for _ in range(2):
+                ustep()
+            torch.cuda.synchronize()
+            k = max(3, min(args.steps, 5))
+            a, c = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            for _ in range(k):
+                ustep()
+            c.record(stream)
+            torch.cuda.synchronize()
+            u_ms = a.elapsed_time(c) / k
+            unfused = {"ms_per_step": u_ms, "tokens_per_s": layout.T / (u_ms * 1e-3),
+                       "tflops": flops / (u_ms * 1e-3) / 1e12,
+                       "hbm_bytes_materialised": 2 * layout.T * V * 2, "steps": k,
+                       "what": "torch.matmul (cuBLAS) bf16 logits [T, V] -> dart_loss_fused -> cuBLAS dh, dW"}
+            del logits, dl2, dh2, dW2
+            torch.cuda.empty_cache()
+        except torch.OutOfMemoryError:
+            unfused = {"skipped": "out of memory for the [T, V] logits + gradient"}
+
+    line = {
+        "metric": "LM-head update pass tokens/s (z = h W^T, fused loss + dz, dh = dz W, dW = dz^T h), "
+                  "V=152064, d=%d" % d,
+        "value": layout.T / (ms * 1e-3), "unit": "tokens/s", "n_gpus": 1, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "bf16", "data": "synthetic (seeded; synth.make_lmhead recipe, DESIGN.md §9)",
+        "config": {"workload": args.config + " (LM-head update pass: NEXT #3 training half)",
+                   "tokens": layout.T, "V": V, "d": d, "chunk_rows": args.chunk_rows, "chunks": len(up.chunks),
+                   "kept_token_frac": float(up.stats_dict()["n_kept_tok"]) / layout.T,
+                   "l2": "inputs larger than L2 (W %.2f GB, hidden %.2f GB, chunk logits %.2f GB)" % (
+                       V * d * 2 / 1e9, layout.T * d * 2 / 1e9, up.rows * V * 4 / 1e9),
+                   "parallelism": "dp1"},
+        "roofline": {"bound": "tensor", "kernel": "3 x gemm (whole step)", "achieved": achieved, "peak": peak_s,
+                     "peak_source": peak_src + " bf16_tflops_sustained", "unit": "TFLOP/s", "frac": achieved / peak_s,
+                     "traffic": None, "algorithmic_flops_per_step": flops},
+        "unfused_cublas_pipeline": unfused,
+        "gpu_launches": launches,
+        "clocks": clocks,
+        "e2e": None,
+        "cpu_baseline": None,
+    }
+    print(json.dumps(line), flush=True)
+
+
 def lmhead_cpu_baseline(args, lb, cfg, rows=64):
     """The oracle (float64 NumPy, BLAS limited to one thread) on the first
     `rows` tokens: LM-head logits + log-softmax / entropy per token."""
@@ -810,6 +923,8 @@ def main():
                     help="time the LM-head-fused old-log-prob pass (NEXT #3) instead of the loss pass")
     ap.add_argument("--hidden", type=int, default=3584, help="hidden size d for --lmhead (Qwen2.5-7B: 3584)")
     ap.add_argument("--no-unfused", action="store_true", help="--lmhead: skip the cuBLAS + logits comparison")
+    ap.add_argument("--update", action="store_true", help="--lmhead: time the update pass (dh, dW) instead")
+    ap.add_argument("--chunk-rows", type=int, default=8192, help="--lmhead --update: rows per chunk")
     ap.add_argument("--backend", default="nccl", choices=["nccl", "gloo"],
                     help="gloo: test path (ranks may share a GPU; collectives staged via host)")
     args = ap.parse_args()
@@ -818,6 +933,8 @@ def main():
         args.warmup = 3
     if args.impl == "reference":
         run_reference(args)
+    elif args.lmhead and args.update:
+        run_lmhead_update(args)
     elif args.lmhead:
         run_lmhead(args)
     elif args.stream_rows > 0:

@@ -53,7 +53,7 @@ class LmHeadUpdate:
     """Buffers + ABI sequence of the LM-head update pass for one shard."""
 
     def __init__(self, layout, V: int, d: int, cfg: dart.Config, device, shard: Optional[Shard] = None,
-                 chunk_rows: int = 4096):
+                 chunk_rows: int = 8192):
         if V % 8 or d % 8:
             raise dart.DartError("the LM-head update needs V % 8 == 0 and d % 8 == 0")
         self.L = dart.lib()
