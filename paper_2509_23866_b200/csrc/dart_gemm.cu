@@ -216,12 +216,8 @@ template <bool A_MN, bool B_MN>
 cudaError_t launch_gemm_t(const CUtensorMap& ta, const CUtensorMap& tb, const GemmParams& p, int num_sms,
                           cudaStream_t st) {
   auto kern = gemm_bf16_kernel<A_MN, B_MN>;
-  static bool attr = false;   // per instantiation
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)GM_SMEM);
-    if (e != cudaSuccess) return e;
-    attr = true;
-  }
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)GM_SMEM);
+  if (e != cudaSuccess) return e;   // (per call: the attribute is per device)
   const int64_t grid = p.n_tiles < num_sms ? p.n_tiles : num_sms;
   kern<<<(unsigned)grid, GM_THREADS, GM_SMEM, st>>>(ta, tb, p);
   return cudaGetLastError();

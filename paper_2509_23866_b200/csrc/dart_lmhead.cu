@@ -266,12 +266,8 @@ cudaError_t launch_lmhead(const void* hidden, int64_t ld_h, const void* weight, 
   CUtensorMap tmA, tmB;
   if (!tc::make_map_bf16(&tmA, hidden, p.T_loc, p.K, ld_h, LM_BK, LM_BM)) return cudaErrorInvalidValue;
   if (!tc::make_map_bf16(&tmB, weight, p.V, p.K, ld_w, LM_BK, LM_BN)) return cudaErrorInvalidValue;
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(lmhead_fwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)LM_SMEM);
-    if (e != cudaSuccess) return e;
-    attr = true;
-  }
+  cudaError_t e = cudaFuncSetAttribute(lmhead_fwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)LM_SMEM);
+  if (e != cudaSuccess) return e;   // (per call: the attribute is per device)
   const int64_t grid = p.n_items < num_sms ? p.n_items : num_sms;
   lmhead_fwd_kernel<<<(unsigned)grid, LM_THREADS, LM_SMEM, st>>>(tmA, tmB, p);
   return cudaGetLastError();
