@@ -168,3 +168,23 @@ def test_binding_refuses_cpu_tensors():
     from paper_2509_23866_b200 import dart
     with pytest.raises(dart.DartError):
         dart._require_cuda(torch.zeros(3))
+
+
+def test_gemm_validation(L):
+    """dart_gemm_bf16 rejects bad shapes / pitches / pointers before any launch."""
+    from paper_2509_23866_b200 import dart
+    f = ctypes.c_void_p(0x100000)
+    E = dart.DART_ERR_INVALID_ARG
+
+    def g(A=f, a_mn=0, lda=64, B=f, b_mn=0, ldb=64, C=f, mode=0, ldc=64, M=64, N=64, K=64):
+        return L.dart_gemm_bf16(A, a_mn, lda, B, b_mn, ldb, C, mode, ldc, M, N, K, None)
+    assert g(mode=7) == dart.DART_ERR_UNSUPPORTED
+    assert g(M=0) == E
+    assert g(N=60, ldc=64) == E                      # N % 8
+    assert g(lda=60) == E                            # pitch % 8
+    assert g(lda=32) == E                            # K-major A: lda < K
+    assert g(a_mn=1, lda=32, M=64) == E              # MN-major A: lda < M
+    assert g(b_mn=1, ldb=32, N=64) == E
+    assert g(C=None) == E
+    assert g(A=ctypes.c_void_p(0x100008)) == E       # misaligned
+    assert g(ldc=32) == E                            # ldc < N
