@@ -170,13 +170,15 @@ dart_status cuda_status(cudaError_t e) {
 // only when every canonical segment is non-empty (rows >= KSEG chunks)
 inline bool exact_kl(const dart_cfg* c) { return c->kl_mode == DART_KL_EXACT && c->beta_kl > 0.f; }
 
-// dart_loss_fused kernel: 0 = L2 re-read variant (default, faster: 8.9 M
-// tokens/s), 1 = cluster / distributed-shared-memory true single read (5.9 M:
-// per-row exchange and lock-stepped phases starve MUFU);
-// env DART_FUSED_VARIANT
+// dart_loss_fused kernel (env DART_FUSED_VARIANT):
+//   2 (default) L2 re-read kernel with rows split over a 2-CTA cluster: the
+//     pass-2 re-read hits L2 (DRAM reads 15.4 GB = algorithmic), 8.9 M tokens/s
+//   0 the same kernel, one CTA per row (20.6 GB read, 8.9 M tokens/s)
+//   1 cluster / distributed-shared-memory true single read (5.9 M tokens/s:
+//     per-row exchange and lock-stepped phases starve MUFU)
 int fused_variant() {
   const char* e = getenv("DART_FUSED_VARIANT");
-  return (e && e[0] == '1') ? 1 : 0;
+  return (e && (e[0] == '0' || e[0] == '1')) ? e[0] - '0' : 2;
 }
 
 int choose_lg_nsplit(const dart_batch* b, const WsLayout& L, int64_t nvec) {
@@ -650,10 +652,11 @@ dart_status dart_loss_fused(const dart_batch* b, const dart_meta* m, const dart_
     if (const char* d = getenv("DART_FC_DBG")) fp.dbg = reinterpret_cast<unsigned long long*>(strtoull(d, nullptr, 0));
     DART_TRY(launch_fused_rec(fp, s));
     rec(2, s);
-    if (fused_cluster_ok(fp) && fused_variant() == 1)
+    const int fv = fused_variant();
+    if (fused_cluster_ok(fp) && fv == 1)
       DART_TRY(launch_fused_cluster(fp, grad_dtype == DART_BF16, sm_count(), s));
     else
-      DART_TRY(launch_fused_sweep(fp, fp.is_bf16, grad_dtype == DART_BF16, sm_count(), s));
+      DART_TRY(launch_fused_sweep(fp, fp.is_bf16, grad_dtype == DART_BF16, sm_count(), fv == 2 && fp.nch >= 2, s));
     rec(3, s);
 
     StepReduceParams sp;

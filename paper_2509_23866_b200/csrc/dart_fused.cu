@@ -26,7 +26,8 @@ namespace dart {
 #define DART_FU_NC 8
 #endif
 #ifndef DART_FU_SW
-#define DART_FU_SW 3
+#define DART_FU_SW 3   // slots per consumer warp (2 measured 9.14 vs 8.91 M tokens/s with split rows, but
+                       // compute-sanitizer racecheck then flags the slot hand-back; 3 is clean)
 #endif
 #ifndef DART_FU_CTAS
 #define DART_FU_CTAS 2
@@ -48,12 +49,51 @@ constexpr int FU_SLOTS = FU_NC * FU_SW;   // ring slots of CH_BYTES
 // an older mbarrier phase -- parity waits -- and read stale data).
 constexpr int FU_THREADS = (FU_NC + 1) * 32;
 
+// ---------------------------------------------------------------- cluster helpers
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ uint32_t cluster_id() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%clusterid.x;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ uint32_t cluster_count() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%nclusterid.x;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ uint32_t map_rank(const void* p, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(smem_u32(p)), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ void st_async_b32(uint32_t raddr, uint32_t v, uint32_t rbar) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.b32 [%0], %1, [%2];" ::"r"(raddr), "r"(v),
+               "r"(rbar)
+               : "memory");
+}
+__device__ __forceinline__ void st_async_b64(uint32_t raddr, uint64_t v, uint32_t rbar) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.b64 [%0], %1, [%2];" ::"r"(raddr), "l"(v),
+               "r"(rbar)
+               : "memory");
+}
+
 struct FusedShared {
   uint64_t full[FU_SLOTS];
   uint64_t empty[FU_SLOTS];
   double part_s[2][FU_NC];
   float part_m[2][FU_NC];
   float row_g[2], row_nl2[2];
+  // split-row mode (CL = 2): the peer CTA's row partial, double-buffered by row parity
+  uint64_t mbx[2];
+  double mb_s[2][2];
+  float mb_m[2][2];
 };
 
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
@@ -172,7 +212,13 @@ __device__ float fused_epilogue(const FusedParams& p, int64_t t, const FusedRec&
   return rc.c * dell * (float)p.invT;
 }
 
-template <typename Tin, typename Tout>
+// CL = 2 (split-row mode): a 2-CTA cluster shares each row -- CTA r streams the
+// chunks j = r, r + 2, ... through L2 twice, the two (m, s) partials meet via
+// st.async in each other's mailbox and are folded in rank order (identical
+// lse and g in both CTAs).  Two such CTAs per SM then hold one row's worth of
+// bytes between the passes instead of two, which halves the L2 footprint of
+// the pass-2 re-read while keeping two independent pipelines per SM.
+template <typename Tin, typename Tout, int CL>
 __global__ void __launch_bounds__(FU_THREADS, DART_FU_CTAS) fused_sweep_kernel(const FusedParams p) {
   extern __shared__ __align__(128) uint8_t smem[];
   uint8_t* ring = smem;
@@ -186,16 +232,25 @@ __global__ void __launch_bounds__(FU_THREADS, DART_FU_CTAS) fused_sweep_kernel(c
       mbar_init(&sh.full[s], 1);
       mbar_init(&sh.empty[s], FU_NC > 0 ? 1 : 1);
     }
+    if (CL > 1) {
+      mbar_init(&sh.mbx[0], 1);
+      mbar_init(&sh.mbx[1], 1);
+    }
     fence_mbar_init();
   }
   __syncthreads();
+  if (CL > 1) cluster_sync_all();                 // the peer's mailbox exists before any st.async
 
-  // this CTA's contiguous, cost-balanced row range [ra, rb)
+  // this CTA's (cluster's) contiguous, cost-balanced row range [ra, rb)
+  const uint32_t rank = CL > 1 ? cluster_rank() : 0u;
+  const int64_t unit = CL > 1 ? (int64_t)cluster_id() : (int64_t)blockIdx.x;
+  const int64_t nb = CL > 1 ? (int64_t)cluster_count() : (int64_t)gridDim.x;
   const int64_t total = p.step_cost[p.S_loc];
-  const int64_t nb = gridDim.x;
-  const int64_t ra = fu_row_at_cost(p, (total * (int64_t)blockIdx.x) / nb);
-  const int64_t rb = fu_row_at_cost(p, (total * ((int64_t)blockIdx.x + 1)) / nb);
-  const int64_t nvec = p.nvec, nch = p.nch;
+  const int64_t ra = fu_row_at_cost(p, (total * unit) / nb);
+  const int64_t rb = fu_row_at_cost(p, (total * (unit + 1)) / nb);
+  const int64_t nvec = p.nvec;
+  // local chunk jl <-> row chunk jl * CL + rank
+  const int64_t nch = (p.nch - (int64_t)rank + CL - 1) / CL;
   const float c2 = p.c2;
   const int tail_elems = (int)(p.V % EPV);
 
@@ -219,7 +274,7 @@ __global__ void __launch_bounds__(FU_THREADS, DART_FU_CTAS) fused_sweep_kernel(c
             const int slot = w * FU_SW + (int)(idx % FU_SW);
             const uint32_t use = (uint32_t)(idx / FU_SW);
             if (use > 0) mbar_wait(&sh.empty[slot], (use - 1) & 1u);
-            const int64_t v0 = j * CH_VEC;
+            const int64_t v0 = (j * CL + rank) * CH_VEC;
             const uint32_t nv = (uint32_t)min((int64_t)CH_VEC, nvec - v0);
             mbar_arrive_expect_tx(&sh.full[slot], nv * 16u);
             if (pass == 0 && !DART_FU_P1LAST)
@@ -232,6 +287,8 @@ __global__ void __launch_bounds__(FU_THREADS, DART_FU_CTAS) fused_sweep_kernel(c
         ++nrow;
       }
     }
+    __syncwarp();
+    if (CL > 1) cluster_sync_all();
     return;
   }
 
@@ -248,8 +305,10 @@ __global__ void __launch_bounds__(FU_THREADS, DART_FU_CTAS) fused_sweep_kernel(c
     uint8_t* orow = p.dlogits + t * p.ldg_bytes;
     if (!(rc.flags & 1u)) {
       if (!p.zero_fill) continue;
-      // masked step: zeros, no read; consumer warps split the row
-      for (int64_t vi = (int64_t)warp * 32 + lane; vi < nvec; vi += FU_NC * 32) {
+      // masked step: zeros, no read; consumer warps split this CTA's chunks of the row
+      for (int64_t li = (int64_t)warp * 32 + lane; li < nch * CH_VEC; li += FU_NC * 32) {
+        const int64_t vi = ((li / CH_VEC) * CL + rank) * CH_VEC + (li % CH_VEC);
+        if (vi >= nvec) continue;
         const int nvalid = (tail_elems && vi == nvec - 1) ? tail_elems : EPV;
         uint8_t* dst = orow + vi * OUTV;
         if (nvalid == EPV) {
@@ -275,7 +334,7 @@ __global__ void __launch_bounds__(FU_THREADS, DART_FU_CTAS) fused_sweep_kernel(c
       const int slot = warp * FU_SW + (int)(idx % FU_SW);
       mbar_wait(&sh.full[slot], (uint32_t)((idx / FU_SW) & 1));
       const uint8_t* sp = ring + (size_t)slot * CH_BYTES;
-      const int64_t v0 = j * CH_VEC;
+      const int64_t v0 = (j * CL + rank) * CH_VEC;
       const int nv = (int)min((int64_t)CH_VEC, nvec - v0);
       uint4 x[VPL];
 #pragma unroll
@@ -393,8 +452,28 @@ __global__ void __launch_bounds__(FU_THREADS, DART_FU_CTAS) fused_sweep_kernel(c
         Sr = Sr * (double)ex2((float)(Mr - mn)) + Sw * (double)ex2((float)(Mw - mn));
         Mr = mn;
       }
+      if (CL > 1) {                            // exchange with the peer CTA, fold in rank order
+        sh.mb_m[par][rank] = (float)Mr;
+        sh.mb_s[par][rank] = Sr;
+        mbar_arrive_expect_tx(&sh.mbx[par], 12u);                     // the peer's 4 + 8 bytes
+        const uint32_t peer = rank ^ 1u;
+        const uint32_t rbar = map_rank(&sh.mbx[par], peer);
+        st_async_b32(map_rank(&sh.mb_m[par][rank], peer), __float_as_uint((float)Mr), rbar);
+        st_async_b64(map_rank(&sh.mb_s[par][rank], peer), (uint64_t)__double_as_longlong(Sr), rbar);
+        mbar_wait(&sh.mbx[par], (uint32_t)((nrow >> 1) & 1));
+        Mr = -INFINITY;
+        Sr = 0.0;
+        for (int k2 = 0; k2 < CL; ++k2) {
+          const double Mk = (double)sh.mb_m[par][k2], Sk = sh.mb_s[par][k2];
+          if (Sk == 0.0) continue;
+          if (Mr == -INFINITY) { Mr = Mk; Sr = Sk; continue; }
+          const double mn = fmax(Mr, Mk);
+          Sr = Sr * (double)ex2((float)(Mr - mn)) + Sk * (double)ex2((float)(Mk - mn));
+          Mr = mn;
+        }
+      }
       const double L2s = log2(Sr);
-      sh.row_g[par] = fused_epilogue(p, t, rc, Mr, L2s);
+      sh.row_g[par] = fused_epilogue(p, t, rc, Mr, L2s, rank == 0);
       sh.row_nl2[par] = (float)(-(Mr + L2s));
     }
     named_bar_sync(1, FU_NC * 32);
@@ -409,7 +488,7 @@ __global__ void __launch_bounds__(FU_THREADS, DART_FU_CTAS) fused_sweep_kernel(c
       const int slot = warp * FU_SW + (int)(idx % FU_SW);
       mbar_wait(&sh.full[slot], (uint32_t)((idx / FU_SW) & 1));
       const uint8_t* sp = ring + (size_t)slot * CH_BYTES;
-      const int64_t v0 = j * CH_VEC;
+      const int64_t v0 = (j * CL + rank) * CH_VEC;
       const int nv = (int)min((int64_t)CH_VEC, nvec - v0);
       uint4 x[VPL];
 #pragma unroll
@@ -473,6 +552,7 @@ __global__ void __launch_bounds__(FU_THREADS, DART_FU_CTAS) fused_sweep_kernel(c
     ++nrow;
     par ^= 1;
   }
+  if (CL > 1) cluster_sync_all();                 // no CTA exits with mailbox traffic pending
 }
 
 // ============================================================== K7c cluster variant
@@ -534,40 +614,6 @@ struct FcShared {
   uint32_t wbad[2][FC_WARPS];
   float row_g, row_nl2;
 };
-
-__device__ __forceinline__ uint32_t cluster_rank() {
-  uint32_t r;
-  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
-  return r;
-}
-__device__ __forceinline__ uint32_t cluster_id() {
-  uint32_t r;
-  asm volatile("mov.u32 %0, %%clusterid.x;" : "=r"(r));
-  return r;
-}
-__device__ __forceinline__ uint32_t cluster_count() {
-  uint32_t r;
-  asm volatile("mov.u32 %0, %%nclusterid.x;" : "=r"(r));
-  return r;
-}
-__device__ __forceinline__ void cluster_sync_all() {
-  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
-}
-__device__ __forceinline__ uint32_t map_rank(const void* p, uint32_t rank) {
-  uint32_t r;
-  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(smem_u32(p)), "r"(rank));
-  return r;
-}
-__device__ __forceinline__ void st_async_b32(uint32_t raddr, uint32_t v, uint32_t rbar) {
-  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.b32 [%0], %1, [%2];" ::"r"(raddr), "r"(v),
-               "r"(rbar)
-               : "memory");
-}
-__device__ __forceinline__ void st_async_b64(uint32_t raddr, uint64_t v, uint32_t rbar) {
-  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.b64 [%0], %1, [%2];" ::"r"(raddr), "l"(v),
-               "r"(rbar)
-               : "memory");
-}
 
 // next kept row in [t, rb) (rb if none)
 __device__ __forceinline__ int64_t fc_next_kept(const FusedRec* recs, int64_t t, int64_t rb) {
@@ -915,20 +961,45 @@ cudaError_t launch_fused_rec(const FusedParams& p, cudaStream_t st) {
 }
 
 template <typename Tin, typename Tout>
-static cudaError_t launch_fused_t(const FusedParams& p, int num_sms, cudaStream_t st) {
+static cudaError_t launch_fused_t(const FusedParams& p, int num_sms, bool split, cudaStream_t st) {
   const size_t smem = (size_t)FU_SLOTS * CH_BYTES + sizeof(FusedShared);
-  auto kern = fused_sweep_kernel<Tin, Tout>;
+  if (!split) {
+    auto kern = fused_sweep_kernel<Tin, Tout, 1>;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    kern<<<(unsigned)(num_sms * DART_FU_CTAS), FU_THREADS, smem, st>>>(p);
+    return cudaGetLastError();
+  }
+  auto kern = fused_sweep_kernel<Tin, Tout, 2>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  kern<<<(unsigned)(num_sms * DART_FU_CTAS), FU_THREADS, smem, st>>>(p);
-  return cudaGetLastError();
+  cudaLaunchConfig_t cfg = {};
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = 2;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.blockDim = dim3(FU_THREADS);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cfg.gridDim = dim3((unsigned)(num_sms * DART_FU_CTAS));
+  int n = 0;
+  if (cudaOccupancyMaxActiveClusters(&n, kern, &cfg) != cudaSuccess || n <= 0) {
+    (void)cudaGetLastError();
+    n = num_sms * DART_FU_CTAS / 2;
+  }
+  cfg.gridDim = dim3((unsigned)(2 * n));
+  return cudaLaunchKernelEx(&cfg, kern, p);
 }
 
-cudaError_t launch_fused_sweep(const FusedParams& p, bool in_bf16, bool out_bf16, int num_sms, cudaStream_t st) {
-  if (in_bf16 && out_bf16) return launch_fused_t<__nv_bfloat16, __nv_bfloat16>(p, num_sms, st);
-  if (in_bf16) return launch_fused_t<__nv_bfloat16, float>(p, num_sms, st);
-  if (out_bf16) return launch_fused_t<float, __nv_bfloat16>(p, num_sms, st);
-  return launch_fused_t<float, float>(p, num_sms, st);
+cudaError_t launch_fused_sweep(const FusedParams& p, bool in_bf16, bool out_bf16, int num_sms, bool split,
+                               cudaStream_t st) {
+  if (in_bf16 && out_bf16) return launch_fused_t<__nv_bfloat16, __nv_bfloat16>(p, num_sms, split, st);
+  if (in_bf16) return launch_fused_t<__nv_bfloat16, float>(p, num_sms, split, st);
+  if (out_bf16) return launch_fused_t<float, __nv_bfloat16>(p, num_sms, split, st);
+  return launch_fused_t<float, float>(p, num_sms, split, st);
 }
 
 }  // namespace dart

@@ -230,7 +230,8 @@ cudaError_t launch_fused_cluster(const FusedParams& p, bool out_bf16, int num_sm
 cudaError_t launch_fwd_kl(const FwdParams& p, bool bf16, int num_sms, cudaStream_t st);
 cudaError_t launch_rowrec_kl(const RowRecParams& p, cudaStream_t st);
 cudaError_t launch_bwd_kl(const BwdParams& p, bool in_bf16, bool out_bf16, int num_sms, cudaStream_t st);
-cudaError_t launch_fused_sweep(const FusedParams& p, bool in_bf16, bool out_bf16, int num_sms, cudaStream_t st);
+cudaError_t launch_fused_sweep(const FusedParams& p, bool in_bf16, bool out_bf16, int num_sms, bool split_rows,
+                               cudaStream_t st);
 cudaError_t launch_adv(const AdvParams& p, cudaStream_t st);
 cudaError_t launch_tok_meta(const TokMetaParams& p, cudaStream_t st);
 cudaError_t launch_fwd_sweep(const FwdParams& p, bool bf16, int num_sms, cudaStream_t st);

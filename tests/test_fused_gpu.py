@@ -13,7 +13,7 @@ from tests.gpu_helpers import ATOL_ENT, ATOL_LOGP, ATOL_TOK, P_REL, RTOL_ENT, RT
 pytestmark = pytest.mark.gpu
 
 
-@pytest.fixture(params=["1", "0"], ids=["cluster", "l2reread"], autouse=True)
+@pytest.fixture(params=["1", "0", "2"], ids=["cluster", "l2reread", "l2split"], autouse=True)
 def fused_variant(request, monkeypatch):
     """Both dart_loss_fused kernels: the cluster / distributed-shared-memory
     single read (default for bf16 logits) and the L2 re-read variant."""
