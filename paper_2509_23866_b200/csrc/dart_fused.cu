@@ -441,17 +441,14 @@ __global__ void __launch_bounds__(FU_THREADS, DART_FU_CTAS) fused_sweep_kernel(c
     }
     named_bar_sync(1, FU_NC * 32);
     // ---------------- row epilogue (warp 0), broadcast through shared memory
-    if (warp == 0 && lane == 0) {
-      double Mr = -INFINITY, Sr = 0.0;
-      for (int w = 0; w < FU_NC; ++w) {        // fixed fold over the consumer warps
-        const double Mw = (double)sh.part_m[par][w];
-        const double Sw = sh.part_s[par][w];
-        if (Sw == 0.0) continue;
-        if (Mr == -INFINITY) { Mr = Mw; Sr = Sw; continue; }
-        const double mn = fmax(Mr, Mw);
-        Sr = Sr * (double)ex2((float)(Mr - mn)) + Sw * (double)ex2((float)(Mw - mn));
-        Mr = mn;
-      }
+    if (warp == 0) {
+      // fixed-order fold of the consumer warps' partials across lanes (butterfly)
+      const float mw = lane < FU_NC ? sh.part_m[par][lane] : -INFINITY;
+      const double sw = lane < FU_NC ? sh.part_s[par][lane] : 0.0;
+      const float Mf = warp_max_f(sw > 0.0 ? mw : -INFINITY);
+      double Sr = warp_sum_d(sw > 0.0 ? sw * (double)ex2(mw - Mf) : 0.0);
+      double Mr = Sr > 0.0 ? (double)Mf : -INFINITY;
+      if (lane == 0) {
       if (CL > 1) {                            // exchange with the peer CTA, fold in rank order
         sh.mb_m[par][rank] = (float)Mr;
         sh.mb_s[par][rank] = Sr;
@@ -475,6 +472,7 @@ __global__ void __launch_bounds__(FU_THREADS, DART_FU_CTAS) fused_sweep_kernel(c
       const double L2s = log2(Sr);
       sh.row_g[par] = fused_epilogue(p, t, rc, Mr, L2s, rank == 0);
       sh.row_nl2[par] = (float)(-(Mr + L2s));
+      }
     }
     named_bar_sync(1, FU_NC * 32);
     const float g = sh.row_g[par], nl2 = sh.row_nl2[par];
