@@ -318,6 +318,28 @@ __device__ __forceinline__ void bwd_issue(OCur& pc, const BwdParams& p, uint64_t
 #ifndef DART_BWD_FULL
 #define DART_BWD_FULL 0
 #endif
+// DART_BWD_TMAST=1: bf16 -> bf16 full chunks are written by one bulk
+// shared->global copy per 4 KB chunk (TMA store, SASS UBLKCP) from a per-warp
+// double-buffered staging area instead of 8 STG.128 per lane; masked chunks
+// are bulk-stored from a zero page.  Correct (parity + racecheck/memcheck
+// clean) but measured SLOWER on B200: bwd sweep 6.16 vs 5.48 ms (84.6% vs
+// 95.1% of the copy peak) -- the staging STS + proxy fence + bulk-group waits
+// cost more than the streaming STG.128 they replace.  Off by default.
+#ifndef DART_BWD_TMAST
+#define DART_BWD_TMAST 0
+#endif
+__device__ __forceinline__ void bulk_s2g(void* gdst, const void* ssrc, uint32_t bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(gdst), "r"(smem_u32(ssrc)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void bulk_wait_read() { asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory"); }
+__device__ __forceinline__ void sts128(void* p, uint4 v) {
+  asm volatile("st.shared.v4.u32 [%0], {%1,%2,%3,%4};" ::"r"(smem_u32(p)), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w)
+               : "memory");
+}
 template <typename Tin, typename Tout, int WARPS, int STAGES>
 __global__ void __launch_bounds__(WARPS * 32, DART_BWD_MINB)
 bwd_sweep_kernel(const BwdParams p) {
@@ -327,10 +349,21 @@ bwd_sweep_kernel(const BwdParams p) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   uint8_t* ring = smem + (size_t)warp * STAGES * CH_BYTES;
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + (size_t)WARPS * STAGES * CH_BYTES) + warp * STAGES;
+  constexpr bool TMAST = DART_BWD_TMAST && sizeof(Tin) == 2 && sizeof(Tout) == 2;
+  // TMA-store staging: [WARPS][2][CH_BYTES] then one zero page (after the barriers, 1 KB aligned)
+  uint8_t* stage_base = smem + (((size_t)WARPS * STAGES * CH_BYTES + (size_t)WARPS * STAGES * 8 + 1023) & ~(size_t)1023);
+  uint8_t* stg_buf = stage_base + (size_t)warp * 2 * CH_BYTES;
+  uint8_t* zero_page = stage_base + (size_t)WARPS * 2 * CH_BYTES;
+  int sbuf = 0;
   if (lane == 0) {
 #pragma unroll
     for (int s = 0; s < STAGES; ++s) mbar_init(&bars[s], 1);
     fence_mbar_init();
+  }
+  if (TMAST) {
+    for (int i = threadIdx.x; i < CH_BYTES / 16; i += blockDim.x) sts128(zero_page + i * 16, make_uint4(0u, 0u, 0u, 0u));
+    fence_proxy_async_smem();
+    __syncthreads();
   }
   __syncwarp();
 
@@ -406,6 +439,35 @@ bwd_sweep_kernel(const BwdParams p) {
       __syncwarp();
       if (pc.valid) bwd_issue<Tin, WARPS, STAGES>(pc, p, bars, ring, slot, lane, pol);
       if (++slot == STAGES) { slot = 0; phase ^= 1u; }
+      if (TMAST && nv == CH_VEC && !(tail_elems && v0 + nv == nvec)) {
+        // gradient of the chunk into this warp's staging buffer, then one bulk store
+        if (lane == 0) bulk_wait_read<1>();         // the buffer's previous bulk store has read it
+        __syncwarp();
+        uint8_t* sb = stg_buf + (size_t)sbuf * CH_BYTES;
+#pragma unroll
+        for (int k = 0; k < VPL; ++k) {
+          float o[EPV];
+          grad_vec<Tin>(x[k], cc2, nl, ng, o);
+          sts128(sb + (lane + 32 * k) * 16, make_uint4(pack_bf16x2(o[0], o[1]), pack_bf16x2(o[2], o[3]),
+                                                       pack_bf16x2(o[4], o[5]), pack_bf16x2(o[6], o[7])));
+        }
+        if (y >= 0) {                               // target element: g (1 - p_y)
+          const int64_t yv = y / EPV;
+          if (yv >= v0 && yv < v0 + nv && lane == (int)((yv - v0) & 31)) {
+            const float py = ex2(fmaf(zy, c2, nl2));
+            reinterpret_cast<__nv_bfloat16*>(sb)[y - v0 * EPV] = __float2bfloat16_rn(fmaf(-g, py, g));
+          }
+        }
+        fence_proxy_async_smem();                   // generic-proxy smem writes -> visible to the bulk copy
+        __syncwarp();
+        if (lane == 0) {
+          bulk_s2g(orow + v0 * OUTV, sb, (uint32_t)CH_BYTES);
+          bulk_commit();
+        }
+        sbuf ^= 1;
+        ocur_advance(cc, p, WARPS);
+        continue;
+      }
       if (full) {
 #pragma unroll
         for (int k = 0; k < VPL; ++k) {
@@ -451,6 +513,14 @@ bwd_sweep_kernel(const BwdParams p) {
       }
     } else {
       // masked step: zeros, no read
+      if (TMAST && nv == CH_VEC && !(tail_elems && v0 + nv == nvec)) {
+        if (lane == 0) {
+          bulk_s2g(orow + v0 * OUTV, zero_page, (uint32_t)CH_BYTES);
+          bulk_commit();
+        }
+        ocur_advance(cc, p, WARPS);
+        continue;
+      }
       float o[EPV];
 #pragma unroll
       for (int e = 0; e < EPV; ++e) o[e] = 0.f;
@@ -473,6 +543,8 @@ bwd_sweep_kernel(const BwdParams p) {
     }
     ocur_advance(cc, p, WARPS);
   }
+  if (TMAST && lane == 0) bulk_wait_read<0>();     // smem must outlive the last bulk stores' reads
+  if (TMAST) __syncthreads();
 }
 
 // ============================================================== launchers
@@ -491,7 +563,9 @@ cudaError_t launch_rowrec(const RowRecParams& p, cudaStream_t st) {
 
 template <typename Tin, typename Tout, int WARPS, int STAGES>
 static cudaError_t launch_bwd_t(const BwdParams& p, int num_sms, cudaStream_t st) {
-  const size_t smem = (size_t)WARPS * STAGES * CH_BYTES + (size_t)WARPS * STAGES * 8;
+  constexpr bool TMAST = DART_BWD_TMAST && sizeof(Tin) == 2 && sizeof(Tout) == 2;
+  size_t smem = (size_t)WARPS * STAGES * CH_BYTES + (size_t)WARPS * STAGES * 8;
+  if (TMAST) smem = ((smem + 1023) & ~(size_t)1023) + (size_t)WARPS * 2 * CH_BYTES + CH_BYTES + 1024;
   auto kern = bwd_sweep_kernel<Tin, Tout, WARPS, STAGES>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
