@@ -16,6 +16,8 @@
 // instruction), warps 2..5 = epilogue from two TMEM accumulators (fp32 store,
 // bf16 store or fp32 read-add-write).  Tiles are rastered in groups of
 // GM_GROUP row blocks for L2 reuse of the B panel.
+#include <cstdlib>
+
 #include "dart_common.cuh"
 #include "dart_internal.h"
 #include "dart_tc.cuh"
@@ -212,6 +214,227 @@ __global__ void __launch_bounds__(GM_THREADS, 1)
   }
 }
 
+// ---------------------------------------------------------------- CTA-pair variant
+// cta_group::2: a 2-CTA cluster computes a 256 x 256 tile -- each CTA stages
+// its 128 rows of A and its 128 rows of B (K-major, 6 stages of 32 KB), the
+// pair leader issues tcgen05.mma.cta_group::2 (M = 256, N = 256) and each CTA
+// reads its 128 accumulator rows from its own TMEM.  Per SM this halves the
+// shared-memory / L2 operand traffic of the B panel.
+constexpr int G2_STAGES = 6;
+constexpr uint32_t G2_A_BYTES = 128 * GM_BK * 2, G2_B_BYTES = 128 * GM_BK * 2;
+constexpr uint32_t G2_STAGE_BYTES = G2_A_BYTES + G2_B_BYTES;
+constexpr size_t G2_SMEM = 1024 + (size_t)G2_STAGES * G2_STAGE_BYTES + 256;
+
+__device__ __forceinline__ uint32_t g2_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ uint32_t g2_cluster_id() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%clusterid.x;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ uint32_t g2_cluster_count() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%nclusterid.x;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void g2_cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+
+__device__ __forceinline__ void g2_tile(const GemmParams& p, int64_t t, int& mt, int& nt) {
+  // p.n_mt counts 256-row pair tiles here
+  gm_tile(p, t, mt, nt);
+}
+
+template <bool A_MN, bool B_MN>
+__global__ void __launch_bounds__(GM_THREADS, 1)
+    gemm_bf16_2sm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                         const GemmParams p) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + G2_STAGES * G2_A_BYTES;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + G2_STAGES * G2_STAGE_BYTES);
+  uint64_t* empty = full + G2_STAGES;
+  uint64_t* tfull = empty + G2_STAGES;
+  uint64_t* tempty = tfull + GM_ACC;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + GM_ACC);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = g2_rank();
+  const bool leader = rank == 0;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < G2_STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int a = 0; a < GM_ACC; ++a) {
+      mbar_init(&tfull[a], 1);
+      mbar_init(&tempty[a], 8);            // 4 epilogue warps x 2 CTAs (leader's copy is the one used)
+    }
+    fence_mbar_init();
+    tc::tma_prefetch_desc(&tmA);
+    tc::tma_prefetch_desc(&tmB);
+  }
+  if (warp == 1) tc::tmem_alloc_2sm(tmem_slot, GM_TMEM_COLS);
+  tc::fence_before();
+  __syncthreads();
+  g2_cluster_sync();
+  tc::fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const int KB = (p.K + GM_BK - 1) / GM_BK;
+  const int64_t cid = g2_cluster_id(), ncl = g2_cluster_count();
+
+  if (warp == 0) {
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t ph = 0;
+      for (int64_t t = cid; t < p.n_tiles; t += ncl) {
+        int mt, nt;
+        g2_tile(p, t, mt, nt);
+        for (int kb = 0; kb < KB; ++kb) {
+          mbar_wait(&empty[stage], ph ^ 1u);
+          if (leader) mbar_arrive_expect_tx(&full[stage], 2 * G2_STAGE_BYTES);   // both CTAs' bytes
+          uint8_t* a = sA + stage * G2_A_BYTES;
+          uint8_t* b = sB + stage * G2_B_BYTES;
+          const int m0 = mt * 256 + 128 * (int)rank, n0 = nt * 256 + 128 * (int)rank;
+          if (A_MN) {
+            tc::tma_load_2d_2sm(a, &tmA, &full[stage], m0, kb * GM_BK);
+            tc::tma_load_2d_2sm(a + 8192, &tmA, &full[stage], m0 + 64, kb * GM_BK);
+          } else {
+            tc::tma_load_2d_2sm(a, &tmA, &full[stage], kb * GM_BK, m0);
+          }
+          if (B_MN) {
+            tc::tma_load_2d_2sm(b, &tmB, &full[stage], n0, kb * GM_BK);
+            tc::tma_load_2d_2sm(b + 8192, &tmB, &full[stage], n0 + 64, kb * GM_BK);
+          } else {
+            tc::tma_load_2d_2sm(b, &tmB, &full[stage], kb * GM_BK, n0);
+          }
+          if (++stage == G2_STAGES) {
+            stage = 0;
+            ph ^= 1u;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (leader && lane == 0) {
+      constexpr uint32_t idesc = tc::idesc_bf16_f32(256, 256, A_MN, B_MN);
+      constexpr uint32_t a_lbo = A_MN ? 8192u : 16u, b_lbo = B_MN ? 8192u : 16u;
+      constexpr uint64_t a_kstep = A_MN ? (2048u >> 4) : (32u >> 4);
+      constexpr uint64_t b_kstep = B_MN ? (2048u >> 4) : (32u >> 4);
+      int stage = 0, acc = 0;
+      uint32_t ph = 0, aph = 0;
+      for (int64_t t = cid; t < p.n_tiles; t += ncl) {
+        mbar_wait(&tempty[acc], aph ^ 1u);
+        tc::fence_after();
+        const uint32_t d_tmem = tmem + (uint32_t)(acc * GM_BN);
+        for (int kb = 0; kb < KB; ++kb) {
+          mbar_wait(&full[stage], ph);
+          tc::fence_after();
+          const uint64_t da = tc::smem_desc_sw128(smem_u32(sA + stage * G2_A_BYTES), a_lbo, 1024);
+          const uint64_t db = tc::smem_desc_sw128(smem_u32(sB + stage * G2_B_BYTES), b_lbo, 1024);
+#pragma unroll
+          for (int k = 0; k < GM_BK / 16; ++k)
+            tc::umma_bf16_2sm(d_tmem, da + a_kstep * k, db + b_kstep * k, idesc, (kb | k) != 0 ? 1u : 0u);
+          tc::umma_commit_2sm(&empty[stage], 0x3);
+          if (++stage == G2_STAGES) {
+            stage = 0;
+            ph ^= 1u;
+          }
+        }
+        tc::umma_commit_2sm(&tfull[acc], 0x3);
+        if (++acc == GM_ACC) {
+          acc = 0;
+          aph ^= 1u;
+        }
+      }
+    }
+  } else {
+    const int q = warp & 3;
+    const int r = q * 32 + lane;
+    int acc = 0;
+    uint32_t aph = 0;
+    for (int64_t t = cid; t < p.n_tiles; t += ncl) {
+      int mt, nt;
+      g2_tile(p, t, mt, nt);
+      mbar_wait(&tfull[acc], aph);
+      tc::fence_after();
+      const int64_t m = (int64_t)mt * 256 + 128 * rank + r;
+      const uint32_t tbase = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * GM_BN);
+#pragma unroll 1
+      for (int j = 0; j < GM_BN / 32; ++j) {
+        float x[32];
+        tc::tmem_ld32(tbase + (uint32_t)(j * 32), x);
+        const int64_t n0 = (int64_t)nt * GM_BN + j * 32;
+        if (m >= p.M || n0 >= p.N) continue;
+        if (p.c_mode == DART_GEMM_STORE_BF16) {
+          __nv_bfloat16* c = reinterpret_cast<__nv_bfloat16*>(p.C) + m * p.ldc + n0;
+#pragma unroll
+          for (int i = 0; i < 32; i += 8)
+            if (n0 + i + 8 <= p.N)
+              *reinterpret_cast<uint4*>(c + i) = make_uint4(pack_bf16x2(x[i], x[i + 1]), pack_bf16x2(x[i + 2], x[i + 3]),
+                                                            pack_bf16x2(x[i + 4], x[i + 5]),
+                                                            pack_bf16x2(x[i + 6], x[i + 7]));
+        } else {
+          float* c = reinterpret_cast<float*>(p.C) + m * p.ldc + n0;
+#pragma unroll
+          for (int i = 0; i < 32; i += 4)
+            if (n0 + i + 4 <= p.N) {
+              float4 v = make_float4(x[i], x[i + 1], x[i + 2], x[i + 3]);
+              if (p.c_mode == DART_GEMM_ACCUM_F32) {
+                const float4 o = *reinterpret_cast<const float4*>(c + i);
+                v.x += o.x; v.y += o.y; v.z += o.z; v.w += o.w;
+              }
+              *reinterpret_cast<float4*>(c + i) = v;
+            }
+        }
+      }
+      tc::fence_before();
+      __syncwarp();
+      if (lane == 0) tc::mbar_arrive_remote(&tempty[acc], 0);   // the leader's accumulator-empty barrier
+      if (++acc == GM_ACC) {
+        acc = 0;
+        aph ^= 1u;
+      }
+    }
+  }
+  tc::fence_before();
+  __syncthreads();
+  g2_cluster_sync();
+  if (warp == 1) {
+    tc::fence_after();
+    tc::tmem_dealloc_2sm(tmem, GM_TMEM_COLS);
+  }
+}
+
+template <bool A_MN, bool B_MN>
+cudaError_t launch_gemm_2sm(const CUtensorMap& ta, const CUtensorMap& tb, GemmParams p, int num_sms,
+                            cudaStream_t st) {
+  auto kern = gemm_bf16_2sm_kernel<A_MN, B_MN>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)G2_SMEM);
+  if (e != cudaSuccess) return e;
+  p.n_mt = (p.M + 255) / 256;
+  p.n_tiles = (int64_t)p.n_mt * p.n_nt;
+  cudaLaunchConfig_t cfg = {};
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = 2;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.blockDim = dim3(GM_THREADS);
+  cfg.dynamicSmemBytes = G2_SMEM;
+  cfg.stream = st;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  int64_t pairs = num_sms / 2;
+  if (pairs > p.n_tiles) pairs = p.n_tiles;
+  cfg.gridDim = dim3((unsigned)(2 * pairs));
+  return cudaLaunchKernelEx(&cfg, kern, ta, tb, p);
+}
+
 template <bool A_MN, bool B_MN>
 cudaError_t launch_gemm_t(const CUtensorMap& ta, const CUtensorMap& tb, const GemmParams& p, int num_sms,
                           cudaStream_t st) {
@@ -240,6 +463,18 @@ cudaError_t launch_gemm_bf16(const void* A, bool a_mn, int64_t lda, const void* 
   p.c_mode = c_mode;
   p.C = C;
   p.ldc = ldc;
+  const char* e2 = getenv("DART_GEMM_2SM");
+  if (!(e2 && e2[0] == '0')) {   // default: CTA-pair kernel (each CTA stages 128 rows of A and of B);
+                                 // 1264-1285 vs 1135 TFLOP/s sustained on [8192 x 3584] x [3584 x 152064]
+    CUtensorMap ta2, tb2;
+    const bool ok2a = a_mn ? tc::make_map_bf16(&ta2, A, K, M, lda, 64, 64) : tc::make_map_bf16(&ta2, A, M, K, lda, 64, 128);
+    const bool ok2b = b_mn ? tc::make_map_bf16(&tb2, B, K, N, ldb, 64, 64) : tc::make_map_bf16(&tb2, B, N, K, ldb, 64, 128);
+    if (!ok2a || !ok2b) return cudaErrorInvalidValue;
+    if (a_mn && b_mn) return launch_gemm_2sm<true, true>(ta2, tb2, p, num_sms, st);
+    if (a_mn) return launch_gemm_2sm<true, false>(ta2, tb2, p, num_sms, st);
+    if (b_mn) return launch_gemm_2sm<false, true>(ta2, tb2, p, num_sms, st);
+    return launch_gemm_2sm<false, false>(ta2, tb2, p, num_sms, st);
+  }
   if (a_mn && b_mn) return launch_gemm_t<true, true>(ta, tb, p, num_sms, st);
   if (a_mn) return launch_gemm_t<true, false>(ta, tb, p, num_sms, st);
   if (b_mn) return launch_gemm_t<false, true>(ta, tb, p, num_sms, st);
