@@ -25,6 +25,20 @@ for name in which:
         dl.check_status()
         print(name, "ok", dl.stats_dict()["loss"])
         continue
+    elif name == "lmupdate":   # NEXT #3 update pass: CTA-pair tcgen05 GEMMs (K- and MN-major) + fused loss
+        from paper_2509_23866_b200 import lmhead
+        lb = synth.make_lmhead("grid2x4x3x20@3000", 256, seed=3)
+        bb = lb.batch
+        old = dart.DartLoss(bb.layout, dart.whole_shard(bb.layout), bb.V, dart.Config(), "cuda", with_grad=False)
+        args = (bb.target.cuda(), bb.logp_old.cuda(), bb.logp_rollout.cuda(), bb.logp_ref.cuda())
+        old.forward_lmhead(lb.hidden.cuda(), lb.weight.cuda(), *args)
+        old.select()
+        up = lmhead.LmHeadUpdate(bb.layout, bb.V, 256, dart.Config(), "cuda", chunk_rows=150)
+        dh, dW = up.run(lb.hidden.cuda(), lb.weight.cuda(), *args, old.keep, old.norm)
+        torch.cuda.synchronize()
+        up.check_status()
+        print(name, "ok", up.stats_dict()["loss"], float(dh.abs().sum()), float(dW.abs().sum()))
+        continue
     elif name in ("fused", "fused_cluster"):   # NEXT #1 (both kernels)
         import os
         os.environ["DART_FUSED_VARIANT"] = "1" if name == "fused_cluster" else "0"
