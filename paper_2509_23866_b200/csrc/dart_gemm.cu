@@ -16,6 +16,7 @@
 // instruction), warps 2..5 = epilogue from two TMEM accumulators (fp32 store,
 // bf16 store or fp32 read-add-write).  Tiles are rastered in groups of
 // GM_GROUP row blocks for L2 reuse of the B panel.
+#include <cstdio>
 #include <cstdlib>
 
 #include "dart_common.cuh"
@@ -430,6 +431,10 @@ cudaError_t launch_gemm_2sm(const CUtensorMap& ta, const CUtensorMap& tb, GemmPa
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   int64_t pairs = num_sms / 2;
+  cfg.gridDim = dim3((unsigned)(2 * pairs));
+  int nclu = 0;   // persistent pairs: never more clusters than can be co-resident
+  if (cudaOccupancyMaxActiveClusters(&nclu, kern, &cfg) == cudaSuccess && nclu > 0 && nclu < pairs) pairs = nclu;
+  (void)cudaGetLastError();
   if (pairs > p.n_tiles) pairs = p.n_tiles;
   cfg.gridDim = dim3((unsigned)(2 * pairs));
   return cudaLaunchKernelEx(&cfg, kern, ta, tb, p);

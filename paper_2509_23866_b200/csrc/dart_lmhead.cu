@@ -22,6 +22,7 @@
 // lanes 32*(w%4) .. +31, i.e. accumulator rows).  Pipelines: LM_STAGES smem
 // stages (full/empty mbarriers), two TMEM accumulators of 256 fp32 columns
 // (tfull/tempty), so the epilogue of tile i overlaps the MMAs of tile i+1.
+#include <cstdio>
 #include <cstdlib>
 
 #include "dart_common.cuh"
@@ -344,6 +345,10 @@ cudaError_t launch_lmhead(const void* hidden, int64_t ld_h, const void* weight, 
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     int64_t pairs = num_sms / 2;
+    cfg.gridDim = dim3((unsigned)(2 * pairs));
+    int nclu = 0;   // persistent pairs: never more clusters than can be co-resident
+    if (cudaOccupancyMaxActiveClusters(&nclu, kern, &cfg) == cudaSuccess && nclu > 0 && nclu < pairs) pairs = nclu;
+    (void)cudaGetLastError();
     if (pairs > q.n_items) pairs = q.n_items;
     cfg.gridDim = dim3((unsigned)(2 * pairs));
     return cudaLaunchKernelEx(&cfg, kern, tmA, tmB, q);
