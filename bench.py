@@ -352,7 +352,10 @@ def run_dart(args):
         try:
             with open(tpath) as f:
                 tj = json.load(f)
-            traffic = tj.get(dom[0], {}).get("dram_bytes_per_launch")
+            key = dom[0]
+            if args.kl == "exact" and not args.fused:      # the exact-KL sweeps have their own captures
+                key = {"fwd_sweep": "fwd_kl", "bwd_sweep": "bwd_kl"}.get(key, key)
+            traffic = tj.get(key, {}).get("dram_bytes_per_launch")
         except Exception:
             traffic = None
 
