@@ -86,8 +86,14 @@ class ClockSampler:
         mx = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         reasons = sorted({names[i] for r in rows for i in range(4) if r[3 + i].lower() == "active"})
+        pw = []
+        for r in rows:
+            try:
+                pw.append(float(r[7]))
+            except ValueError:
+                pass
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(rows)}
+                "reasons": reasons, "samples": len(rows), "power_w": statistics.median(pw) if pw else None}
 
 
 # ------------------------------------------------------------------ setup
@@ -310,6 +316,34 @@ def run_dart(args):
         fwd_ms.append(e[0].elapsed_time(e[1]))
         bwd_ms.append(e[2].elapsed_time(e[3]))
 
+    # context, not the roofline denominator: a plain device copy (torch
+    # copy_, the kernel MEASURED_PEAKS.json's hbm_gbs is taken with) timed the
+    # same way as the step -- back to back, as long as the timed loop, under
+    # the same power-cap conditions -- over buffers of the step's size
+    copy_ref = None
+    if not args.fused and dl.dlogits is not None and rank == 0 and world == 1 and batch.logits.is_contiguous() \
+            and dl.dlogits_store.numel() >= batch.logits.numel() and dl.dlogits_store.dtype == batch.logits.dtype:
+        src = batch.logits.view(-1)
+        dst = dl.dlogits_store.view(-1)[:src.numel()]
+        n_copy = max(3, int(round(elapsed_ms / max(1e-3, 2.0 * src.numel() * src.element_size() / 6.0e9))))
+        for _ in range(3):
+            dst.copy_(src)
+        torch.cuda.synchronize()
+        clk2 = ClockSampler(local)
+        clk2.start()
+        time.sleep(0.15)
+        c0, c1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        c0.record(stream)
+        for _ in range(n_copy):
+            dst.copy_(src)
+        c1.record(stream)
+        torch.cuda.synchronize()
+        cclk = clk2.stop()
+        cms = c0.elapsed_time(c1) / n_copy
+        copy_ref = {"what": "torch copy_ of the logits buffer into dlogits, back to back for the timed loop's duration",
+                    "bytes": 2 * src.numel() * src.element_size(), "launches": n_copy, "avg_ms": cms,
+                    "GBps": 2 * src.numel() * src.element_size() / (cms * 1e-3) / 1e9, "clocks": cclk}
+
     ms = elapsed_ms / args.steps
     if world > 1:
         import torch.distributed as dist
@@ -400,6 +434,9 @@ def run_dart(args):
             "e2e": e2e,
             "cpu_baseline": cpu,
         }
+        if copy_ref is not None:
+            copy_ref["step_frac_vs_copy"] = line["kernels"]["step_GBps"] / copy_ref["GBps"]
+            line["copy_sustained"] = copy_ref
         print(json.dumps(line), flush=True)
     if world > 1:
         import torch.distributed as dist

@@ -328,6 +328,26 @@ __device__ __forceinline__ void bwd_issue(OCur& pc, const BwdParams& p, uint64_t
 #ifndef DART_BWD_TMAST
 #define DART_BWD_TMAST 0
 #endif
+// DART_BWD_V8=1: bf16 -> bf16 full chunks (all 256 vectors inside the row, no
+// tail) run without per-vector guards and each lane owns PAIRS of adjacent
+// 16-byte input vectors, so its 16 gradients leave in one 32-byte store
+// (st.global.v8.b32, SASS STG.E.256): 31% fewer instructions than the guarded
+// STG.128 path (1.68e9 vs 2.43e9 per launch, ncu) -- and SLOWER on B200:
+// 6.07 vs 5.35 ms isolated.  ncu: 26% of warp stalls become long_scoreboard
+// on the STG.256 source registers (ptxas reuses them for the next pair's
+// unpack right after the store, so each warp waits for the LSU to drain its
+// 1 KB store).  =2 spreads the stores (one opaque uniform branch per pair):
+// 6.07 ms, same.  DART_BWD_FULL=2 (STG.128, no per-lane guards, spread the
+// same way): 6.2 ms.  The guarded path stays the default.  Needs 32-byte
+// aligned gradient rows (checked per launch).
+#ifndef DART_BWD_V8
+#define DART_BWD_V8 0
+#endif
+__device__ __forceinline__ void stg256_cs(void* p, uint4 a, uint4 b) {
+  asm volatile("st.global.cs.v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(p), "r"(a.x), "r"(a.y), "r"(a.z),
+               "r"(a.w), "r"(b.x), "r"(b.y), "r"(b.z), "r"(b.w)
+               : "memory");
+}
 __device__ __forceinline__ void bulk_s2g(void* gdst, const void* ssrc, uint32_t bytes) {
   asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(gdst), "r"(smem_u32(ssrc)),
                "r"(bytes)
@@ -350,6 +370,8 @@ bwd_sweep_kernel(const BwdParams p) {
   uint8_t* ring = smem + (size_t)warp * STAGES * CH_BYTES;
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + (size_t)WARPS * STAGES * CH_BYTES) + warp * STAGES;
   constexpr bool TMAST = DART_BWD_TMAST && sizeof(Tin) == 2 && sizeof(Tout) == 2;
+  constexpr bool V8T = DART_BWD_V8 && !DART_BWD_TMAST && sizeof(Tin) == 2 && sizeof(Tout) == 2;
+  const bool v8_ok = V8T && ((p.ldg_bytes & 31) == 0) && ((reinterpret_cast<uintptr_t>(p.dlogits) & 31) == 0);
   // TMA-store staging: [WARPS][2][CH_BYTES] then one zero page (after the barriers, 1 KB aligned)
   uint8_t* stage_base = smem + (((size_t)WARPS * STAGES * CH_BYTES + (size_t)WARPS * STAGES * 8 + 1023) & ~(size_t)1023);
   uint8_t* stg_buf = stage_base + (size_t)warp * 2 * CH_BYTES;
@@ -402,7 +424,8 @@ bwd_sweep_kernel(const BwdParams p) {
     const int64_t v0 = (int64_t)cc.c * CH_VEC;
     const int nv = (int)min((int64_t)CH_VEC, nvec - v0);
     // full chunk: all lanes hold VPL complete vectors (no tail, no predicates)
-    const bool full = DART_BWD_FULL && (nv == CH_VEC) && !(tail_elems && v0 + nv == nvec);
+    const bool full8 = v8_ok && (nv == CH_VEC) && !(tail_elems && v0 + nv == nvec);
+    const bool full = !full8 && DART_BWD_FULL && (nv == CH_VEC) && !(tail_elems && v0 + nv == nvec);
     uint8_t* orow = dlog + t * ldg_bytes;
     uint8_t* olane = orow + (v0 + lane) * OUTV;    // this lane's first output vector
     if (cc.kept) {
@@ -420,7 +443,13 @@ bwd_sweep_kernel(const BwdParams p) {
       const uint8_t* sp = ring + (size_t)slot * CH_BYTES;
       const float2 cc2 = make_float2(c2, c2), nl = make_float2(nl2, nl2), ng = make_float2(-g, -g);
       uint4 x[VPL];
-      if (full) {
+      if (V8T && full8) {       // lane owns vector pairs (lane + 32 k): 32 contiguous bytes each
+#pragma unroll
+        for (int k = 0; k < VPL / 2; ++k) {
+          x[2 * k] = lds128(sp + (lane + 32 * k) * 32);
+          x[2 * k + 1] = lds128(sp + (lane + 32 * k) * 32 + 16);
+        }
+      } else if (full) {
 #pragma unroll
         for (int k = 0; k < VPL; ++k) x[k] = lds128(sp + (lane + 32 * k) * 16);
       } else {
@@ -439,6 +468,33 @@ bwd_sweep_kernel(const BwdParams p) {
       __syncwarp();
       if (pc.valid) bwd_issue<Tin, WARPS, STAGES>(pc, p, bars, ring, slot, lane, pol);
       if (++slot == STAGES) { slot = 0; phase ^= 1u; }
+      if (V8T && full8) {
+#pragma unroll
+        for (int k = 0; k < VPL / 2; ++k) {
+          float o[16];
+#if DART_BWD_V8 == 2
+          // always true on a full chunk, but opaque to the compiler: one branch
+          // region per pair keeps each pair's stores next to its math
+          if ((nv >> 6) <= k) break;
+#endif
+          grad_vec<Tin>(x[2 * k], cc2, nl, ng, o);
+          grad_vec<Tin>(x[2 * k + 1], cc2, nl, ng, o + 8);
+          stg256_cs(orow + (v0 + 2 * (lane + 32 * k)) * 16,
+                    make_uint4(pack_bf16x2(o[0], o[1]), pack_bf16x2(o[2], o[3]), pack_bf16x2(o[4], o[5]),
+                               pack_bf16x2(o[6], o[7])),
+                    make_uint4(pack_bf16x2(o[8], o[9]), pack_bf16x2(o[10], o[11]), pack_bf16x2(o[12], o[13]),
+                               pack_bf16x2(o[14], o[15])));
+        }
+        if (y >= 0) {           // target element g (1 - p_y), after its pair's store (same thread)
+          const int64_t yv = y / EPV;
+          if (yv >= v0 && yv < v0 + CH_VEC && lane == (int)(((yv - v0) >> 1) & 31)) {
+            const float py = ex2(fmaf(zy, c2, nl2));
+            reinterpret_cast<__nv_bfloat16*>(orow)[y] = __float2bfloat16_rn(fmaf(-g, py, g));
+          }
+        }
+        ocur_advance(cc, p, WARPS);
+        continue;
+      }
       if (TMAST && nv == CH_VEC && !(tail_elems && v0 + nv == nvec)) {
         // gradient of the chunk into this warp's staging buffer, then one bulk store
         if (lane == 0) bulk_wait_read<1>();         // the buffer's previous bulk store has read it
@@ -471,6 +527,9 @@ bwd_sweep_kernel(const BwdParams p) {
       if (full) {
 #pragma unroll
         for (int k = 0; k < VPL; ++k) {
+#if DART_BWD_FULL == 2
+          if ((nv >> 5) <= k) break;   // always true here; one branch region per vector (spreads the stores)
+#endif
 #if DART_BWD_STYLE == 1
           if (lane + 32 * k < nv) {   // always true here: keeps compute/store of each vector together
 #endif
@@ -513,6 +572,13 @@ bwd_sweep_kernel(const BwdParams p) {
       }
     } else {
       // masked step: zeros, no read
+      if (V8T && full8) {
+        const uint4 zz = make_uint4(0u, 0u, 0u, 0u);
+#pragma unroll
+        for (int k = 0; k < VPL / 2; ++k) stg256_cs(orow + (v0 + 2 * (lane + 32 * k)) * 16, zz, zz);
+        ocur_advance(cc, p, WARPS);
+        continue;
+      }
       if (TMAST && nv == CH_VEC && !(tail_elems && v0 + nv == nvec)) {
         if (lane == 0) {
           bulk_s2g(orow + v0 * OUTV, zero_page, (uint32_t)CH_BYTES);

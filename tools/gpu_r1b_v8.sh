@@ -1,0 +1,8 @@
+export PATH=/usr/local/cuda/bin:$PATH
+mkdir -p gpurun_out
+timeout 900 python -m pytest tests/test_parity_gpu.py tests/test_stream_gpu.py tests/test_virtual_ranks.py -m gpu -q -x > gpurun_out/pytest_v8.log 2>&1; echo "pytest rc=$?"; tail -3 gpurun_out/pytest_v8.log
+for f in paper_2509_23866_b200/libdart_loss.so build_variants/old.so build_variants/v8w12.so build_variants/v8w16s3.so paper_2509_23866_b200/libdart_loss.so build_variants/old.so; do echo "== $f"; DART_LIB_PATH=$PWD/$f timeout 600 python tools/diag_loop.py 2>&1 | grep -E '"mode"' | python -c "
+import sys,json
+for l in sys.stdin:
+    j=json.loads(l); c=j['clocks'] or {}
+    print(j['mode'], j['gap'], 'fwd', j['fwd_ms'], j['fwd_frac'], 'bwd', j['bwd_ms'], j['bwd_frac'], c.get('sm_mhz'), c.get('power_w'))"; done
