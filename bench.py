@@ -834,16 +834,17 @@ def run_e2e(args, dl, batch, stream, world, inputs):
 
 
 # ------------------------------------------------------------------ oracle arms
-def oracle_sample(batch, n_traj=None, max_tokens=1024):
-    """A bounded sample of the workload: the first group's first trajectories,
-    truncated to whole steps totalling <= max_tokens tokens."""
+def oracle_sample(batch, n_traj=None, max_tokens=1024, group=0):
+    """A bounded sample of the workload: task group `group`'s first
+    trajectories, truncated to whole steps totalling <= max_tokens tokens."""
     from paper_2509_23866_b200 import synth
     L = batch.layout
     steps, toks = 0, 0
     tso, sto = L.traj_step_off, L.step_tok_off
     lens = []
-    i = 0
-    while i < L.N_traj and L.traj_group[i] == L.traj_group[0]:
+    i0 = int(np.searchsorted(L.traj_group, group, side="left"))
+    i = i0
+    while i < L.N_traj and L.traj_group[i] == L.traj_group[i0]:
         li = 0
         for s in range(tso[i], tso[i + 1]):
             ns = int(sto[s + 1] - sto[s])
@@ -859,11 +860,11 @@ def oracle_sample(batch, n_traj=None, max_tokens=1024):
     rows = []
     tso2, sto2 = [0], [0]
     for j, li in enumerate(lens):
-        for s in range(tso[j], tso[j] + li):
+        for s in range(tso[i0 + j], tso[i0 + j] + li):
             rows.extend(range(int(sto[s]), int(sto[s + 1])))
             sto2.append(sto2[-1] + int(sto[s + 1] - sto[s]))
         tso2.append(tso2[-1] + li)
-    lay = synth.Layout(G=1, traj_group=np.zeros(len(lens), np.int32), traj_reward=L.traj_reward[:len(lens)],
+    lay = synth.Layout(G=1, traj_group=np.zeros(len(lens), np.int32), traj_reward=L.traj_reward[i0:i0 + len(lens)],
                        traj_step_off=np.asarray(tso2, np.int64), step_tok_off=np.asarray(sto2, np.int64),
                        step_fork=np.zeros(len(sto2) - 1, bool))
     rows_t = torch.as_tensor(rows, device=batch.logits.device)
@@ -877,15 +878,87 @@ def oracle_sample(batch, n_traj=None, max_tokens=1024):
     return d, len(rows), len(lens), len(sto2) - 1
 
 
-def cpu_baseline(args, batch, cfg):
+# ---- the oracle on the host cores: the unmodified oracle, one independent
+# bounded sample per worker process (fork: the samples are inherited, never
+# pickled), wall time over all of them.  SURVEY §8(d): "parallelised over
+# token rows with multiprocessing across all host cores".
+_ORACLE_JOBS = None
+
+
+def _oracle_job(i):
     from oracle import dart_oracle as O
-    d, ntok, ntraj, nstep = oracle_sample(batch, max_tokens=args.cpu_tokens)
-    t0 = time.time()
-    O.loss_pass(d, cfg.as_f32())
-    dt = time.time() - t0
-    return {"value": ntok / dt, "unit": "logit-tokens/s", "cores": 1, "kind": "oracle",
-            "sample": f"{ntok} tokens ({ntraj} trajectories x whole steps of task 0, V={batch.V}); "
-                      f"full fwd+select+bwd incl. dlogits, float64 NumPy, single thread",
+    d, cfg = _ORACLE_JOBS[i]
+    O.loss_pass(d, cfg)
+    return i
+
+
+def oracle_procs(sample_bytes):
+    """Worker count: the host's usable cores, bounded by ~3x the sample's
+    bytes of free memory per worker (the oracle holds float64 rows)."""
+    try:
+        cores = len(os.sched_getaffinity(0))
+    except Exception:
+        cores = os.cpu_count() or 1
+    try:
+        import psutil
+        avail = psutil.virtual_memory().available
+        cores = min(cores, max(1, int(0.6 * avail // max(1, 3 * sample_bytes))))
+    except Exception:
+        pass
+    return max(1, min(cores, 64))
+
+
+class OraclePool:
+    def __init__(self, samples, cfg, procs):
+        global _ORACLE_JOBS
+        import multiprocessing as mp
+        self.n = len(samples)
+        _ORACLE_JOBS = [(d, cfg) for d in samples]
+        for v in ("OMP_NUM_THREADS", "OPENBLAS_NUM_THREADS", "MKL_NUM_THREADS"):
+            os.environ[v] = "1"
+        self.procs = procs
+        self.pool = mp.get_context("fork").Pool(procs) if procs > 1 else None
+
+    def run(self):
+        """One pass over every sample; returns wall seconds."""
+        t0 = time.perf_counter()
+        if self.pool is None:
+            for i in range(self.n):
+                _oracle_job(i)
+        else:
+            self.pool.map(_oracle_job, range(self.n), chunksize=1)
+        return time.perf_counter() - t0
+
+    def close(self):
+        if self.pool is not None:
+            self.pool.close()
+            self.pool.join()
+
+
+def oracle_samples(batch, per_sample_tokens, n):
+    """n samples (task groups 0, 1, ... cycled), whole steps, <= per_sample_tokens each."""
+    G = int(batch.layout.G)
+    out, ntok = [], 0
+    for i in range(n):
+        d, nt, _, _ = oracle_sample(batch, max_tokens=per_sample_tokens, group=i % G)
+        out.append(d)
+        ntok += nt
+    return out, ntok
+
+
+def cpu_baseline(args, batch, cfg):
+    per = args.cpu_tokens
+    procs = oracle_procs(per * batch.V * 4) if args.cpu_procs <= 0 else args.cpu_procs
+    samples, ntok = oracle_samples(batch, per, procs)
+    pool = OraclePool(samples, cfg.as_f32(), procs)
+    try:
+        dt = pool.run()
+    finally:
+        pool.close()
+    return {"value": ntok / dt, "unit": "logit-tokens/s", "cores": procs, "kind": "oracle",
+            "sample": f"{procs} independent samples run concurrently, one per process, each <= {per} tokens "
+                      f"of whole steps of one task group (groups cycled; {ntok} tokens in all, V={batch.V}); "
+                      f"full fwd+select+bwd incl. dlogits, float64 NumPy, one thread per process",
             "seconds": dt}
 
 
@@ -903,13 +976,16 @@ def run_reference(args):
     batch = synth.make_batch(args.config, seed=args.seed * 1000, device="cpu", layout=_first_traj_layout(layout_r),
                              V=V, dtype=dtype)
     cfg = dart.Config(entropy_q=args.q, beta_kl=args.beta)
-    d, ntok, ntraj, nstep = oracle_sample(batch, max_tokens=args.cpu_tokens)
-    for _ in range(args.warmup):
-        O.loss_pass(d, cfg.as_f32())
-    t0 = time.perf_counter()
-    for _ in range(args.steps):
-        O.loss_pass(d, cfg.as_f32())
-    dt = (time.perf_counter() - t0) / args.steps
+    d, ntok1, ntraj, nstep = oracle_sample(batch, max_tokens=args.cpu_tokens)
+    procs = oracle_procs(ntok1 * V * 4) if args.cpu_procs <= 0 else args.cpu_procs
+    pool = OraclePool([d] * procs, cfg.as_f32(), procs)      # the same sample on every core
+    ntok = ntok1 * procs
+    try:
+        for _ in range(args.warmup):
+            pool.run()
+        dt = sum(pool.run() for _ in range(args.steps)) / args.steps
+    finally:
+        pool.close()
     value = ntok / dt
     line = {"impl": "reference", "metric": "loss fwd+bwd logit-tokens/s at V=152064 bf16, % of HBM peak, 1/2/4/8 GPU",
             "value": value, "unit": "logit-tokens/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
@@ -919,9 +995,10 @@ def run_reference(args):
                        + (" (exact full-vocabulary KL from reference logits: NEXT #4)" if args.kl == "exact" else ""),
                        "desc": CONFIG_DESC.get(args.config, args.config),
                        "sample_tokens": ntok},
-            "cpu_baseline": {"value": value, "unit": "logit-tokens/s", "cores": 1, "kind": "oracle",
-                             "sample": f"{ntok} tokens of {args.config} ({ntraj} trajectories of task 0), "
-                                       f"float64 NumPy oracle, single thread, per step"},
+            "cpu_baseline": {"value": value, "unit": "logit-tokens/s", "cores": procs, "kind": "oracle",
+                             "sample": f"per step: {procs} concurrent runs (one process per core) of one sample of "
+                                       f"{ntok1} tokens of {args.config} ({ntraj} trajectories of task 0, whole "
+                                       f"steps), float64 NumPy oracle, one thread per process"},
             "e2e": {"value": value, "unit": "logit-tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -955,7 +1032,8 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-cpu", action="store_true")
-    ap.add_argument("--cpu-tokens", type=int, default=1024)
+    ap.add_argument("--cpu-tokens", type=int, default=1024, help="oracle sample tokens per worker process")
+    ap.add_argument("--cpu-procs", type=int, default=0, help="oracle worker processes (0: host cores, memory-bounded)")
     ap.add_argument("--stream-rows", type=int, default=0,
                     help="chunk-stream the batch with chunks of at most this many rows (configs > HBM)")
     ap.add_argument("--pool", type=int, default=3, help="logits/dlogits pool buffers when streaming")
