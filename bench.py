@@ -145,20 +145,30 @@ def run_streamed(args):
     """Configs whose logits exceed HBM (long-horizon 249 GB, scale sweep):
     forward over chunks -> select -> backward over chunks, logits/dlogits in a
     pool of P buffers (chunk c -> slot c mod P in both sweeps; the synthetic
-    slot contents are generated once, so both sweeps read identical bytes)."""
+    slot contents are generated once, so both sweeps read identical bytes).
+    N > 1 (torchrun): the config's batch is the GLOBAL batch (strong scaling),
+    sharded into token-balanced ranges of whole trajectories; each rank
+    streams its own shard, C1 all-gathers every rank's per-chunk step
+    entropies, one selection, C2 all-reduces the statistics."""
     from paper_2509_23866_b200 import build as B
-    B.build()
+    if int(os.environ.get("RANK", "0")) == 0:
+        B.build()
     world, rank, local = dist_setup(args)
+    import torch.distributed as tdist
     if world > 1:
-        raise SystemExit("--stream-rows is single-process (per-rank streaming with a global "
-                         "normaliser is not implemented yet)")
+        tdist.barrier()
     from paper_2509_23866_b200 import dart, synth
+    from paper_2509_23866_b200 import dist as D
     from paper_2509_23866_b200.stream import StreamedPass
     dev = torch.device("cuda", torch.cuda.current_device())
     layout, V, dtype, _ = synth.config_layout(args.config, seed=args.seed)
     cfg = dart.Config(entropy_q=args.q, beta_kl=args.beta, zero_fill_masked=0 if args.compact else 1,
                       select_rule=dart.SEL_OFF if args.q <= 0 else dart.SEL_FLOOR)
-    sp = StreamedPass(layout, V, cfg, dev, max_rows=args.stream_rows, pool=args.pool, logits_dtype=dtype)
+    group = tdist.group.WORLD if world > 1 else None
+    shards = D.shard_layout(layout, world)
+    me = shards[rank]
+    sp = StreamedPass(layout, V, cfg, dev, max_rows=args.stream_rows, pool=args.pool, logits_dtype=dtype,
+                      group=group, world_shards=shards)
     P = sp.P
     # synthetic rows for the P pool slots (P x rows tokens, the config's value
     # recipe); chunk c row r reads slot (c mod P) row r in both sweeps
@@ -169,24 +179,27 @@ def run_streamed(args):
                        step_tok_off=np.minimum(np.arange(nstep + 1, dtype=np.int64) * 64, P * rows),
                        step_fork=np.random.default_rng(args.seed).random(nstep) < 0.3)
     t0 = time.time()
-    sb = synth.make_batch(args.config, seed=args.seed, device=dev, layout=sub, V=V, dtype=dtype)
+    sb = synth.make_batch(args.config, seed=args.seed * 1000 + rank, device=dev, layout=sub, V=V, dtype=dtype)
     for k in range(P):
         sp.pool_logits[k].copy_(sb.logits[k * rows:(k + 1) * rows])
     T = layout.T
-    idx = torch.empty(T, dtype=torch.int64, device=dev)
+    idx = torch.empty(me.T_loc, dtype=torch.int64, device=dev)
     for i, c in enumerate(sp.chunks):
         base = (i % P) * rows
-        idx[c.tok_begin:c.tok_end] = torch.arange(base, base + c.T_loc, device=dev)
+        idx[c.tok_begin - me.tok_begin:c.tok_end - me.tok_begin] = torch.arange(base, base + c.T_loc, device=dev)
     target, lo, lr, lref = (x[idx].contiguous() for x in (sb.target, sb.logp_old, sb.logp_rollout, sb.logp_ref))
     del sb
     torch.cuda.synchronize()
-    log(f"streamed {args.config}: T={T} in {len(sp.chunks)} chunks of <= {sp.rows} rows, pool {P}; "
-        f"setup {time.time() - t0:.1f}s")
+    log(f"[rank {rank}] streamed {args.config}: T={T} (local {me.T_loc}) in {len(sp.chunks)} chunks of "
+        f"<= {sp.rows} rows, pool {P}; setup {time.time() - t0:.1f}s")
     for _ in range(args.warmup):
         sp.run(target, lo, lr, lref)
     torch.cuda.synchronize()
     sp.status.zero_()
     sp.launches = 0
+    if world > 1:
+        tdist.barrier()
+    torch.cuda.synchronize()
     stream = torch.cuda.current_stream()
     clk = ClockSampler(local)
     clk.start()
@@ -198,27 +211,45 @@ def run_streamed(args):
         sp.run(target, lo, lr, lref)
     s1.record(stream)
     torch.cuda.synchronize()
+    if world > 1:
+        tdist.barrier()
     clocks = clk.stop()
     sp.check_status()
-    ms = s0.elapsed_time(s1) / args.steps
+    ms_loc = s0.elapsed_time(s1) / args.steps
+    ms = ms_loc
+    if world > 1:
+        t = torch.tensor([ms_loc, -ms_loc], dtype=torch.float64, device=dev)
+        D.all_reduce(t, op=tdist.ReduceOp.MAX)
+        ms, ms_min = float(t[0].item()), -float(t[1].item())
     keep = sp.keep.cpu().numpy()[:layout.S].astype(bool)
     n = np.diff(layout.step_tok_off)
+    kept_loc = int(n[me.step_begin:me.step_end][keep[me.step_begin:me.step_end]].sum())
     kept = int(n[keep].sum())
     es = 2
-    byts = T * (es * V + 24) + kept * 2 * es * V + (0 if args.compact else (T - kept) * es * V)
+    byts = me.T_loc * (es * V + 24) + kept_loc * 2 * es * V + (0 if args.compact else (me.T_loc - kept_loc) * es * V)
     peak, src = hbm_peak()
     gbs = byts / (ms * 1e-3) / 1e9
-    line = {"metric": "loss fwd+bwd logit-tokens/s at V=152064 bf16, % of HBM peak, 1/2/4/8 GPU",
-            "value": T / (ms * 1e-3), "unit": "logit-tokens/s", "n_gpus": 1, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
-            "vs_baseline": None, "dtype": "bf16", "data": "synthetic (seeded; pooled chunk logits)",
-            "config": {"workload": args.config, "global_tokens": T, "V": V, "groups": layout.G,
-                       "steps_total": layout.S, "chunks": len(sp.chunks), "chunk_rows": sp.rows, "pool": P,
-                       "kept_token_frac": kept / T, "streamed": True},
-            "roofline": {"bound": "hbm", "kernel": "whole step (fwd+select+bwd sweeps)", "achieved": gbs,
-                         "peak": peak, "peak_source": src, "unit": "GB/s", "frac": gbs / peak, "traffic": None},
-            "gpu_launches": sp.launches, "clocks": clocks, "e2e": None, "cpu_baseline": None}
-    print(json.dumps(line), flush=True)
+    if rank == 0:
+        line = {"metric": "loss fwd+bwd logit-tokens/s at V=152064 bf16, % of HBM peak, 1/2/4/8 GPU",
+                "value": T / (ms * 1e-3), "unit": "logit-tokens/s", "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+                "scaling": "strong" if world > 1 else "weak",
+                "vs_baseline": None, "dtype": "bf16", "data": "synthetic (seeded; pooled chunk logits)",
+                "config": {"workload": args.config, "global_tokens": T, "tokens_per_gpu": me.T_loc, "V": V,
+                           "groups": layout.G, "steps_total": layout.S, "chunks": len(sp.chunks),
+                           "chunk_rows": sp.rows, "pool": P, "kept_token_frac": kept / T, "streamed": True,
+                           "l2": "inputs larger than L2 (pooled chunks of %.1f GB)" % (sp.rows * V * es / 1e9),
+                           "parallelism": f"dp{world} (trajectory-sharded, global batch split across ranks)"},
+                "roofline": {"bound": "hbm", "kernel": "whole step (fwd+select+bwd sweeps), rank 0",
+                             "achieved": gbs, "peak": peak, "peak_source": src, "unit": "GB/s", "frac": gbs / peak,
+                             "traffic": None},
+                "gpu_launches": sp.launches, "clocks": clocks, "e2e": None, "cpu_baseline": None}
+        if world > 1:
+            line["rank_time_ms"] = {"max": ms, "min": ms_min}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        tdist.barrier()
+        tdist.destroy_process_group()
 
 
 # ------------------------------------------------------------------ our arm

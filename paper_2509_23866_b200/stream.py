@@ -17,6 +17,14 @@ slot (e.g. from the LM head or a host copy); for throughput measurement the
 bench fills each slot once and re-uses it, which keeps both sweeps reading
 identical bytes.  `consume(c, dlogits)` receives each chunk's gradient.
 
+Across ranks (`group`): rank r streams the chunks of its own shard (a
+contiguous, token-balanced range of whole trajectories, `dist.shard_layout`).
+Every rank's chunks are the virtual ranks of ONE global selection: rank r
+owns virtual ranks [r*C_max, (r+1)*C_max) (C_max = the largest per-rank chunk
+count; missing ones are empty), so C1 is a single all-gather of each rank's
+[C_max, S_pad] step-entropy block, `dart_select_steps` then yields the same
+keep bits and normaliser on every rank, and C2 all-reduces the statistics.
+
 All arithmetic runs in the CUDA library; this module only sequences the ABI
 calls and owns the buffers.
 """
@@ -32,16 +40,18 @@ from . import dart
 from .dart import DART_BF16, DART_F32, Shard, _check, _ptr
 
 
-def chunk_layout(layout, max_rows: int) -> List[Shard]:
-    """Greedy split into contiguous ranges of whole trajectories with at most
-    `max_rows` token rows each (a single longer trajectory gets its own chunk)."""
+def chunk_layout(layout, max_rows: int, traj_begin: int = 0, traj_end: Optional[int] = None) -> List[Shard]:
+    """Greedy split of trajectories [traj_begin, traj_end) into contiguous
+    ranges of whole trajectories with at most `max_rows` token rows each (a
+    single longer trajectory gets its own chunk)."""
     tso = np.asarray(layout.traj_step_off, dtype=np.int64)
     sto = np.asarray(layout.step_tok_off, dtype=np.int64)
+    end = layout.N_traj if traj_end is None else int(traj_end)
     shards = []
-    a = 0
-    while a < layout.N_traj:
+    a = int(traj_begin)
+    while a < end:
         b = a + 1
-        while b < layout.N_traj and sto[tso[b + 1]] - sto[tso[a]] <= max_rows:
+        while b < end and sto[tso[b + 1]] - sto[tso[a]] <= max_rows:
             b += 1
         s0, s1 = int(tso[a]), int(tso[b])
         shards.append(Shard(a, b, s0, s1, int(sto[s0]), int(sto[s1])))
@@ -49,17 +59,47 @@ def chunk_layout(layout, max_rows: int) -> List[Shard]:
     return shards
 
 
+def virtual_ranks(layout, world_shards: List[Shard], max_rows: int):
+    """Chunks of every rank and the global virtual-rank table: returns
+    (chunks per rank, C_max, S_pad, rank_step_off [world*C_max + 1]); rank r's
+    chunk j is virtual rank r*C_max + j, missing ones are empty (no steps)."""
+    per = [chunk_layout(layout, max_rows, sh.traj_begin, sh.traj_end) or [sh] for sh in world_shards]
+    # (a rank without trajectories keeps one empty chunk: its forward call
+    # still builds the global group tables the selection reads)
+    c_max = max(1, max(len(c) for c in per))
+    s_pad = max(1, max((c.S_loc for cs in per for c in cs), default=1))
+    off = []
+    for sh, cs in zip(world_shards, per):
+        off.extend([c.step_begin for c in cs] + [sh.step_end] * (c_max - len(cs)))
+    off.append(int(layout.S))
+    return per, c_max, s_pad, np.asarray(off, dtype=np.int64)
+
+
 class StreamedPass:
     def __init__(self, layout, V: int, cfg: dart.Config, device, max_rows: int, pool: int = 3,
-                 logits_dtype=torch.bfloat16, grad_dtype=torch.bfloat16):
+                 logits_dtype=torch.bfloat16, grad_dtype=torch.bfloat16, group=None,
+                 world_shards: Optional[List[Shard]] = None):
         self.L = dart.lib()
         dev = torch.device(device)
         self.device, self.layout, self.V, self.cfg = dev, layout, int(V), cfg
         self.logits_dtype, self.grad_dtype = logits_dtype, grad_dtype
         self.meta = dart.Meta.from_layout(layout, dev)
-        self.chunks = chunk_layout(layout, max_rows)
-        self.rows = max(c.T_loc for c in self.chunks)
-        self.P = min(pool, len(self.chunks))
+        self.group = group
+        if group is not None:
+            import torch.distributed as tdist
+            from . import dist as D
+            self.world, self.rank = tdist.get_world_size(group), tdist.get_rank(group)
+            world_shards = world_shards or D.shard_layout(layout, self.world)
+        else:
+            self.world, self.rank = 1, 0
+            world_shards = world_shards or [dart.whole_shard(layout)]
+        if len(world_shards) != self.world:
+            raise dart.DartError("world_shards must hold one shard per rank")
+        self.shard = world_shards[self.rank]
+        per, self.C_max, self.S_pad, rso = virtual_ranks(layout, world_shards, max_rows)
+        self.chunks = per[self.rank]
+        self.rows = max([c.T_loc for c in self.chunks] + [1])
+        self.P = max(1, min(pool, len(self.chunks)))
         self.pool_logits = [torch.empty((self.rows, self.V), dtype=logits_dtype, device=dev) for _ in range(self.P)]
         self.pool_dlogits = [torch.empty((self.rows, self.V), dtype=grad_dtype, device=dev) for _ in range(self.P)]
         f32 = dict(dtype=torch.float32, device=dev)
@@ -71,11 +111,12 @@ class StreamedPass:
         self.tau = torch.empty(max(layout.G, 1), **f32)
         self.norm = torch.empty(5, dtype=torch.int64, device=dev)
         n = len(self.chunks)
-        self.S_pad = max(max(c.S_loc for c in self.chunks), 1)
-        self.gathered = torch.zeros(n * self.S_pad, **f32)
-        self.rank_step_off = torch.tensor([c.step_begin for c in self.chunks] + [self.chunks[-1].step_end],
-                                          dtype=torch.int64, device=dev)
-        self.stats_all = torch.zeros((n, len(dart.STATS_FIELDS)), dtype=torch.float64, device=dev)
+        self.n_virtual = self.world * self.C_max
+        self.local_H = torch.zeros(self.C_max * self.S_pad, **f32)       # this rank's block of C1
+        self.gathered = torch.zeros(self.n_virtual * self.S_pad, **f32)
+        self.rank_step_off = torch.as_tensor(rso, dtype=torch.int64).to(dev)
+        self.stats_all = torch.zeros((max(n, 1), len(dart.STATS_FIELDS)), dtype=torch.float64, device=dev)
+        self.stats = torch.zeros(len(dart.STATS_FIELDS), dtype=torch.float64, device=dev)
         # per-chunk state: forward outputs + workspace (tens of bytes per token)
         self.state = []
         for c in self.chunks:
@@ -102,27 +143,35 @@ class StreamedPass:
 
     def run(self, target, logp_old, logp_roll, logp_ref, fill: Optional[Callable] = None,
             consume: Optional[Callable] = None):
-        """target / log-prob inputs are global [T] device tensors.  fill(c, buf)
-        must write chunk c's logits into buf[:T_c] (None: the pool slot already
-        holds them).  consume(c, dlogits) gets a view of chunk c's gradient."""
+        """target / log-prob inputs are this rank's [T_loc] device tensors
+        (the whole batch when single-process; row 0 = the shard's first
+        token).  fill(c, buf) must write local chunk c's logits into buf[:T_c]
+        (None: the pool slot already holds them).  consume(c, dlogits) gets a
+        view of chunk c's gradient.  Returns the (all-reduced) statistics."""
         s = torch.cuda.current_stream(self.device).cuda_stream
         meta, cfg = ctypes.byref(self.meta.c()), ctypes.byref(self.cfg.c())
         beta = self.cfg.beta_kl > 0
+        base = self.shard.tok_begin
         batches = []
         for i, c in enumerate(self.chunks):           # sweep 1: forward over every chunk
             buf = self.pool_logits[i % self.P]
             if fill is not None:
                 fill(i, buf)
-            sl = slice(c.tok_begin, c.tok_end)
+            sl = slice(c.tok_begin - base, c.tok_end - base)
             b = self._batch(c, buf, target[sl], logp_old[sl], logp_roll[sl], logp_ref[sl] if beta else None)
             batches.append(b)
             st = self.state[i]
             _check(self.L.dart_loss_fwd(ctypes.byref(b), meta, cfg, ctypes.byref(self._out(st)), _ptr(st["ws"]),
                                         st["ws_bytes"], ctypes.c_void_p(s)))
             self.launches += self.L.dart_last_launch_count()
-            self.gathered[i * self.S_pad: i * self.S_pad + c.S_loc].copy_(st["step_H"][:c.S_loc])
+            self.local_H[i * self.S_pad: i * self.S_pad + c.S_loc].copy_(st["step_H"][:c.S_loc])
+        if self.world > 1:                             # C1: one all-gather of every rank's block
+            from . import dist as D
+            D.all_gather_into(self.gathered, self.local_H, group=self.group)
+        else:
+            self.gathered.copy_(self.local_H)
         st0 = self.state[0]                            # select once (chunk 0's ws holds the group table)
-        _check(self.L.dart_select_steps(_ptr(self.gathered), _ptr(self.rank_step_off), len(self.chunks),
+        _check(self.L.dart_select_steps(_ptr(self.gathered), _ptr(self.rank_step_off), self.n_virtual,
                                         self.S_pad, meta, cfg, _ptr(self.group_ok), _ptr(self.keep),
                                         _ptr(self.tau), _ptr(self.norm), _ptr(st0["ws"]), st0["ws_bytes"],
                                         ctypes.c_void_p(s)))
@@ -140,11 +189,14 @@ class StreamedPass:
             self.launches += self.L.dart_last_launch_count()
             if consume is not None:
                 consume(i, out[:c.T_loc])
-        return self.stats_all
+        torch.sum(self.stats_all, dim=0, out=self.stats)
+        if self.world > 1:                             # C2: statistics all-reduce
+            from . import dist as D
+            D.all_reduce(self.stats, group=self.group)
+        return self.stats
 
     def stats_dict(self):
-        tot = self.stats_all.sum(dim=0).cpu().tolist()
-        return dict(zip(dart.STATS_FIELDS, tot))
+        return dict(zip(dart.STATS_FIELDS, self.stats.cpu().tolist()))
 
     def check_status(self):
         v = int(self.status.item())

@@ -42,3 +42,74 @@ def test_streamed_equals_resident(max_rows, pool):
     L = ref.stats_dict()["loss"]
     assert abs(sp.stats_dict()["loss"] - L) <= 1e-12 * abs(L) + 1e-15
     assert sp.stats_dict()["n_kept_tok"] == ref.stats_dict()["n_kept_tok"]
+
+
+def _mr_worker(rank, world, port, max_rows, q):
+    import os
+    import torch.distributed as dist
+    from paper_2509_23866_b200 import dist as D
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        torch.cuda.set_device(0)
+        dev = torch.device("cuda", 0)
+        b = synth.make_batch("mid", seed=4)
+        shards = D.shard_layout(b.layout, world)
+        me = shards[rank]
+        sp = StreamedPass(b.layout, b.V, dart.Config(), dev, max_rows=max_rows, pool=2, group=dist.group.WORLD,
+                          world_shards=shards)
+        logits = b.logits.to(dev)
+        got = torch.empty((me.T_loc, b.V), dtype=torch.bfloat16, device=dev)
+
+        def fill(i, buf):
+            c = sp.chunks[i]
+            buf[:c.T_loc].copy_(logits[c.tok_begin:c.tok_end])
+
+        def consume(i, dz):
+            c = sp.chunks[i]
+            got[c.tok_begin - me.tok_begin:c.tok_end - me.tok_begin].copy_(dz)
+
+        sl = slice(me.tok_begin, me.tok_end)
+        sp.run(*(x[sl].to(dev).contiguous() for x in (b.target, b.logp_old, b.logp_rollout, b.logp_ref)),
+               fill=fill, consume=consume)
+        torch.cuda.synchronize()
+        sp.check_status()
+        q.put((rank, got.view(torch.int16).cpu().numpy(), sp.keep.cpu().numpy(), sp.norm.cpu().numpy(),
+               sp.stats_dict(), me.tok_begin, me.tok_end, len(sp.chunks)))
+    except Exception as e:  # pragma: no cover
+        q.put((rank, repr(e), None, None, None, 0, 0, 0))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("max_rows", [300, 100000])
+def test_streamed_two_ranks_equal_resident(max_rows):
+    """The multi-rank streamed pass (each rank streams its own shard's chunks,
+    one all-gather of every rank's per-chunk step entropies, one selection,
+    statistics all-reduce) with 2 ranks sharing one GPU through gloo: each
+    rank's dlogits bitwise equal to the resident unsharded pass."""
+    import socket
+    import torch.multiprocessing as mp
+    b = synth.make_batch("mid", seed=4)
+    ref = run_gpu(b, dart.Config())
+    ref_dz = ref.dlogits.view(torch.int16).cpu().numpy()
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    ps = [ctx.Process(target=_mr_worker, args=(r, 2, port, max_rows, q)) for r in range(2)]
+    for p in ps:
+        p.start()
+    res = [q.get(timeout=600) for _ in ps]
+    for p in ps:
+        p.join(timeout=60)
+    L = ref.stats_dict()["loss"]
+    for rank, dz, keep, norm, st, t0, t1, nch in res:
+        assert keep is not None, dz
+        assert np.array_equal(keep[:b.layout.S], ref.keep.cpu().numpy()[:b.layout.S])
+        assert np.array_equal(norm, ref.norm.cpu().numpy())
+        assert np.array_equal(dz, ref_dz[t0:t1])
+        assert abs(st["loss"] - L) <= 1e-12 * abs(L) + 1e-15       # all-reduced on every rank
+        assert st["n_kept_tok"] == ref.stats_dict()["n_kept_tok"]
