@@ -825,7 +825,11 @@ def run_e2e(args, dl, batch, stream, world, inputs):
     """Same pass through the public API with the step's inputs copied from
     pinned host memory each step and the loss read back to the host."""
     from paper_2509_23866_b200 import dart  # noqa: F401
-    host = [t.cpu().pin_memory() for t in inputs]
+    host = []
+    for t in inputs:           # straight into pinned memory (no pageable staging copy)
+        h = torch.empty(t.shape, dtype=t.dtype, pin_memory=True)
+        h.copy_(t)
+        host.append(h)
     dev_bufs = [torch.empty_like(t, device=batch.logits.device) for t in host]
     loss_h = torch.empty(len(dl.stats), dtype=torch.float64).pin_memory()
     h2d = sum(t.numel() * t.element_size() for t in host)

@@ -85,13 +85,21 @@ EXPORTED = ["dart_workspace_size", "dart_loss_fwd", "dart_select_steps", "dart_l
 GEMM_STORE_F32, GEMM_STORE_BF16, GEMM_ACCUM_F32 = 0, 1, 2
 
 
-def gemm_bf16(A, B, C, a_mn_major=False, b_mn_major=False, mode=GEMM_STORE_F32, stream=None):
+def gemm_bf16(A, B, C, a_mn_major=False, b_mn_major=False, mode=None, stream=None):
     """C (+)= A_op @ B_op^T on the tensor cores (dart_gemm_bf16).  A_op is A
     ([M, K]) or, with a_mn_major, A.T where A is stored [K, M]; likewise B_op
-    ([N, K] or B stored [K, N]).  C: fp32 (STORE_F32 / ACCUM_F32) or bf16 [M, N]."""
+    ([N, K] or B stored [K, N]).  C: fp32 (STORE_F32 / ACCUM_F32) or bf16
+    (STORE_BF16) [M, N]; mode=None picks the store mode from C's dtype, and a
+    mode that does not match C's dtype is refused (the ABI sees only a
+    pointer: an fp32 store into a bf16 buffer would run past its end)."""
     _require_cuda(A, B, C)
     if A.dtype != torch.bfloat16 or B.dtype != torch.bfloat16:
         raise DartError("gemm_bf16 takes bf16 operands")
+    if mode is None:
+        mode = GEMM_STORE_BF16 if C.dtype == torch.bfloat16 else GEMM_STORE_F32
+    want = torch.bfloat16 if mode == GEMM_STORE_BF16 else torch.float32
+    if mode not in (GEMM_STORE_F32, GEMM_STORE_BF16, GEMM_ACCUM_F32) or C.dtype != want:
+        raise DartError(f"gemm_bf16 mode {mode} needs a {want} C, got {C.dtype}")
     if A.stride(1) != 1 or B.stride(1) != 1 or C.stride(1) != 1:
         raise DartError("row-major operands expected")
     M, K = (A.shape[1], A.shape[0]) if a_mn_major else (A.shape[0], A.shape[1])

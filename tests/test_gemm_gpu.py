@@ -64,3 +64,20 @@ def test_gemm_rejects_bad_arguments():
     C = torch.zeros(64, 60, device="cuda")                                   # N % 8 != 0
     with pytest.raises(dart.DartError):
         dart.gemm_bf16(A, A[:60], C)
+
+
+def test_gemm_store_mode_must_match_c_dtype():
+    """The ABI sees only C's pointer: an fp32 store into a bf16 buffer would
+    run past its end, so the binding refuses a mode that does not match C's
+    dtype and, by default, picks the store mode from it."""
+    A = torch.ones(128, 64, dtype=torch.bfloat16, device="cuda")
+    Cb = torch.zeros(128, 256, dtype=torch.bfloat16, device="cuda")
+    Cf = torch.zeros(128, 256, device="cuda")
+    with pytest.raises(dart.DartError):
+        dart.gemm_bf16(A, A.new_ones(256, 64), Cb, mode=dart.GEMM_STORE_F32)
+    with pytest.raises(dart.DartError):
+        dart.gemm_bf16(A, A.new_ones(256, 64), Cf, mode=dart.GEMM_STORE_BF16)
+    dart.gemm_bf16(A, A.new_ones(256, 64), Cb)                                # inferred: bf16 store
+    dart.gemm_bf16(A, A.new_ones(256, 64), Cf)                                # inferred: fp32 store
+    torch.cuda.synchronize()
+    assert torch.all(Cb == 64) and torch.all(Cf == 64)
