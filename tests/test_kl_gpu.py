@@ -109,3 +109,60 @@ def test_exact_kl_zero_for_identical_reference():
     b.ref_logits = b.logits.clone()
     dl = _run(b, dart.Config(kl_mode=dart.KL_EXACT, beta_kl=0.5))
     assert float(dl.stats_dict()["sum_kl"]) <= 1e-5 * b.layout.T
+
+
+def test_exact_kl_single_config_full_size_sampled():
+    """BASELINE.json single config at full size (T = 61440, V = 152064 bf16,
+    reference logits of the same shape) as `bench.py --kl exact` runs it:
+    selection from the GPU's own step entropies, 10 sampled rows against the
+    oracle row by row (kl_exact_row / token_row / token_loss composed as in
+    `loss_pass`: l = surrogate + beta KL, dz = c invT [dl/dlogp (onehot - p)
+    + beta p (log p - log q - KL)]), masked rows zero."""
+    b = synth.make_batch("single", seed=0, device="cuda", with_ref=True)
+    cfg = dart.Config(kl_mode=dart.KL_EXACT)
+    cfgf = cfg.as_f32()
+    dl = _run(b, cfg)
+    L = b.layout
+    keep = dl.keep.cpu().numpy()[:L.S]
+    keep_same, _ = oracle_select_on(dl, b, cfgf)
+    assert np.array_equal(keep, keep_same)
+    nd = dl.norm_dict()
+    tok_keep = np.repeat(keep, np.diff(L.step_tok_off)).astype(bool)
+    A, _ = O.advantages(L.traj_reward, L.traj_group, L.traj_step_off, L.G)
+    s_of_t = O.step_of_token(L.step_tok_off, L.T)
+    tr_of_s = O.traj_of_step(L.traj_step_off, L.S)
+    cfg0 = {**cfgf, "beta_kl": 0.0}
+    beta, invT = cfgf["beta_kl"], cfgf["inv_temperature"]
+    rng = np.random.default_rng(11)
+    for t in sorted(rng.choice(np.nonzero(tok_keep)[0], 10, replace=False).tolist()):
+        z = b.logits[t].float().cpu().numpy()
+        zr = b.ref_logits[t].float().cpu().numpy()
+        y = int(b.target[t])
+        lse, logp, H, p = O.token_row(z, y, invT)
+        klt, lpq = O.kl_exact_row(z, zr, invT)
+        pg, dpg, w, r, clipped, _ = O.token_loss(logp, float(b.logp_old[t]), float(b.logp_rollout[t]),
+                                                 float(b.logp_ref[t]), A[tr_of_s[s_of_t[t]]], cfg0)
+        assert abs(float(dl.H[t]) - H) <= RTOL_ENT * H + ATOL_ENT
+        assert abs(float(dl.logp[t]) - logp) <= ATOL_LOGP
+        if min(abs(r - (1 - cfgf["eps_low"])), abs(r - (1 + cfgf["eps_high"]))) < 1e-5 * r:
+            continue
+        ell = pg + beta * klt
+        assert abs(float(dl.ell[t]) - ell) <= RTOL_TOK * abs(ell) + ATOL_TOK
+        c = nd["inv_norm"]
+        onehot = np.zeros_like(p)
+        onehot[y] = 1.0
+        term = np.where(p > 0, p * (np.nan_to_num(lpq, nan=0.0, posinf=0.0, neginf=0.0) - klt), 0.0)
+        dref = c * dpg * invT * (onehot - p) + c * beta * invT * term
+        a = abs(c * invT)
+        tol = bf16_ulp(dref) + a * (RTOL_TOK * abs(dpg) + ATOL_TOK) * np.abs(onehot - p)
+        tol = tol + a * 4e-6 * p * (abs(dpg) + beta * (np.abs(lpq) + klt + 1.0))
+        tol = tol + a * beta * p * 2e-5 * (1.0 + np.abs(lpq)) + 1e-38
+        dz = dl.dlogits[t].float().cpu().numpy()
+        err = np.abs(dz - dref)
+        assert np.all(err <= tol), (t, np.argmax(err - tol), err.max())
+    masked = torch.as_tensor(np.nonzero(~tok_keep)[0][:128], device="cuda")
+    assert torch.all(dl.dlogits[masked] == 0)
+    st = dl.stats_dict()
+    ell_all = dl.ell.cpu().numpy().astype(np.float64)
+    L_chk = np.sum(ell_all[tok_keep]) * nd["inv_norm"]
+    assert abs(st["loss"] - L_chk) <= 1e-9 * np.sum(np.abs(ell_all[tok_keep])) * nd["inv_norm"] + 1e-15
