@@ -142,3 +142,60 @@ def test_lmhead_update_default_clip_rows():
     err = np.abs(dh.cpu().numpy() - dh_ref)
     bad = np.argwhere((err > tol) & ~near[:, None])
     assert bad.size == 0, (bad[:5], err[tuple(bad[0])], tol[tuple(bad[0])], ref["dell"][bad[0][0]], r[bad[0][0]])
+
+
+def test_lmhead_update_full_size_sampled_rows():
+    """`bench.py --lmhead --update` at full size (T = 61440, d = 3584,
+    V = 152064, 8192-row chunks): dh on sampled rows against the oracle
+    (z_t = h_t W^T in float64 -> the loss terms -> dz_t -> dz_t W, same error
+    model as above), masked rows' dh exactly zero.  The mask is the old pass's
+    (checked against the oracle's rule on the GPU's own step entropies, the
+    same-precision decision); the normaliser is recomputed from it here."""
+    layout, V, _, _ = synth.config_layout("single", seed=0)
+    d = 3584
+    lb = synth.make_lmhead(None, d, seed=0, device="cuda", layout=layout, V=V)
+    b = lb.batch
+    cfg = dart.Config()
+    cfgf = cfg.as_f32()
+    old = old_pass(lb, cfg)
+    L = b.layout
+    from tests.gpu_helpers import oracle_select_on
+    keep_same, _ = oracle_select_on(old, b, cfgf)
+    keep = old.keep.cpu().numpy()[:L.S]
+    assert np.array_equal(keep, keep_same)
+    up, dh, dW = run_update(lb, cfg, old.keep, old.norm, 8192)
+    assert len(up.chunks) == 8
+    tok_keep = np.repeat(keep, np.diff(L.step_tok_off)).astype(bool)
+    inv_norm = 1.0 / float(tok_keep.sum())                    # TOKEN_MEAN_KEPT (SURVEY Q11)
+    A, _ = O.advantages(L.traj_reward, L.traj_group, L.traj_step_off, L.G)
+    s_of_t = O.step_of_token(L.step_tok_off, L.T)
+    tr_of_s = O.traj_of_step(L.traj_step_off, L.S)
+    W = lb.weight.float().cpu().numpy().astype(np.float64)
+    rng = np.random.default_rng(5)
+    rows = rng.choice(np.nonzero(tok_keep)[0], 4, replace=False).tolist()
+    dh_np = dh.cpu().numpy()
+    for t in rows:
+        h_t = lb.hidden[t].float().cpu().numpy().astype(np.float64)
+        z = O.lmhead_logits(h_t[None, :], W)[0]
+        y = int(b.target[t])
+        lse, logp, H, p = O.token_row(z, y)
+        ell, dell, w, r, clipped, kl = O.token_loss(logp, float(b.logp_old[t]), float(b.logp_rollout[t]),
+                                                    float(b.logp_ref[t]), A[tr_of_s[s_of_t[t]]], cfgf)
+        Ez = float((-(-d // 16) + 4) * U * (np.abs(h_t) @ np.abs(W).T).max())
+        if min(abs(r - (1 - cfgf["eps_low"])), abs(r - (1 + cfgf["eps_high"]))) < (1e-5 + 4 * Ez) * r:
+            continue
+        g = inv_norm * dell
+        onehot = np.zeros_like(p)
+        onehot[y] = 1.0
+        dz = g * (onehot - p)
+        dh_ref = dz @ W            # lmhead_grads' dL/dh row (its [V, d] dW product is not needed here)
+        rel = 2.0 ** -8 + 2e-5 + 2 * Ez + ATOL_TOK / max(abs(dell), 1e-30)
+        a = abs(g) * (P_REL + 2 * Ez) * p
+        tol = (rel + (-(-V // 16) + 4) * U) * (np.abs(dz) @ np.abs(W)) + a @ np.abs(W) + 1e-30
+        err = np.abs(dh_np[t] - dh_ref)
+        assert np.all(err <= tol), (t, err.max(), tol[np.argmax(err - tol)])
+    masked = np.nonzero(~tok_keep)[0][:256]
+    assert np.all(dh_np[masked] == 0)
+    assert np.all(np.isfinite(dW[:4096].cpu().numpy()))
+    st = up.stats_dict()
+    assert st["n_kept_tok"] == tok_keep.sum()
