@@ -221,10 +221,24 @@ __global__ void __launch_bounds__(GM_THREADS, 1)
 // pair leader issues tcgen05.mma.cta_group::2 (M = 256, N = 256) and each CTA
 // reads its 128 accumulator rows from its own TMEM.  Per SM this halves the
 // shared-memory / L2 operand traffic of the B panel.
-constexpr int G2_STAGES = 6;
-constexpr uint32_t G2_A_BYTES = 128 * GM_BK * 2, G2_B_BYTES = 128 * GM_BK * 2;
-constexpr uint32_t G2_STAGE_BYTES = G2_A_BYTES + G2_B_BYTES;
-constexpr size_t G2_SMEM = 1024 + (size_t)G2_STAGES * G2_STAGE_BYTES + 256;
+// NW = 2 ("wide"): the pair computes a 256 x 512 tile -- each CTA stages 128
+// rows of A and 2 x 128 rows of B per stage, the leader issues two N = 256
+// MMAs per K step into the two halves of one 512-column accumulator -- so a
+// tile moves (256 + 512) K rows from L2 per 2x the flops: 3/4 of the NW = 1
+// operand traffic (ncu: our 256 x 256 pair kernel reads the theoretical
+// 70 GB through L2 for z = h W^T, cuBLAS 52 GB), at the price of a single
+// accumulator (the epilogue no longer overlaps the next tile's MMAs).
+template <int NW> struct G2 {
+  static constexpr int STAGES = NW == 1 ? 6 : 4;
+  static constexpr int ACC = NW == 1 ? 2 : 1;
+  static constexpr int BN = 256 * NW;                       // tile N (pair)
+  static constexpr uint32_t A_BYTES = 128 * GM_BK * 2;      // per CTA per stage
+  static constexpr uint32_t B_HALF = 128 * GM_BK * 2;       // one N = 256 MMA's share of B per CTA
+  static constexpr uint32_t B_BYTES = B_HALF * NW;
+  static constexpr uint32_t STAGE_BYTES = A_BYTES + B_BYTES;
+  static constexpr size_t SMEM = 1024 + (size_t)STAGES * STAGE_BYTES + 256;
+};
+constexpr size_t G2_SMEM = G2<1>::SMEM;
 
 __device__ __forceinline__ uint32_t g2_rank() {
   uint32_t r;
@@ -250,10 +264,13 @@ __device__ __forceinline__ void g2_tile(const GemmParams& p, int64_t t, int& mt,
   gm_tile(p, t, mt, nt);
 }
 
-template <bool A_MN, bool B_MN>
+template <bool A_MN, bool B_MN, int NW>
 __global__ void __launch_bounds__(GM_THREADS, 1)
     gemm_bf16_2sm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                          const GemmParams p) {
+  using C2 = G2<NW>;
+  constexpr int G2_STAGES = C2::STAGES, G2_ACC = C2::ACC, G2_BN = C2::BN;
+  constexpr uint32_t G2_A_BYTES = C2::A_BYTES, G2_B_BYTES = C2::B_BYTES, G2_STAGE_BYTES = C2::STAGE_BYTES;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
   uint8_t* sA = smem;
@@ -261,8 +278,8 @@ __global__ void __launch_bounds__(GM_THREADS, 1)
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + G2_STAGES * G2_STAGE_BYTES);
   uint64_t* empty = full + G2_STAGES;
   uint64_t* tfull = empty + G2_STAGES;
-  uint64_t* tempty = tfull + GM_ACC;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + GM_ACC);
+  uint64_t* tempty = tfull + G2_ACC;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + G2_ACC);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t rank = g2_rank();
   const bool leader = rank == 0;
@@ -271,7 +288,7 @@ __global__ void __launch_bounds__(GM_THREADS, 1)
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
     }
-    for (int a = 0; a < GM_ACC; ++a) {
+    for (int a = 0; a < G2_ACC; ++a) {
       mbar_init(&tfull[a], 1);
       mbar_init(&tempty[a], 8);            // 4 epilogue warps x 2 CTAs (leader's copy is the one used)
     }
@@ -300,18 +317,23 @@ __global__ void __launch_bounds__(GM_THREADS, 1)
           if (leader) mbar_arrive_expect_tx(&full[stage], 2 * G2_STAGE_BYTES);   // both CTAs' bytes
           uint8_t* a = sA + stage * G2_A_BYTES;
           uint8_t* b = sB + stage * G2_B_BYTES;
-          const int m0 = mt * 256 + 128 * (int)rank, n0 = nt * 256 + 128 * (int)rank;
+          const int m0 = mt * 256 + 128 * (int)rank;
           if (A_MN) {
             tc::tma_load_2d_2sm(a, &tmA, &full[stage], m0, kb * GM_BK);
             tc::tma_load_2d_2sm(a + 8192, &tmA, &full[stage], m0 + 64, kb * GM_BK);
           } else {
             tc::tma_load_2d_2sm(a, &tmA, &full[stage], kb * GM_BK, m0);
           }
-          if (B_MN) {
-            tc::tma_load_2d_2sm(b, &tmB, &full[stage], n0, kb * GM_BK);
-            tc::tma_load_2d_2sm(b + 8192, &tmB, &full[stage], n0 + 64, kb * GM_BK);
-          } else {
-            tc::tma_load_2d_2sm(b, &tmB, &full[stage], kb * GM_BK, n0);
+#pragma unroll
+          for (int hh = 0; hh < NW; ++hh) {   // B rows of MMA hh: [nt*BN + 256 hh, +256), this CTA's 128
+            const int n0 = nt * G2_BN + 256 * hh + 128 * (int)rank;
+            uint8_t* bh = b + hh * C2::B_HALF;
+            if (B_MN) {
+              tc::tma_load_2d_2sm(bh, &tmB, &full[stage], n0, kb * GM_BK);
+              tc::tma_load_2d_2sm(bh + 8192, &tmB, &full[stage], n0 + 64, kb * GM_BK);
+            } else {
+              tc::tma_load_2d_2sm(bh, &tmB, &full[stage], kb * GM_BK, n0);
+            }
           }
           if (++stage == G2_STAGES) {
             stage = 0;
@@ -331,15 +353,19 @@ __global__ void __launch_bounds__(GM_THREADS, 1)
       for (int64_t t = cid; t < p.n_tiles; t += ncl) {
         mbar_wait(&tempty[acc], aph ^ 1u);
         tc::fence_after();
-        const uint32_t d_tmem = tmem + (uint32_t)(acc * GM_BN);
+        const uint32_t d_tmem = tmem + (uint32_t)(acc * G2_BN);
         for (int kb = 0; kb < KB; ++kb) {
           mbar_wait(&full[stage], ph);
           tc::fence_after();
           const uint64_t da = tc::smem_desc_sw128(smem_u32(sA + stage * G2_A_BYTES), a_lbo, 1024);
-          const uint64_t db = tc::smem_desc_sw128(smem_u32(sB + stage * G2_B_BYTES), b_lbo, 1024);
 #pragma unroll
-          for (int k = 0; k < GM_BK / 16; ++k)
-            tc::umma_bf16_2sm(d_tmem, da + a_kstep * k, db + b_kstep * k, idesc, (kb | k) != 0 ? 1u : 0u);
+          for (int hh = 0; hh < NW; ++hh) {
+            const uint64_t db = tc::smem_desc_sw128(smem_u32(sB + stage * G2_B_BYTES + hh * C2::B_HALF), b_lbo, 1024);
+#pragma unroll
+            for (int k = 0; k < GM_BK / 16; ++k)
+              tc::umma_bf16_2sm(d_tmem + 256 * hh, da + a_kstep * k, db + b_kstep * k, idesc,
+                                (kb | k) != 0 ? 1u : 0u);
+          }
           tc::umma_commit_2sm(&empty[stage], 0x3);
           if (++stage == G2_STAGES) {
             stage = 0;
@@ -347,7 +373,7 @@ __global__ void __launch_bounds__(GM_THREADS, 1)
           }
         }
         tc::umma_commit_2sm(&tfull[acc], 0x3);
-        if (++acc == GM_ACC) {
+        if (++acc == G2_ACC) {
           acc = 0;
           aph ^= 1u;
         }
@@ -364,12 +390,12 @@ __global__ void __launch_bounds__(GM_THREADS, 1)
       mbar_wait(&tfull[acc], aph);
       tc::fence_after();
       const int64_t m = (int64_t)mt * 256 + 128 * rank + r;
-      const uint32_t tbase = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * GM_BN);
+      const uint32_t tbase = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * G2_BN);
 #pragma unroll 1
-      for (int j = 0; j < GM_BN / 32; ++j) {
+      for (int j = 0; j < G2_BN / 32; ++j) {
         float x[32];
         tc::tmem_ld32(tbase + (uint32_t)(j * 32), x);
-        const int64_t n0 = (int64_t)nt * GM_BN + j * 32;
+        const int64_t n0 = (int64_t)nt * G2_BN + j * 32;
         if (m >= p.M || n0 >= p.N) continue;
         if (p.c_mode == DART_GEMM_STORE_BF16) {
           __nv_bfloat16* c = reinterpret_cast<__nv_bfloat16*>(p.C) + m * p.ldc + n0;
@@ -396,7 +422,7 @@ __global__ void __launch_bounds__(GM_THREADS, 1)
       tc::fence_before();
       __syncwarp();
       if (lane == 0) tc::mbar_arrive_remote(&tempty[acc], 0);   // the leader's accumulator-empty barrier
-      if (++acc == GM_ACC) {
+      if (++acc == G2_ACC) {
         acc = 0;
         aph ^= 1u;
       }
@@ -411,13 +437,15 @@ __global__ void __launch_bounds__(GM_THREADS, 1)
   }
 }
 
-template <bool A_MN, bool B_MN>
+template <bool A_MN, bool B_MN, int NW>
 cudaError_t launch_gemm_2sm(const CUtensorMap& ta, const CUtensorMap& tb, GemmParams p, int num_sms,
                             cudaStream_t st) {
-  auto kern = gemm_bf16_2sm_kernel<A_MN, B_MN>;
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)G2_SMEM);
+  auto kern = gemm_bf16_2sm_kernel<A_MN, B_MN, NW>;
+  constexpr size_t smem = G2<NW>::SMEM;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   p.n_mt = (p.M + 255) / 256;
+  p.n_nt = (p.N + G2<NW>::BN - 1) / G2<NW>::BN;
   p.n_tiles = (int64_t)p.n_mt * p.n_nt;
   cudaLaunchConfig_t cfg = {};
   cudaLaunchAttribute attr[1];
@@ -426,7 +454,7 @@ cudaError_t launch_gemm_2sm(const CUtensorMap& ta, const CUtensorMap& tb, GemmPa
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
   cfg.blockDim = dim3(GM_THREADS);
-  cfg.dynamicSmemBytes = G2_SMEM;
+  cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
@@ -475,10 +503,16 @@ cudaError_t launch_gemm_bf16(const void* A, bool a_mn, int64_t lda, const void* 
     const bool ok2a = a_mn ? tc::make_map_bf16(&ta2, A, K, M, lda, 64, 64) : tc::make_map_bf16(&ta2, A, M, K, lda, 64, 128);
     const bool ok2b = b_mn ? tc::make_map_bf16(&tb2, B, K, N, ldb, 64, 64) : tc::make_map_bf16(&tb2, B, N, K, ldb, 64, 128);
     if (!ok2a || !ok2b) return cudaErrorInvalidValue;
-    if (a_mn && b_mn) return launch_gemm_2sm<true, true>(ta2, tb2, p, num_sms, st);
-    if (a_mn) return launch_gemm_2sm<true, false>(ta2, tb2, p, num_sms, st);
-    if (b_mn) return launch_gemm_2sm<false, true>(ta2, tb2, p, num_sms, st);
-    return launch_gemm_2sm<false, false>(ta2, tb2, p, num_sms, st);
+    if (e2 && e2[0] == '2') {     // 256 x 512 pair tiles (opt-in, see G2<2>)
+      if (a_mn && b_mn) return launch_gemm_2sm<true, true, 2>(ta2, tb2, p, num_sms, st);
+      if (a_mn) return launch_gemm_2sm<true, false, 2>(ta2, tb2, p, num_sms, st);
+      if (b_mn) return launch_gemm_2sm<false, true, 2>(ta2, tb2, p, num_sms, st);
+      return launch_gemm_2sm<false, false, 2>(ta2, tb2, p, num_sms, st);
+    }
+    if (a_mn && b_mn) return launch_gemm_2sm<true, true, 1>(ta2, tb2, p, num_sms, st);
+    if (a_mn) return launch_gemm_2sm<true, false, 1>(ta2, tb2, p, num_sms, st);
+    if (b_mn) return launch_gemm_2sm<false, true, 1>(ta2, tb2, p, num_sms, st);
+    return launch_gemm_2sm<false, false, 1>(ta2, tb2, p, num_sms, st);
   }
   if (a_mn && b_mn) return launch_gemm_t<true, true>(ta, tb, p, num_sms, st);
   if (a_mn) return launch_gemm_t<true, false>(ta, tb, p, num_sms, st);
