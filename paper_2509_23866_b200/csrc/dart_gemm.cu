@@ -237,6 +237,10 @@ template <int NW> struct G2 {
   static constexpr uint32_t B_BYTES = B_HALF * NW;
   static constexpr uint32_t STAGE_BYTES = A_BYTES + B_BYTES;
   static constexpr size_t SMEM = 1024 + (size_t)STAGES * STAGE_BYTES + 256;
+  // epilogue warps: 4 per 256 accumulator columns (NW = 2: two groups drain
+  // the two halves of the single accumulator at the same time)
+  static constexpr int EPI_WARPS = 4 * NW;
+  static constexpr int THREADS = 64 + 32 * EPI_WARPS;
 };
 constexpr size_t G2_SMEM = G2<1>::SMEM;
 
@@ -265,7 +269,7 @@ __device__ __forceinline__ void g2_tile(const GemmParams& p, int64_t t, int& mt,
 }
 
 template <bool A_MN, bool B_MN, int NW>
-__global__ void __launch_bounds__(GM_THREADS, 1)
+__global__ void __launch_bounds__(G2<NW>::THREADS, 1)
     gemm_bf16_2sm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                          const GemmParams p) {
   using C2 = G2<NW>;
@@ -290,7 +294,7 @@ __global__ void __launch_bounds__(GM_THREADS, 1)
     }
     for (int a = 0; a < G2_ACC; ++a) {
       mbar_init(&tfull[a], 1);
-      mbar_init(&tempty[a], 8);            // 4 epilogue warps x 2 CTAs (leader's copy is the one used)
+      mbar_init(&tempty[a], 2 * C2::EPI_WARPS);   // epilogue warps x 2 CTAs (leader's copy is the one used)
     }
     fence_mbar_init();
     tc::tma_prefetch_desc(&tmA);
@@ -380,7 +384,8 @@ __global__ void __launch_bounds__(GM_THREADS, 1)
       }
     }
   } else {
-    const int q = warp & 3;
+    const int q = warp & 3;                     // TMEM lane quadrant this warp may access
+    const int half = (warp - 2) >> 2;           // column group: [256 half, 256 half + 256)
     const int r = q * 32 + lane;
     int acc = 0;
     uint32_t aph = 0;
@@ -390,12 +395,12 @@ __global__ void __launch_bounds__(GM_THREADS, 1)
       mbar_wait(&tfull[acc], aph);
       tc::fence_after();
       const int64_t m = (int64_t)mt * 256 + 128 * rank + r;
-      const uint32_t tbase = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * G2_BN);
+      const uint32_t tbase = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * G2_BN + 256 * half);
 #pragma unroll 1
-      for (int j = 0; j < G2_BN / 32; ++j) {
+      for (int j = 0; j < 256 / 32; ++j) {
         float x[32];
         tc::tmem_ld32(tbase + (uint32_t)(j * 32), x);
-        const int64_t n0 = (int64_t)nt * G2_BN + j * 32;
+        const int64_t n0 = (int64_t)nt * G2_BN + 256 * half + j * 32;
         if (m >= p.M || n0 >= p.N) continue;
         if (p.c_mode == DART_GEMM_STORE_BF16) {
           __nv_bfloat16* c = reinterpret_cast<__nv_bfloat16*>(p.C) + m * p.ldc + n0;
@@ -453,7 +458,7 @@ cudaError_t launch_gemm_2sm(const CUtensorMap& ta, const CUtensorMap& tb, GemmPa
   attr[0].val.clusterDim.x = 2;
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
-  cfg.blockDim = dim3(GM_THREADS);
+  cfg.blockDim = dim3(G2<NW>::THREADS);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
   cfg.attrs = attr;
