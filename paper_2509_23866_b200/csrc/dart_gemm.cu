@@ -221,6 +221,15 @@ __global__ void __launch_bounds__(GM_THREADS, 1)
 // pair leader issues tcgen05.mma.cta_group::2 (M = 256, N = 256) and each CTA
 // reads its 128 accumulator rows from its own TMEM.  Per SM this halves the
 // shared-memory / L2 operand traffic of the B panel.
+// DART_GEMM_CST = 1: the epilogue transposes each warp's 32 rows x 32 columns
+// through shared memory and writes whole 128-byte row segments (8 lanes per
+// row) instead of one 16-byte piece of 32 different rows per store -- the
+// thread-per-row stores touched every L2 sector twice (ncu: 2x the output
+// bytes crossed L1 -> L2) and, for the single-accumulator 256 x 512 tile,
+// kept the tensor pipe idle 40% of the time.
+#ifndef DART_GEMM_CST
+#define DART_GEMM_CST 1
+#endif
 // NW = 2 ("wide"): the pair computes a 256 x 512 tile -- each CTA stages 128
 // rows of A and 2 x 128 rows of B per stage, the leader issues two N = 256
 // MMAs per K step into the two halves of one 512-column accumulator -- so a
@@ -238,9 +247,14 @@ template <int NW> struct G2 {
   static constexpr uint32_t STAGE_BYTES = A_BYTES + B_BYTES;
   static constexpr size_t SMEM = 1024 + (size_t)STAGES * STAGE_BYTES + 256;
   // epilogue warps: 4 per 256 accumulator columns (NW = 2: two groups drain
-  // the two halves of the single accumulator at the same time)
-  static constexpr int EPI_WARPS = 4 * NW;
+  // the two halves of the single accumulator at the same time); with the
+  // coalesced epilogue (DART_GEMM_CST) 4 warps that stage each 32 x 32 block
+  // through shared memory (4.5 KB per warp)
+  static constexpr int EPI_WARPS = DART_GEMM_CST ? 4 : 4 * NW;
   static constexpr int THREADS = 64 + 32 * EPI_WARPS;
+  static constexpr uint32_t EPI_STRIDE = 36;                          // floats per staged row (16 B aligned)
+  static constexpr size_t EPI_BYTES = DART_GEMM_CST ? (size_t)EPI_WARPS * 32 * EPI_STRIDE * 4 : 0;
+  static constexpr size_t SMEM_ALL = SMEM + EPI_BYTES;
 };
 constexpr size_t G2_SMEM = G2<1>::SMEM;
 
@@ -385,8 +399,10 @@ __global__ void __launch_bounds__(G2<NW>::THREADS, 1)
     }
   } else {
     const int q = warp & 3;                     // TMEM lane quadrant this warp may access
-    const int half = (warp - 2) >> 2;           // column group: [256 half, 256 half + 256)
+    const int half = DART_GEMM_CST ? 0 : (warp - 2) >> 2;   // column group: [256 half, 256 half + 256)
+    constexpr int EPI_COLS = DART_GEMM_CST ? G2_BN : 256;   // columns this warp drains per tile
     const int r = q * 32 + lane;
+    float* T = reinterpret_cast<float*>(smem + G2_STAGES * G2_STAGE_BYTES + 256) + (warp - 2) * (32 * C2::EPI_STRIDE);
     int acc = 0;
     uint32_t aph = 0;
     for (int64_t t = cid; t < p.n_tiles; t += ncl) {
@@ -395,12 +411,46 @@ __global__ void __launch_bounds__(G2<NW>::THREADS, 1)
       mbar_wait(&tfull[acc], aph);
       tc::fence_after();
       const int64_t m = (int64_t)mt * 256 + 128 * rank + r;
+      const int64_t mrow0 = (int64_t)mt * 256 + 128 * rank + q * 32;   // this warp's first row
       const uint32_t tbase = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * G2_BN + 256 * half);
 #pragma unroll 1
-      for (int j = 0; j < 256 / 32; ++j) {
+      for (int j = 0; j < EPI_COLS / 32; ++j) {
         float x[32];
         tc::tmem_ld32(tbase + (uint32_t)(j * 32), x);
         const int64_t n0 = (int64_t)nt * G2_BN + 256 * half + j * 32;
+        if (DART_GEMM_CST) {
+          if (n0 >= p.N) continue;
+          // stage: lane = row
+#pragma unroll
+          for (int g = 0; g < 8; ++g)
+            *reinterpret_cast<float4*>(T + lane * C2::EPI_STRIDE + 4 * g) =
+                make_float4(x[4 * g], x[4 * g + 1], x[4 * g + 2], x[4 * g + 3]);
+          __syncwarp();
+          // write: 8 lanes per row (4 columns each), 4 rows per instruction
+          const int col = 4 * (lane & 7);
+          const int64_t n = n0 + col;
+#pragma unroll
+          for (int k = 0; k < 8; ++k) {
+            const int ri = 4 * k + (lane >> 3);
+            const int64_t mm = mrow0 + ri;
+            if (mm < p.M && n + 4 <= p.N) {
+              float4 v = *reinterpret_cast<const float4*>(T + ri * C2::EPI_STRIDE + col);
+              if (p.c_mode == DART_GEMM_STORE_BF16) {
+                *reinterpret_cast<uint2*>(reinterpret_cast<__nv_bfloat16*>(p.C) + mm * p.ldc + n) =
+                    make_uint2(pack_bf16x2(v.x, v.y), pack_bf16x2(v.z, v.w));
+              } else {
+                float* c = reinterpret_cast<float*>(p.C) + mm * p.ldc + n;
+                if (p.c_mode == DART_GEMM_ACCUM_F32) {
+                  const float4 o = *reinterpret_cast<const float4*>(c);
+                  v.x += o.x; v.y += o.y; v.z += o.z; v.w += o.w;
+                }
+                *reinterpret_cast<float4*>(c) = v;
+              }
+            }
+          }
+          __syncwarp();
+          continue;
+        }
         if (m >= p.M || n0 >= p.N) continue;
         if (p.c_mode == DART_GEMM_STORE_BF16) {
           __nv_bfloat16* c = reinterpret_cast<__nv_bfloat16*>(p.C) + m * p.ldc + n0;
@@ -446,7 +496,7 @@ template <bool A_MN, bool B_MN, int NW>
 cudaError_t launch_gemm_2sm(const CUtensorMap& ta, const CUtensorMap& tb, GemmParams p, int num_sms,
                             cudaStream_t st) {
   auto kern = gemm_bf16_2sm_kernel<A_MN, B_MN, NW>;
-  constexpr size_t smem = G2<NW>::SMEM;
+  constexpr size_t smem = G2<NW>::SMEM_ALL;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   p.n_mt = (p.M + 255) / 256;
