@@ -347,6 +347,32 @@ def run_dart(args):
         fwd_ms.append(e[0].elapsed_time(e[1]))
         bwd_ms.append(e[2].elapsed_time(e[3]))
 
+    # per-phase pass (SURVEY §8(d) timing protocol: K0-K2, C1, K3, K4+K5(+K6), C2),
+    # events on the launching stream between the public API's phase calls
+    phases = None
+    if not args.fused:
+        names = ["fwd (K0-K2)", "C1 all-gather", "select (K3)", "bwd (K6, K4/K5)", "C2 all-reduce"]
+        pev = [[torch.cuda.Event(enable_timing=True) for _ in range(6)] for _ in range(args.steps)]
+        acc = {n: [] for n in names}
+        for k in range(args.steps):
+            ev = pev[k]
+            ev[0].record(stream)
+            dl.forward(*inputs)
+            ev[1].record(stream)
+            dl.gather()
+            ev[2].record(stream)
+            dl.select()
+            ev[3].record(stream)
+            dl.backward()
+            ev[4].record(stream)
+            dl.reduce_stats()
+            ev[5].record(stream)
+        torch.cuda.synchronize()
+        for k in range(args.steps):
+            for i, n in enumerate(names):
+                acc[n].append(pev[k][i].elapsed_time(pev[k][i + 1]))
+        phases = {n: round(statistics.median(v), 4) for n, v in acc.items()}
+
     # context, not the roofline denominator: a plain device copy (torch
     # copy_, the kernel MEASURED_PEAKS.json's hbm_gbs is taken with) timed the
     # same way as the step -- back to back, as long as the timed loop, under
@@ -459,7 +485,8 @@ def run_dart(args):
                         "bwd_sweep": {"avg_ms": bwd_avg, "GBps": bwd_gbs, "frac": bwd_gbs / peak,
                                       "bytes": bwd_bytes},
                         "step_GBps": step_bytes / (ms * 1e-3) / 1e9,
-                        "step_frac": step_bytes / (ms * 1e-3) / 1e9 / peak},
+                        "step_frac": step_bytes / (ms * 1e-3) / 1e9 / peak,
+                        "phases_median_ms": phases},
             "gpu_launches": launches,
             "clocks": clocks,
             "e2e": e2e,
