@@ -256,7 +256,6 @@ template <int NW> struct G2 {
   static constexpr size_t EPI_BYTES = DART_GEMM_CST ? (size_t)EPI_WARPS * 32 * EPI_STRIDE * 4 : 0;
   static constexpr size_t SMEM_ALL = SMEM + EPI_BYTES;
 };
-constexpr size_t G2_SMEM = G2<1>::SMEM;
 
 __device__ __forceinline__ uint32_t g2_rank() {
   uint32_t r;

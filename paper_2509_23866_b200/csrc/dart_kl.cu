@@ -406,7 +406,6 @@ bwd_kl_kernel(const BwdParams p) {
   const int64_t J1 = kl_ordinal_at_cost(p, (total * ((int64_t)blockIdx.x + 1)) / nb);
   const int tail_elems = (int)(p.V % EPV);
   const float c2 = p.c2;
-  const float invT = p.invT_f;
   const uint64_t pol = policy_evict_first();
   const float4* rec = reinterpret_cast<const float4*>(p.rec);
   const int64_t nvec = p.nvec;
