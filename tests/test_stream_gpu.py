@@ -44,7 +44,7 @@ def test_streamed_equals_resident(max_rows, pool):
     assert sp.stats_dict()["n_kept_tok"] == ref.stats_dict()["n_kept_tok"]
 
 
-def _mr_worker(rank, world, port, max_rows, q):
+def _mr_worker(rank, world, port, max_rows, q, name="mid", seed=4):
     import os
     import torch.distributed as dist
     from paper_2509_23866_b200 import dist as D
@@ -53,13 +53,15 @@ def _mr_worker(rank, world, port, max_rows, q):
     try:
         torch.cuda.set_device(0)
         dev = torch.device("cuda", 0)
-        b = synth.make_batch("mid", seed=4)
+        b = synth.make_batch(name, seed=seed)
         shards = D.shard_layout(b.layout, world)
         me = shards[rank]
-        sp = StreamedPass(b.layout, b.V, dart.Config(), dev, max_rows=max_rows, pool=2, group=dist.group.WORLD,
-                          world_shards=shards)
+        gd = torch.float32 if b.logits.dtype == torch.float32 else torch.bfloat16
+        cfg = dart.Config(is_cap=2.0) if name == "tiny" else dart.Config()
+        sp = StreamedPass(b.layout, b.V, cfg, dev, max_rows=max_rows, pool=2, group=dist.group.WORLD,
+                          world_shards=shards, logits_dtype=b.logits.dtype, grad_dtype=gd)
         logits = b.logits.to(dev)
-        got = torch.empty((me.T_loc, b.V), dtype=torch.bfloat16, device=dev)
+        got = torch.empty((me.T_loc, b.V), dtype=gd, device=dev)
 
         def fill(i, buf):
             c = sp.chunks[i]
@@ -74,7 +76,8 @@ def _mr_worker(rank, world, port, max_rows, q):
                fill=fill, consume=consume)
         torch.cuda.synchronize()
         sp.check_status()
-        q.put((rank, got.view(torch.int16).cpu().numpy(), sp.keep.cpu().numpy(), sp.norm.cpu().numpy(),
+        q.put((rank, got.view(torch.int16 if gd == torch.bfloat16 else torch.int32).cpu().numpy(),
+               sp.keep.cpu().numpy(), sp.norm.cpu().numpy(),
                sp.stats_dict(), me.tok_begin, me.tok_end, len(sp.chunks)))
     except Exception as e:  # pragma: no cover
         q.put((rank, repr(e), None, None, None, 0, 0, 0))
@@ -113,3 +116,36 @@ def test_streamed_two_ranks_equal_resident(max_rows):
         assert np.array_equal(dz, ref_dz[t0:t1])
         assert abs(st["loss"] - L) <= 1e-12 * abs(L) + 1e-15       # all-reduced on every rank
         assert st["n_kept_tok"] == ref.stats_dict()["n_kept_tok"]
+
+
+def test_streamed_more_ranks_than_trajectories():
+    """5 ranks for the tiny config's 4 trajectories: one rank owns nothing
+    (one empty chunk; its forward call still builds the global group tables);
+    every rank's gradient rows bitwise equal to the resident pass."""
+    import socket
+    import torch.multiprocessing as mp
+    from paper_2509_23866_b200 import dist as D
+    b = synth.make_batch("tiny", seed=1)
+    ref = run_gpu(b, dart.Config(is_cap=2.0))
+    assert any(s.T_loc == 0 for s in D.shard_layout(b.layout, 5))
+    ref_dz = ref.dlogits.view(torch.int32).cpu().numpy()
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    ps = [ctx.Process(target=_mr_worker, args=(r, 5, port, 40, q, "tiny", 1)) for r in range(5)]
+    for p in ps:
+        p.start()
+    res = [q.get(timeout=600) for _ in ps]
+    for p in ps:
+        p.join(timeout=60)
+    L = ref.stats_dict()["loss"]
+    for rank, dz, keep, norm, st, t0, t1, nch in res:
+        assert keep is not None, dz
+        assert np.array_equal(keep[:b.layout.S], ref.keep.cpu().numpy()[:b.layout.S])
+        assert np.array_equal(norm, ref.norm.cpu().numpy())
+        assert np.array_equal(dz, ref_dz[t0:t1])
+        assert abs(st["loss"] - L) <= 1e-12 * abs(L) + 1e-15
+

@@ -27,7 +27,8 @@ def _unpack(gathered, rso, S_pad, S):
 
 @pytest.mark.parametrize("name,world,max_rows", [("small_multi", 2, 40), ("small_multi", 3, 15),
                                                  ("adaptive", 8, 32768), ("adaptive", 3, 2000),
-                                                 ("single", 2, 4096), ("tiny", 4, 64)])
+                                                 ("single", 2, 4096), ("tiny", 4, 64),
+                                                 ("tiny", 6, 64)])
 def test_virtual_rank_table(name, world, max_rows):
     L, _, _, _ = synth.config_layout(name, seed=1)
     shards = D.shard_layout(L, world)
