@@ -347,6 +347,23 @@ def run_dart(args):
         fwd_ms.append(e[0].elapsed_time(e[1]))
         bwd_ms.append(e[2].elapsed_time(e[3]))
 
+    # the same pass replayed from a CUDA graph (one host launch per step): context
+    graph = None
+    if args.graph and world == 1 and not args.fused:
+        g = dl.capture(*inputs)
+        for _ in range(args.warmup):
+            g.replay()
+        torch.cuda.synchronize()
+        g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        g0.record(stream)
+        for _ in range(args.steps):
+            g.replay()
+        g1.record(stream)
+        torch.cuda.synchronize()
+        gms = g0.elapsed_time(g1) / args.steps
+        graph = {"ms_per_step": gms, "value": layout_r.T / (gms * 1e-3), "what": "DartLoss.capture() replayed"}
+        del g
+
     # per-phase pass (SURVEY §8(d) timing protocol: K0-K2, C1, K3, K4+K5(+K6), C2),
     # events on the launching stream between the public API's phase calls
     phases = None
@@ -495,6 +512,8 @@ def run_dart(args):
         if copy_ref is not None:
             copy_ref["step_frac_vs_copy"] = line["kernels"]["step_GBps"] / copy_ref["GBps"]
             line["copy_sustained"] = copy_ref
+        if graph is not None:
+            line["cuda_graph"] = graph
         print(json.dumps(line), flush=True)
     if world > 1:
         import torch.distributed as dist
@@ -1092,6 +1111,7 @@ def main():
     ap.add_argument("--fused", action="store_true",
                     help="time the single-read fused update with the mask known in advance (NEXT #1)")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--graph", action="store_true", help="also time the pass replayed from a CUDA graph")
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-tokens", type=int, default=1024, help="oracle sample tokens per worker process")

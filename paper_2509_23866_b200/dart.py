@@ -472,6 +472,20 @@ class DartLoss:
         from . import dist as D
         D.all_reduce(self.stats, group=self.group)
 
+    def capture(self, logits, target, logp_old, logp_roll, logp_ref=None, ref_logits=None):
+        """Capture one whole pass over these (device-resident) inputs into a
+        CUDA graph; `graph.replay()` then re-runs it with a single launch from
+        the host (the buffers it reads and writes are fixed at capture).
+        Single-process passes only (the N > 1 collectives stay eager)."""
+        if self.world > 1:
+            raise DartError("capture() is for single-process passes")
+        self.run(logits, target, logp_old, logp_roll, logp_ref, ref_logits)     # warm-up (attributes, tables)
+        torch.cuda.synchronize(self.device)
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            self.run(logits, target, logp_old, logp_roll, logp_ref, ref_logits)
+        return g
+
     def run(self, logits, target, logp_old, logp_roll, logp_ref=None, ref_logits=None):
         """One whole pass (fwd -> C1 -> select -> bwd -> C2), stream-ordered."""
         self.forward(logits, target, logp_old, logp_roll, logp_ref, ref_logits)
