@@ -47,7 +47,7 @@ def hbm_peak():
 class ClockSampler:
     FIELDS = "clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown," \
              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown," \
-             "clocks_event_reasons.sw_power_cap,power.draw"
+             "clocks_event_reasons.sw_power_cap,power.draw,clocks.mem"
 
     def __init__(self, index):
         self.index = index
@@ -86,14 +86,19 @@ class ClockSampler:
         mx = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         reasons = sorted({names[i] for r in rows for i in range(4) if r[3 + i].lower() == "active"})
-        pw = []
+        pw, mem = [], []
         for r in rows:
             try:
                 pw.append(float(r[7]))
-            except ValueError:
+            except (ValueError, IndexError):
+                pass
+            try:
+                mem.append(float(r[8]))
+            except (ValueError, IndexError):
                 pass
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(rows), "power_w": statistics.median(pw) if pw else None}
+                "reasons": reasons, "samples": len(rows), "power_w": statistics.median(pw) if pw else None,
+                "mem_mhz": statistics.median(mem) if mem else None}
 
 
 # ------------------------------------------------------------------ setup
@@ -497,12 +502,14 @@ def run_dart(args):
                          "peak_source": peak_src, "unit": "GB/s", "frac": dom[1] / peak,
                          "traffic": traffic, "algorithmic_bytes_per_launch": dom[2],
                          "avg_launch_ms": dom[3]},
-            "kernels": {"fwd_sweep": {"avg_ms": fwd_avg, "GBps": fwd_gbs, "frac": fwd_gbs / peak,
-                                      "bytes": fwd_bytes},
-                        "bwd_sweep": {"avg_ms": bwd_avg, "GBps": bwd_gbs, "frac": bwd_gbs / peak,
-                                      "bytes": bwd_bytes},
+            "kernels": {"fwd_sweep": {"avg_ms": fwd_avg, "median_ms": statistics.median(fwd_ms) if not args.fused else None,
+                                      "best_ms": min(fwd_ms) if not args.fused else None,
+                                      "GBps": fwd_gbs, "frac": fwd_gbs / peak, "bytes": fwd_bytes},
+                        "bwd_sweep": {"avg_ms": bwd_avg, "median_ms": statistics.median(bwd_ms), "best_ms": min(bwd_ms),
+                                      "GBps": bwd_gbs, "frac": bwd_gbs / peak, "bytes": bwd_bytes},
                         "step_GBps": step_bytes / (ms * 1e-3) / 1e9,
                         "step_frac": step_bytes / (ms * 1e-3) / 1e9 / peak,
+                        "step_frac_of_8TBps_spec": step_bytes / (ms * 1e-3) / 1e9 / 8000.0,
                         "phases_median_ms": phases},
             "gpu_launches": launches,
             "clocks": clocks,
