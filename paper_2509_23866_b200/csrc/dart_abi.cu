@@ -513,7 +513,7 @@ dart_status dart_loss_bwd(const dart_batch* b, const dart_meta* m, const dart_cf
   const size_t es = esize(b->logits_dtype);
   const int64_t nvec = (int64_t)((b->V * es + 15) / 16);
   const bool kx = exact_kl(c);
-  const int64_t chv = kx ? CH_VEC / 2 : CH_VEC;            // exact KL: 2 KB of z + 2 KB of z_ref per slot
+  const int64_t chv = kx ? CH_VEC / 2 : BCH_VEC;           // exact KL: 2 KB of z + 2 KB of z_ref per slot
   const int64_t nch = (nvec + chv - 1) / chv;
 
   BwdPrepParams pp;

@@ -169,6 +169,7 @@ __global__ void rowrec_kernel(RowRecParams p) {
 // w, w+WARPS, ...).  Every SM thus streams ONE contiguous read region and ONE
 // write region at a time -- far fewer concurrent DRAM streams than a
 // warp-per-range split -- while still running WARPS independent rings.
+constexpr int BVPL = BCH_VEC / 32;   // 16-byte vectors per lane per bwd chunk
 struct OCur {
   int64_t j, jend;  // chunk ordinal (in the local chunk sequence) and the warp's end
   int64_t s;        // local step
@@ -297,11 +298,11 @@ __device__ __forceinline__ void store_full(uint8_t* dst, const float* o) {
 template <typename Tin, int WARPS, int STAGES>
 __device__ __forceinline__ void bwd_issue(OCur& pc, const BwdParams& p, uint64_t* bars, uint8_t* ring, int slot,
                                           int lane, uint64_t pol) {
-  const int64_t v0 = (int64_t)pc.c * CH_VEC;
-  const int64_t nv = min((int64_t)CH_VEC, p.nvec - v0);
+  const int64_t v0 = (int64_t)pc.c * BCH_VEC;
+  const int64_t nv = min((int64_t)BCH_VEC, p.nvec - v0);
   if (lane == 0) {
     mbar_arrive_expect_tx(&bars[slot], (uint32_t)nv * 16u);
-    bulk_g2s_hint(ring + (size_t)slot * CH_BYTES, p.logits + pc.t * p.ld_bytes + v0 * 16, (uint32_t)nv * 16u,
+    bulk_g2s_hint(ring + (size_t)slot * BCH_BYTES, p.logits + pc.t * p.ld_bytes + v0 * 16, (uint32_t)nv * 16u,
                   &bars[slot], pol);
   }
   ocur_advance(pc, p, WARPS);
@@ -367,15 +368,15 @@ bwd_sweep_kernel(const BwdParams p) {
   constexpr int EPV = 16 / sizeof(Tin);       // logits per 16-byte input vector
   constexpr bool OUT_BF16 = sizeof(Tout) == 2;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  uint8_t* ring = smem + (size_t)warp * STAGES * CH_BYTES;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + (size_t)WARPS * STAGES * CH_BYTES) + warp * STAGES;
+  uint8_t* ring = smem + (size_t)warp * STAGES * BCH_BYTES;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + (size_t)WARPS * STAGES * BCH_BYTES) + warp * STAGES;
   constexpr bool TMAST = DART_BWD_TMAST && sizeof(Tin) == 2 && sizeof(Tout) == 2;
   constexpr bool V8T = DART_BWD_V8 && !DART_BWD_TMAST && sizeof(Tin) == 2 && sizeof(Tout) == 2;
   const bool v8_ok = V8T && ((p.ldg_bytes & 31) == 0) && ((reinterpret_cast<uintptr_t>(p.dlogits) & 31) == 0);
-  // TMA-store staging: [WARPS][2][CH_BYTES] then one zero page (after the barriers, 1 KB aligned)
-  uint8_t* stage_base = smem + (((size_t)WARPS * STAGES * CH_BYTES + (size_t)WARPS * STAGES * 8 + 1023) & ~(size_t)1023);
-  uint8_t* stg_buf = stage_base + (size_t)warp * 2 * CH_BYTES;
-  uint8_t* zero_page = stage_base + (size_t)WARPS * 2 * CH_BYTES;
+  // TMA-store staging: [WARPS][2][BCH_BYTES] then one zero page (after the barriers, 1 KB aligned)
+  uint8_t* stage_base = smem + (((size_t)WARPS * STAGES * BCH_BYTES + (size_t)WARPS * STAGES * 8 + 1023) & ~(size_t)1023);
+  uint8_t* stg_buf = stage_base + (size_t)warp * 2 * BCH_BYTES;
+  uint8_t* zero_page = stage_base + (size_t)WARPS * 2 * BCH_BYTES;
   int sbuf = 0;
   if (lane == 0) {
 #pragma unroll
@@ -383,7 +384,7 @@ bwd_sweep_kernel(const BwdParams p) {
     fence_mbar_init();
   }
   if (TMAST) {
-    for (int i = threadIdx.x; i < CH_BYTES / 16; i += blockDim.x) sts128(zero_page + i * 16, make_uint4(0u, 0u, 0u, 0u));
+    for (int i = threadIdx.x; i < BCH_BYTES / 16; i += blockDim.x) sts128(zero_page + i * 16, make_uint4(0u, 0u, 0u, 0u));
     fence_proxy_async_smem();
     __syncthreads();
   }
@@ -421,11 +422,11 @@ bwd_sweep_kernel(const BwdParams p) {
 #pragma unroll 1
   while (cc.valid) {
     const int64_t t = cc.t;
-    const int64_t v0 = (int64_t)cc.c * CH_VEC;
-    const int nv = (int)min((int64_t)CH_VEC, nvec - v0);
-    // full chunk: all lanes hold VPL complete vectors (no tail, no predicates)
-    const bool full8 = v8_ok && (nv == CH_VEC) && !(tail_elems && v0 + nv == nvec);
-    const bool full = !full8 && DART_BWD_FULL && (nv == CH_VEC) && !(tail_elems && v0 + nv == nvec);
+    const int64_t v0 = (int64_t)cc.c * BCH_VEC;
+    const int nv = (int)min((int64_t)BCH_VEC, nvec - v0);
+    // full chunk: all lanes hold BVPL complete vectors (no tail, no predicates)
+    const bool full8 = v8_ok && (nv == BCH_VEC) && !(tail_elems && v0 + nv == nvec);
+    const bool full = !full8 && DART_BWD_FULL && (nv == BCH_VEC) && !(tail_elems && v0 + nv == nvec);
     uint8_t* orow = dlog + t * ldg_bytes;
     uint8_t* olane = orow + (v0 + lane) * OUTV;    // this lane's first output vector
     if (cc.kept) {
@@ -440,21 +441,21 @@ bwd_sweep_kernel(const BwdParams p) {
       const float g = __int_as_float(cur.x), nl2 = __int_as_float(cur.y), zy = __int_as_float(cur.w);
       const int32_t y = cur.z;
       mbar_wait(&bars[slot], phase);
-      const uint8_t* sp = ring + (size_t)slot * CH_BYTES;
+      const uint8_t* sp = ring + (size_t)slot * BCH_BYTES;
       const float2 cc2 = make_float2(c2, c2), nl = make_float2(nl2, nl2), ng = make_float2(-g, -g);
-      uint4 x[VPL];
+      uint4 x[BVPL];
       if (V8T && full8) {       // lane owns vector pairs (lane + 32 k): 32 contiguous bytes each
 #pragma unroll
-        for (int k = 0; k < VPL / 2; ++k) {
+        for (int k = 0; k < BVPL / 2; ++k) {
           x[2 * k] = lds128(sp + (lane + 32 * k) * 32);
           x[2 * k + 1] = lds128(sp + (lane + 32 * k) * 32 + 16);
         }
       } else if (full) {
 #pragma unroll
-        for (int k = 0; k < VPL; ++k) x[k] = lds128(sp + (lane + 32 * k) * 16);
+        for (int k = 0; k < BVPL; ++k) x[k] = lds128(sp + (lane + 32 * k) * 16);
       } else {
 #pragma unroll
-        for (int k = 0; k < VPL; ++k) {
+        for (int k = 0; k < BVPL; ++k) {
           const int vi = lane + 32 * k;
           x[k] = (vi < nv) ? lds128(sp + vi * 16) : make_uint4(0u, 0u, 0u, 0u);
         }
@@ -463,14 +464,14 @@ bwd_sweep_kernel(const BwdParams p) {
       // engine (read-then-async-write: the reads have completed)
       uint32_t dep = 0;
 #pragma unroll
-      for (int k = 0; k < VPL; ++k) dep |= x[k].x | x[k].y | x[k].z | x[k].w;
+      for (int k = 0; k < BVPL; ++k) dep |= x[k].x | x[k].y | x[k].z | x[k].w;
       asm volatile("" ::"r"(dep));
       __syncwarp();
       if (pc.valid) bwd_issue<Tin, WARPS, STAGES>(pc, p, bars, ring, slot, lane, pol);
       if (++slot == STAGES) { slot = 0; phase ^= 1u; }
       if (V8T && full8) {
 #pragma unroll
-        for (int k = 0; k < VPL / 2; ++k) {
+        for (int k = 0; k < BVPL / 2; ++k) {
           float o[16];
 #if DART_BWD_V8 == 2
           // always true on a full chunk, but opaque to the compiler: one branch
@@ -487,7 +488,7 @@ bwd_sweep_kernel(const BwdParams p) {
         }
         if (y >= 0) {           // target element g (1 - p_y), after its pair's store (same thread)
           const int64_t yv = y / EPV;
-          if (yv >= v0 && yv < v0 + CH_VEC && lane == (int)(((yv - v0) >> 1) & 31)) {
+          if (yv >= v0 && yv < v0 + BCH_VEC && lane == (int)(((yv - v0) >> 1) & 31)) {
             const float py = ex2(fmaf(zy, c2, nl2));
             reinterpret_cast<__nv_bfloat16*>(orow)[y] = __float2bfloat16_rn(fmaf(-g, py, g));
           }
@@ -495,13 +496,13 @@ bwd_sweep_kernel(const BwdParams p) {
         ocur_advance(cc, p, WARPS);
         continue;
       }
-      if (TMAST && nv == CH_VEC && !(tail_elems && v0 + nv == nvec)) {
+      if (TMAST && nv == BCH_VEC && !(tail_elems && v0 + nv == nvec)) {
         // gradient of the chunk into this warp's staging buffer, then one bulk store
         if (lane == 0) bulk_wait_read<1>();         // the buffer's previous bulk store has read it
         __syncwarp();
-        uint8_t* sb = stg_buf + (size_t)sbuf * CH_BYTES;
+        uint8_t* sb = stg_buf + (size_t)sbuf * BCH_BYTES;
 #pragma unroll
-        for (int k = 0; k < VPL; ++k) {
+        for (int k = 0; k < BVPL; ++k) {
           float o[EPV];
           grad_vec<Tin>(x[k], cc2, nl, ng, o);
           sts128(sb + (lane + 32 * k) * 16, make_uint4(pack_bf16x2(o[0], o[1]), pack_bf16x2(o[2], o[3]),
@@ -517,7 +518,7 @@ bwd_sweep_kernel(const BwdParams p) {
         fence_proxy_async_smem();                   // generic-proxy smem writes -> visible to the bulk copy
         __syncwarp();
         if (lane == 0) {
-          bulk_s2g(orow + v0 * OUTV, sb, (uint32_t)CH_BYTES);
+          bulk_s2g(orow + v0 * OUTV, sb, (uint32_t)BCH_BYTES);
           bulk_commit();
         }
         sbuf ^= 1;
@@ -526,7 +527,7 @@ bwd_sweep_kernel(const BwdParams p) {
       }
       if (full) {
 #pragma unroll
-        for (int k = 0; k < VPL; ++k) {
+        for (int k = 0; k < BVPL; ++k) {
 #if DART_BWD_FULL == 2
           if ((nv >> 5) <= k) break;   // always true here; one branch region per vector (spreads the stores)
 #endif
@@ -547,7 +548,7 @@ bwd_sweep_kernel(const BwdParams p) {
         }
       } else {
 #pragma unroll
-        for (int k = 0; k < VPL; ++k) {
+        for (int k = 0; k < BVPL; ++k) {
           const int vi = lane + 32 * k;
           if (vi < nv) {
             const int64_t gv = v0 + vi;
@@ -575,13 +576,13 @@ bwd_sweep_kernel(const BwdParams p) {
       if (V8T && full8) {
         const uint4 zz = make_uint4(0u, 0u, 0u, 0u);
 #pragma unroll
-        for (int k = 0; k < VPL / 2; ++k) stg256_cs(orow + (v0 + 2 * (lane + 32 * k)) * 16, zz, zz);
+        for (int k = 0; k < BVPL / 2; ++k) stg256_cs(orow + (v0 + 2 * (lane + 32 * k)) * 16, zz, zz);
         ocur_advance(cc, p, WARPS);
         continue;
       }
-      if (TMAST && nv == CH_VEC && !(tail_elems && v0 + nv == nvec)) {
+      if (TMAST && nv == BCH_VEC && !(tail_elems && v0 + nv == nvec)) {
         if (lane == 0) {
-          bulk_s2g(orow + v0 * OUTV, zero_page, (uint32_t)CH_BYTES);
+          bulk_s2g(orow + v0 * OUTV, zero_page, (uint32_t)BCH_BYTES);
           bulk_commit();
         }
         ocur_advance(cc, p, WARPS);
@@ -592,10 +593,10 @@ bwd_sweep_kernel(const BwdParams p) {
       for (int e = 0; e < EPV; ++e) o[e] = 0.f;
       if (full) {
 #pragma unroll
-        for (int k = 0; k < VPL; ++k) store_full<Tout, EPV>(olane + k * 32 * OUTV, o);
+        for (int k = 0; k < BVPL; ++k) store_full<Tout, EPV>(olane + k * 32 * OUTV, o);
       } else {
 #pragma unroll
-        for (int k = 0; k < VPL; ++k) {
+        for (int k = 0; k < BVPL; ++k) {
           const int vi = lane + 32 * k;
           if (vi < nv) {
             const int64_t gv = v0 + vi;
@@ -630,8 +631,8 @@ cudaError_t launch_rowrec(const RowRecParams& p, cudaStream_t st) {
 template <typename Tin, typename Tout, int WARPS, int STAGES>
 static cudaError_t launch_bwd_t(const BwdParams& p, int num_sms, cudaStream_t st) {
   constexpr bool TMAST = DART_BWD_TMAST && sizeof(Tin) == 2 && sizeof(Tout) == 2;
-  size_t smem = (size_t)WARPS * STAGES * CH_BYTES + (size_t)WARPS * STAGES * 8;
-  if (TMAST) smem = ((smem + 1023) & ~(size_t)1023) + (size_t)WARPS * 2 * CH_BYTES + CH_BYTES + 1024;
+  size_t smem = (size_t)WARPS * STAGES * BCH_BYTES + (size_t)WARPS * STAGES * 8;
+  if (TMAST) smem = ((smem + 1023) & ~(size_t)1023) + (size_t)WARPS * 2 * BCH_BYTES + BCH_BYTES + 1024;
   auto kern = bwd_sweep_kernel<Tin, Tout, WARPS, STAGES>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;

@@ -23,6 +23,12 @@ constexpr int FWD_WARPS = DART_FWD_WARPS;
 constexpr int FWD_STAGES = DART_FWD_STAGES;
 constexpr int BWD_WARPS = DART_BWD_WARPS;
 constexpr int BWD_STAGES = DART_BWD_STAGES;
+// bwd sweep bulk-copy chunk (bytes); the fwd / fused / KL sweeps use CH_BYTES
+#ifndef DART_BWD_CHB
+#define DART_BWD_CHB 4096
+#endif
+constexpr int BCH_BYTES = DART_BWD_CHB;
+constexpr int BCH_VEC = BCH_BYTES / 16;
 
 struct AdvParams {
   int64_t G, N_traj, S, T;
