@@ -182,7 +182,7 @@ int fused_variant() {
 }
 
 int choose_lg_nsplit(const dart_batch* b, const WsLayout& L, int64_t nvec) {
-  if (!L.split_alloc || nvec < (int64_t)KSEG * CH_VEC) return 0;
+  if (!L.split_alloc || nvec < (int64_t)KSEG * FCH_VEC) return 0;
   const int64_t target_units = 4LL * sm_count() * 16;
   int lg = 0;
   while ((1 << lg) < KSEG && (b->T_loc << lg) < target_units) ++lg;

@@ -118,13 +118,14 @@ __global__ void tok_meta_kernel(TokMetaParams p) {
 
 // ============================================================== K1 helpers
 // Canonical row decomposition: KSEG segments whose boundaries are multiples of
-// the chunk (CH_VEC vectors) -- only the row's last chunk can be partial.  The
+// the chunk (FCH_VEC vectors) -- only the row's last chunk can be partial.  The
 // per-row reduction order (lane <- vector mod 32, chunk-wise max update,
 // segment partials folded left to right) depends only on nvec, never on how
 // rows or segments are distributed over warps.
+constexpr int FVPL = FCH_VEC / 32;   // 16-byte vectors per lane per fwd chunk
 __device__ __forceinline__ int64_t seg_begin(int64_t nvec, int k) {
   if (k >= KSEG) return nvec;
-  return ((nvec * k) / KSEG) & ~(int64_t)(CH_VEC - 1);
+  return ((nvec * k) / KSEG) & ~(int64_t)(FCH_VEC - 1);
 }
 
 // Work stream of one warp: units u = wid, wid+W, ...; unit = (row, part);
@@ -213,16 +214,16 @@ __device__ __forceinline__ void acc_pair(LaneAcc& a, int j, float2 z, float2 cc,
 // ------------------------------------------------------------ chunk bodies
 // bf16: one 16-byte vector = 8 logits = 4 bf16x2 words
 template <bool FULL>
-__device__ __forceinline__ void chunk_bf16(uint4 (&x)[VPL], int nv, int lane, float c2, LaneAcc& a,
+__device__ __forceinline__ void chunk_bf16(uint4 (&x)[FVPL], int nv, int lane, float c2, LaneAcc& a,
                                            uint32_t& bad, int tail_idx, uint32_t tail_keep_mask) {
   if (!FULL) {
 #pragma unroll
-    for (int k = 0; k < VPL; ++k)
+    for (int k = 0; k < FVPL; ++k)
       if (lane + 32 * k >= nv) x[k] = make_uint4(0xff80ff80u, 0xff80ff80u, 0xff80ff80u, 0xff80ff80u);
   }
   if (tail_idx >= 0) {  // last vector of the row: logits >= V are not part of the row
 #pragma unroll
-    for (int k = 0; k < VPL; ++k) {
+    for (int k = 0; k < FVPL; ++k) {
       if (lane + 32 * k == tail_idx) {
         uint32_t* w = reinterpret_cast<uint32_t*>(&x[k]);
 #pragma unroll
@@ -235,7 +236,7 @@ __device__ __forceinline__ void chunk_bf16(uint4 (&x)[VPL], int nv, int lane, fl
   }
   uint32_t mx = 0xff80ff80u;
 #pragma unroll
-  for (int k = 0; k < VPL; ++k) {
+  for (int k = 0; k < FVPL; ++k) {
     mx = bmax2_nan(mx, x[k].x);
     mx = bmax2_nan(mx, x[k].y);
     mx = bmax2_nan(mx, x[k].z);
@@ -248,7 +249,7 @@ __device__ __forceinline__ void chunk_bf16(uint4 (&x)[VPL], int nv, int lane, fl
   if (__any_sync(0xffffffffu, cm > a.m + LAZY_M)) acc_rescale(a, (cm > a.m + LAZY_M) ? cm : a.m);
   const float2 cc = make_float2(c2, c2), nm = make_float2(-a.m, -a.m);
 #pragma unroll
-  for (int k = 0; k < VPL; ++k) {
+  for (int k = 0; k < FVPL; ++k) {
     if (FULL || lane + 32 * k < nv) {
       acc_pair(a, 0, make_float2(bf16lo(x[k].x), bf16hi(x[k].x)), cc, nm);
       acc_pair(a, 1, make_float2(bf16lo(x[k].y), bf16hi(x[k].y)), cc, nm);
@@ -260,11 +261,11 @@ __device__ __forceinline__ void chunk_bf16(uint4 (&x)[VPL], int nv, int lane, fl
 
 // f32: one vector = 4 logits
 template <bool FULL>
-__device__ __forceinline__ void chunk_f32(const uint4 (&xr)[VPL], int nv, int lane, float c2, LaneAcc& a,
+__device__ __forceinline__ void chunk_f32(const uint4 (&xr)[FVPL], int nv, int lane, float c2, LaneAcc& a,
                                           uint32_t& bad, int tail_idx, uint32_t tail_keep_mask) {
-  float4 x[VPL];
+  float4 x[FVPL];
 #pragma unroll
-  for (int k = 0; k < VPL; ++k) {
+  for (int k = 0; k < FVPL; ++k) {
     const int vi = lane + 32 * k;
     if (FULL || vi < nv) {
       x[k] = make_float4(__uint_as_float(xr[k].x), __uint_as_float(xr[k].y), __uint_as_float(xr[k].z),
@@ -275,7 +276,7 @@ __device__ __forceinline__ void chunk_f32(const uint4 (&xr)[VPL], int nv, int la
   }
   if (tail_idx >= 0) {
 #pragma unroll
-    for (int k = 0; k < VPL; ++k) {
+    for (int k = 0; k < FVPL; ++k) {
       if (lane + 32 * k == tail_idx) {
         if (!((tail_keep_mask >> 0) & 1u)) x[k].x = NEG_CLAMP;
         if (!((tail_keep_mask >> 1) & 1u)) x[k].y = NEG_CLAMP;
@@ -286,7 +287,7 @@ __device__ __forceinline__ void chunk_f32(const uint4 (&xr)[VPL], int nv, int la
   }
   float cmr = -INFINITY;
 #pragma unroll
-  for (int k = 0; k < VPL; ++k) {
+  for (int k = 0; k < FVPL; ++k) {
     cmr = fmax_nan(cmr, x[k].x);
     cmr = fmax_nan(cmr, x[k].y);
     cmr = fmax_nan(cmr, x[k].z);
@@ -298,7 +299,7 @@ __device__ __forceinline__ void chunk_f32(const uint4 (&xr)[VPL], int nv, int la
   if (__any_sync(0xffffffffu, cm > a.m + LAZY_M)) acc_rescale(a, (cm > a.m + LAZY_M) ? cm : a.m);
   const float2 cc = make_float2(c2, c2), nm = make_float2(-a.m, -a.m);
 #pragma unroll
-  for (int k = 0; k < VPL; ++k) {
+  for (int k = 0; k < FVPL; ++k) {
     if (FULL || lane + 32 * k < nv) {
       acc_pair(a, 0, make_float2(x[k].x, x[k].y), cc, nm);
       acc_pair(a, 1, make_float2(x[k].z, x[k].w), cc, nm);
@@ -406,10 +407,10 @@ __device__ __forceinline__ void row_epilogue(const FwdParams& p, int64_t row, Pa
 // Issue the bulk copy of the producer stream's next chunk into `slot` and advance it.
 __device__ __forceinline__ void issue_next(Stream& ps, uint64_t* bars, uint8_t* ring, int slot, const FwdParams& p,
                                            int64_t W, int64_t units, int lg, int64_t nvec, int lane, uint64_t pol) {
-  const int nv = min(CH_VEC, ps.vend - ps.v);
+  const int nv = min(FCH_VEC, ps.vend - ps.v);
   if (lane == 0) {
     mbar_arrive_expect_tx(&bars[slot], (uint32_t)nv * 16u);
-    bulk_g2s_hint(ring + (size_t)slot * CH_BYTES, p.logits + ps.row * p.ld_bytes + (int64_t)ps.v * 16,
+    bulk_g2s_hint(ring + (size_t)slot * FCH_BYTES, p.logits + ps.row * p.ld_bytes + (int64_t)ps.v * 16,
                   (uint32_t)nv * 16u, &bars[slot], pol);
   }
   ps.v += nv;
@@ -420,12 +421,12 @@ __device__ __forceinline__ void issue_next(Stream& ps, uint64_t* bars, uint8_t* 
 // registers (the OR consumes each loaded word, so the LDS results have landed
 // before the async-proxy write is issued), and refill it STAGES chunks ahead.
 template <int STAGES>
-__device__ __forceinline__ void release_refill(const uint4 (&x)[VPL], uint64_t* bars, uint8_t* ring, int slot,
+__device__ __forceinline__ void release_refill(const uint4 (&x)[FVPL], uint64_t* bars, uint8_t* ring, int slot,
                                                Stream& ps, const FwdParams& p, int64_t W, int64_t units, int lg,
                                                int64_t nvec, int lane, uint64_t pol) {
   uint32_t dep = 0;
 #pragma unroll
-  for (int kk = 0; kk < VPL; ++kk) dep |= x[kk].x | x[kk].y | x[kk].z | x[kk].w;
+  for (int kk = 0; kk < FVPL; ++kk) dep |= x[kk].x | x[kk].y | x[kk].z | x[kk].w;
   asm volatile("" ::"r"(dep));
   __syncwarp();
   // (no fence.proxy.async needed: this is a read-then-async-write hazard and
@@ -439,8 +440,8 @@ __global__ void __launch_bounds__(WARPS * 32)
 fwd_sweep_kernel(const FwdParams p) {
   extern __shared__ __align__(128) uint8_t smem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  uint8_t* ring = smem + (size_t)warp * STAGES * CH_BYTES;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + (size_t)WARPS * STAGES * CH_BYTES) + warp * STAGES;
+  uint8_t* ring = smem + (size_t)warp * STAGES * FCH_BYTES;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + (size_t)WARPS * STAGES * FCH_BYTES) + warp * STAGES;
   constexpr bool IS_BF16 = sizeof(Tin) == 2;
   constexpr int EPV = 16 / sizeof(Tin);
 
@@ -485,26 +486,26 @@ fwd_sweep_kernel(const FwdParams p) {
   while (cs.valid) {
     const int64_t row = cs.row;
     const int32_t v0 = cs.v;
-    const int nv = min(CH_VEC, cs.vend - cs.v);
+    const int nv = min(FCH_VEC, cs.vend - cs.v);
     const int k = cs.k;
     cs.v += nv;
     const bool seg_end = (cs.v == cs.vend);
     bool unit_end = false;
     if (seg_end) unit_end = stream_next_segment(cs, W, units, lg, nvec);
     mbar_wait(&bars[slot], phase);
-    const uint8_t* sp = ring + (size_t)slot * CH_BYTES;
+    const uint8_t* sp = ring + (size_t)slot * FCH_BYTES;
     const int tail_idx = (tail_elems && (int64_t)v0 + nv == nvec) ? nv - 1 : -1;
-    if (nv == CH_VEC && tail_idx < 0) {
-      uint4 x[VPL];
+    if (nv == FCH_VEC && tail_idx < 0) {
+      uint4 x[FVPL];
 #pragma unroll
-      for (int kk = 0; kk < VPL; ++kk) x[kk] = lds128(sp + (lane + 32 * kk) * 16);
+      for (int kk = 0; kk < FVPL; ++kk) x[kk] = lds128(sp + (lane + 32 * kk) * 16);
       release_refill<STAGES>(x, bars, ring, slot, ps, p, W, units, lg, nvec, lane, pol);
       if (IS_BF16) chunk_bf16<true>(x, nv, lane, c2, a, bad, -1, tail_keep);
       else chunk_f32<true>(x, nv, lane, c2, a, bad, -1, tail_keep);
     } else {
-      uint4 x[VPL];
+      uint4 x[FVPL];
 #pragma unroll
-      for (int kk = 0; kk < VPL; ++kk) {
+      for (int kk = 0; kk < FVPL; ++kk) {
         const int vi = lane + 32 * kk;
         x[kk] = (vi < nv) ? lds128(sp + vi * 16) : make_uint4(0u, 0u, 0u, 0u);
       }
@@ -691,7 +692,7 @@ __global__ void step_reduce_kernel(StepReduceParams p) {
 // ============================================================== launchers
 template <typename Tin, int WARPS, int STAGES>
 static cudaError_t launch_fwd_sweep_t(const FwdParams& p, int num_sms, cudaStream_t st) {
-  const size_t smem = (size_t)WARPS * STAGES * CH_BYTES + (size_t)WARPS * STAGES * 8;
+  const size_t smem = (size_t)WARPS * STAGES * FCH_BYTES + (size_t)WARPS * STAGES * 8;
   auto kern = fwd_sweep_kernel<Tin, WARPS, STAGES>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;

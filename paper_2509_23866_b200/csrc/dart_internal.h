@@ -29,6 +29,12 @@ constexpr int BWD_STAGES = DART_BWD_STAGES;
 #endif
 constexpr int BCH_BYTES = DART_BWD_CHB;
 constexpr int BCH_VEC = BCH_BYTES / 16;
+// fwd sweep bulk-copy chunk (bytes); canonical segments align to it
+#ifndef DART_FWD_CHB
+#define DART_FWD_CHB 4096
+#endif
+constexpr int FCH_BYTES = DART_FWD_CHB;
+constexpr int FCH_VEC = FCH_BYTES / 16;
 
 struct AdvParams {
   int64_t G, N_traj, S, T;
