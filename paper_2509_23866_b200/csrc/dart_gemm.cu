@@ -281,10 +281,17 @@ __device__ __forceinline__ void g2_tile(const GemmParams& p, int64_t t, int& mt,
   gm_tile(p, t, mt, nt);
 }
 
-template <bool A_MN, bool B_MN, int NW>
+// MC = 2: a 4-CTA cluster = two CTA pairs on adjacent N tiles of the same M
+// tile; each 128-row A block is loaded once for both pairs (each pair's CTA
+// loads 64 of its rows and multicasts them to its counterpart in the other
+// pair), so a pair reads (128 + 256) instead of (256 + 256) rows per stage
+// from L2.  Stage slots are freed only when BOTH pairs' MMAs have read them
+// (empty barriers count the two leaders' commits).
+template <bool A_MN, bool B_MN, int NW, int MC = 1>
 __global__ void __launch_bounds__(G2<NW>::THREADS, 1)
     gemm_bf16_2sm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                          const GemmParams p) {
+  static_assert(MC == 1 || NW == 1, "multicast pairs use 256 x 256 tiles");
   using C2 = G2<NW>;
   constexpr int G2_STAGES = C2::STAGES, G2_ACC = C2::ACC, G2_BN = C2::BN;
   constexpr uint32_t G2_A_BYTES = C2::A_BYTES, G2_B_BYTES = C2::B_BYTES, G2_STAGE_BYTES = C2::STAGE_BYTES;
@@ -298,12 +305,15 @@ __global__ void __launch_bounds__(G2<NW>::THREADS, 1)
   uint64_t* tempty = tfull + G2_ACC;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + G2_ACC);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const uint32_t rank = g2_rank();
+  const uint32_t crank = g2_rank();
+  const uint32_t rank = crank & 1u;            // rank within the CTA pair
+  const uint32_t pr = crank >> 1;              // pair index within the cluster (MC = 2)
   const bool leader = rank == 0;
+  const uint16_t pair_mask = (uint16_t)(0x3u << (2 * pr));
   if (threadIdx.x == 0) {
     for (int s = 0; s < G2_STAGES; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], 1);
+      mbar_init(&empty[s], MC);                // one commit per pair that reads the slot
     }
     for (int a = 0; a < G2_ACC; ++a) {
       mbar_init(&tfull[a], 1);
@@ -329,13 +339,20 @@ __global__ void __launch_bounds__(G2<NW>::THREADS, 1)
       for (int64_t t = cid; t < p.n_tiles; t += ncl) {
         int mt, nt;
         g2_tile(p, t, mt, nt);
+        if (MC == 2) nt = 2 * nt + (int)pr;      // p.n_nt counts pairs of N tiles here
         for (int kb = 0; kb < KB; ++kb) {
           mbar_wait(&empty[stage], ph ^ 1u);
           if (leader) mbar_arrive_expect_tx(&full[stage], 2 * G2_STAGE_BYTES);   // both CTAs' bytes
           uint8_t* a = sA + stage * G2_A_BYTES;
           uint8_t* b = sB + stage * G2_B_BYTES;
           const int m0 = mt * 256 + 128 * (int)rank;
-          if (A_MN) {
+          if (MC == 2) {                         // this CTA's 64-row half of the block, to both pairs
+            const uint16_t mmask = (uint16_t)((1u << rank) | (1u << (rank + 2)));
+            if (A_MN)
+              tc::tma_load_2d_2sm_mc(a + 8192 * pr, &tmA, &full[stage], m0 + 64 * (int)pr, kb * GM_BK, mmask);
+            else
+              tc::tma_load_2d_2sm_mc(a + 8192 * pr, &tmA, &full[stage], kb * GM_BK, m0 + 64 * (int)pr, mmask);
+          } else if (A_MN) {
             tc::tma_load_2d_2sm(a, &tmA, &full[stage], m0, kb * GM_BK);
             tc::tma_load_2d_2sm(a + 8192, &tmA, &full[stage], m0 + 64, kb * GM_BK);
           } else {
@@ -383,13 +400,13 @@ __global__ void __launch_bounds__(G2<NW>::THREADS, 1)
               tc::umma_bf16_2sm(d_tmem + 256 * hh, da + a_kstep * k, db + b_kstep * k, idesc,
                                 (kb | k) != 0 ? 1u : 0u);
           }
-          tc::umma_commit_2sm(&empty[stage], 0x3);
+          tc::umma_commit_2sm(&empty[stage], MC == 2 ? (uint16_t)0xF : pair_mask);
           if (++stage == G2_STAGES) {
             stage = 0;
             ph ^= 1u;
           }
         }
-        tc::umma_commit_2sm(&tfull[acc], 0x3);
+        tc::umma_commit_2sm(&tfull[acc], pair_mask);
         if (++acc == G2_ACC) {
           acc = 0;
           aph ^= 1u;
@@ -407,6 +424,7 @@ __global__ void __launch_bounds__(G2<NW>::THREADS, 1)
     for (int64_t t = cid; t < p.n_tiles; t += ncl) {
       int mt, nt;
       g2_tile(p, t, mt, nt);
+      if (MC == 2) nt = 2 * nt + (int)pr;
       mbar_wait(&tfull[acc], aph);
       tc::fence_after();
       const int64_t m = (int64_t)mt * 256 + 128 * rank + r;
@@ -475,7 +493,7 @@ __global__ void __launch_bounds__(G2<NW>::THREADS, 1)
       }
       tc::fence_before();
       __syncwarp();
-      if (lane == 0) tc::mbar_arrive_remote(&tempty[acc], 0);   // the leader's accumulator-empty barrier
+      if (lane == 0) tc::mbar_arrive_remote(&tempty[acc], crank & ~1u);   // the pair leader's accumulator-empty barrier
       if (++acc == G2_ACC) {
         acc = 0;
         aph ^= 1u;
@@ -491,20 +509,22 @@ __global__ void __launch_bounds__(G2<NW>::THREADS, 1)
   }
 }
 
-template <bool A_MN, bool B_MN, int NW>
+template <bool A_MN, bool B_MN, int NW, int MC = 1>
 cudaError_t launch_gemm_2sm(const CUtensorMap& ta, const CUtensorMap& tb, GemmParams p, int num_sms,
                             cudaStream_t st) {
-  auto kern = gemm_bf16_2sm_kernel<A_MN, B_MN, NW>;
+  auto kern = gemm_bf16_2sm_kernel<A_MN, B_MN, NW, MC>;
   constexpr size_t smem = G2<NW>::SMEM_ALL;
+  constexpr int CL = 2 * MC;                 // CTAs per cluster
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   p.n_mt = (p.M + 255) / 256;
   p.n_nt = (p.N + G2<NW>::BN - 1) / G2<NW>::BN;
+  if (MC == 2) p.n_nt = (p.n_nt + 1) / 2;    // cluster items: pairs of N tiles
   p.n_tiles = (int64_t)p.n_mt * p.n_nt;
   cudaLaunchConfig_t cfg = {};
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = 2;
+  attr[0].val.clusterDim.x = CL;
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
   cfg.blockDim = dim3(G2<NW>::THREADS);
@@ -512,13 +532,13 @@ cudaError_t launch_gemm_2sm(const CUtensorMap& ta, const CUtensorMap& tb, GemmPa
   cfg.stream = st;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  int64_t pairs = num_sms / 2;
-  cfg.gridDim = dim3((unsigned)(2 * pairs));
-  int nclu = 0;   // persistent pairs: never more clusters than can be co-resident
-  if (cudaOccupancyMaxActiveClusters(&nclu, kern, &cfg) == cudaSuccess && nclu > 0 && nclu < pairs) pairs = nclu;
+  int64_t clusters = num_sms / CL;
+  cfg.gridDim = dim3((unsigned)(CL * clusters));
+  int nclu = 0;   // persistent clusters: never more than can be co-resident
+  if (cudaOccupancyMaxActiveClusters(&nclu, kern, &cfg) == cudaSuccess && nclu > 0 && nclu < clusters) clusters = nclu;
   (void)cudaGetLastError();
-  if (pairs > p.n_tiles) pairs = p.n_tiles;
-  cfg.gridDim = dim3((unsigned)(2 * pairs));
+  if (clusters > p.n_tiles) clusters = p.n_tiles;
+  cfg.gridDim = dim3((unsigned)(CL * clusters));
   return cudaLaunchKernelEx(&cfg, kern, ta, tb, p);
 }
 
@@ -557,6 +577,20 @@ cudaError_t launch_gemm_bf16(const void* A, bool a_mn, int64_t lda, const void* 
     const bool ok2a = a_mn ? tc::make_map_bf16(&ta2, A, K, M, lda, 64, 64) : tc::make_map_bf16(&ta2, A, M, K, lda, 64, 128);
     const bool ok2b = b_mn ? tc::make_map_bf16(&tb2, B, K, N, ldb, 64, 64) : tc::make_map_bf16(&tb2, B, N, K, ldb, 64, 128);
     if (!ok2a || !ok2b) return cudaErrorInvalidValue;
+    // default: 4-CTA multicast clusters for narrow N (the LM head's dh = dz W and
+    // dW = dz^T h: N = d), CTA pairs otherwise (z = h W^T, N = V) -- measured per
+    // shape in a sustained loop (profiles/r01_gemm_vs_cublas.md)
+    const int64_t n_nt_pair = (N + 255) / 256;
+    const bool use_mc = (e2 && e2[0] == '4') || (!e2 && n_nt_pair <= 64 && M >= 1024);
+    if (use_mc) {                 // 4-CTA clusters: A blocks multicast to two pairs (see MC)
+      CUtensorMap ta4;
+      if (!(a_mn ? tc::make_map_bf16(&ta4, A, K, M, lda, 64, 64) : tc::make_map_bf16(&ta4, A, M, K, lda, 64, 64)))
+        return cudaErrorInvalidValue;
+      if (a_mn && b_mn) return launch_gemm_2sm<true, true, 1, 2>(ta4, tb2, p, num_sms, st);
+      if (a_mn) return launch_gemm_2sm<true, false, 1, 2>(ta4, tb2, p, num_sms, st);
+      if (b_mn) return launch_gemm_2sm<false, true, 1, 2>(ta4, tb2, p, num_sms, st);
+      return launch_gemm_2sm<false, false, 1, 2>(ta4, tb2, p, num_sms, st);
+    }
     if (e2 && e2[0] == '2') {     // 256 x 512 pair tiles (opt-in, see G2<2>)
       if (a_mn && b_mn) return launch_gemm_2sm<true, true, 2>(ta2, tb2, p, num_sms, st);
       if (a_mn) return launch_gemm_2sm<true, false, 2>(ta2, tb2, p, num_sms, st);
