@@ -292,6 +292,8 @@ __global__ void __launch_bounds__(G2<NW>::THREADS, 1)
     gemm_bf16_2sm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                          const GemmParams p) {
   static_assert(MC == 1 || NW == 1, "multicast pairs use 256 x 256 tiles");
+  // MC = 3: the same with the roles swapped -- the two pairs sit on adjacent
+  // M tiles of the same N tile and the B block is the one multicast
   using C2 = G2<NW>;
   constexpr int G2_STAGES = C2::STAGES, G2_ACC = C2::ACC, G2_BN = C2::BN;
   constexpr uint32_t G2_A_BYTES = C2::A_BYTES, G2_B_BYTES = C2::B_BYTES, G2_STAGE_BYTES = C2::STAGE_BYTES;
@@ -313,7 +315,7 @@ __global__ void __launch_bounds__(G2<NW>::THREADS, 1)
   if (threadIdx.x == 0) {
     for (int s = 0; s < G2_STAGES; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], MC);                // one commit per pair that reads the slot
+      mbar_init(&empty[s], MC >= 2 ? 2 : 1);   // one commit per pair that reads the slot
     }
     for (int a = 0; a < G2_ACC; ++a) {
       mbar_init(&tfull[a], 1);
@@ -340,6 +342,7 @@ __global__ void __launch_bounds__(G2<NW>::THREADS, 1)
         int mt, nt;
         g2_tile(p, t, mt, nt);
         if (MC == 2) nt = 2 * nt + (int)pr;      // p.n_nt counts pairs of N tiles here
+        if (MC == 3) mt = 2 * mt + (int)pr;      // p.n_mt counts pairs of M tiles here
         for (int kb = 0; kb < KB; ++kb) {
           mbar_wait(&empty[stage], ph ^ 1u);
           if (leader) mbar_arrive_expect_tx(&full[stage], 2 * G2_STAGE_BYTES);   // both CTAs' bytes
@@ -362,7 +365,13 @@ __global__ void __launch_bounds__(G2<NW>::THREADS, 1)
           for (int hh = 0; hh < NW; ++hh) {   // B rows of MMA hh: [nt*BN + 256 hh, +256), this CTA's 128
             const int n0 = nt * G2_BN + 256 * hh + 128 * (int)rank;
             uint8_t* bh = b + hh * C2::B_HALF;
-            if (B_MN) {
+            if (MC == 3) {                       // this CTA's 64-row half of the B block, to both pairs
+              const uint16_t mmask = (uint16_t)((1u << rank) | (1u << (rank + 2)));
+              if (B_MN)
+                tc::tma_load_2d_2sm_mc(bh + 8192 * pr, &tmB, &full[stage], n0 + 64 * (int)pr, kb * GM_BK, mmask);
+              else
+                tc::tma_load_2d_2sm_mc(bh + 8192 * pr, &tmB, &full[stage], kb * GM_BK, n0 + 64 * (int)pr, mmask);
+            } else if (B_MN) {
               tc::tma_load_2d_2sm(bh, &tmB, &full[stage], n0, kb * GM_BK);
               tc::tma_load_2d_2sm(bh + 8192, &tmB, &full[stage], n0 + 64, kb * GM_BK);
             } else {
@@ -400,7 +409,7 @@ __global__ void __launch_bounds__(G2<NW>::THREADS, 1)
               tc::umma_bf16_2sm(d_tmem + 256 * hh, da + a_kstep * k, db + b_kstep * k, idesc,
                                 (kb | k) != 0 ? 1u : 0u);
           }
-          tc::umma_commit_2sm(&empty[stage], MC == 2 ? (uint16_t)0xF : pair_mask);
+          tc::umma_commit_2sm(&empty[stage], MC >= 2 ? (uint16_t)0xF : pair_mask);
           if (++stage == G2_STAGES) {
             stage = 0;
             ph ^= 1u;
@@ -425,6 +434,7 @@ __global__ void __launch_bounds__(G2<NW>::THREADS, 1)
       int mt, nt;
       g2_tile(p, t, mt, nt);
       if (MC == 2) nt = 2 * nt + (int)pr;
+      if (MC == 3) mt = 2 * mt + (int)pr;
       mbar_wait(&tfull[acc], aph);
       tc::fence_after();
       const int64_t m = (int64_t)mt * 256 + 128 * rank + r;
@@ -514,12 +524,13 @@ cudaError_t launch_gemm_2sm(const CUtensorMap& ta, const CUtensorMap& tb, GemmPa
                             cudaStream_t st) {
   auto kern = gemm_bf16_2sm_kernel<A_MN, B_MN, NW, MC>;
   constexpr size_t smem = G2<NW>::SMEM_ALL;
-  constexpr int CL = 2 * MC;                 // CTAs per cluster
+  constexpr int CL = MC >= 2 ? 4 : 2;        // CTAs per cluster
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   p.n_mt = (p.M + 255) / 256;
   p.n_nt = (p.N + G2<NW>::BN - 1) / G2<NW>::BN;
   if (MC == 2) p.n_nt = (p.n_nt + 1) / 2;    // cluster items: pairs of N tiles
+  if (MC == 3) p.n_mt = (p.n_mt + 1) / 2;    // cluster items: pairs of M tiles
   p.n_tiles = (int64_t)p.n_mt * p.n_nt;
   cudaLaunchConfig_t cfg = {};
   cudaLaunchAttribute attr[1];
@@ -590,6 +601,15 @@ cudaError_t launch_gemm_bf16(const void* A, bool a_mn, int64_t lda, const void* 
       if (a_mn) return launch_gemm_2sm<true, false, 1, 2>(ta4, tb2, p, num_sms, st);
       if (b_mn) return launch_gemm_2sm<false, true, 1, 2>(ta4, tb2, p, num_sms, st);
       return launch_gemm_2sm<false, false, 1, 2>(ta4, tb2, p, num_sms, st);
+    }
+    if (e2 && e2[0] == '5') {     // 4-CTA clusters: B blocks multicast to two pairs (opt-in, MC = 3)
+      CUtensorMap tb4;
+      if (!(b_mn ? tc::make_map_bf16(&tb4, B, K, N, ldb, 64, 64) : tc::make_map_bf16(&tb4, B, N, K, ldb, 64, 64)))
+        return cudaErrorInvalidValue;
+      if (a_mn && b_mn) return launch_gemm_2sm<true, true, 1, 3>(ta2, tb4, p, num_sms, st);
+      if (a_mn) return launch_gemm_2sm<true, false, 1, 3>(ta2, tb4, p, num_sms, st);
+      if (b_mn) return launch_gemm_2sm<false, true, 1, 3>(ta2, tb4, p, num_sms, st);
+      return launch_gemm_2sm<false, false, 1, 3>(ta2, tb4, p, num_sms, st);
     }
     if (e2 && e2[0] == '2') {     // 256 x 512 pair tiles (opt-in, see G2<2>)
       if (a_mn && b_mn) return launch_gemm_2sm<true, true, 2>(ta2, tb2, p, num_sms, st);
