@@ -757,7 +757,7 @@ def run_lmhead_update(args):
     torch.cuda.synchronize()
     keep, norm = old.keep.clone(), old.norm.clone()
     del old
-    up = lmhead.LmHeadUpdate(layout, V, d, cfg, dev, chunk_rows=args.chunk_rows)
+    up = lmhead.LmHeadUpdate(layout, V, d, cfg, dev, chunk_rows=args.chunk_rows, dw_group=args.dw_group)
     dh = torch.empty((layout.T, d), dtype=torch.float32, device=dev)
     dW = torch.empty((V, d), dtype=torch.float32, device=dev)
     args_in = (lb.hidden, lb.weight, b.target, b.logp_old, b.logp_rollout, b.logp_ref, keep, norm)
@@ -829,6 +829,7 @@ def run_lmhead_update(args):
         "vs_baseline": None, "dtype": "bf16", "data": "synthetic (seeded; synth.make_lmhead recipe, DESIGN.md §9)",
         "config": {"workload": args.config + " (LM-head update pass: NEXT #3 training half)",
                    "tokens": layout.T, "V": V, "d": d, "chunk_rows": args.chunk_rows, "chunks": len(up.chunks),
+                   "dw_group": up.dw_group,
                    "kept_token_frac": float(up.stats_dict()["n_kept_tok"]) / layout.T,
                    "l2": "inputs larger than L2 (W %.2f GB, hidden %.2f GB, chunk logits %.2f GB)" % (
                        V * d * 2 / 1e9, layout.T * d * 2 / 1e9, up.rows * V * 4 / 1e9),
@@ -1132,6 +1133,7 @@ def main():
     ap.add_argument("--no-unfused", action="store_true", help="--lmhead: skip the cuBLAS + logits comparison")
     ap.add_argument("--update", action="store_true", help="--lmhead: time the update pass (dh, dW) instead")
     ap.add_argument("--chunk-rows", type=int, default=8192, help="--lmhead --update: rows per chunk")
+    ap.add_argument("--dw-group", type=int, default=1, help="--lmhead --update: chunks per dW GEMM")
     ap.add_argument("--backend", default="nccl", choices=["nccl", "gloo"],
                     help="gloo: test path (ranks may share a GPU; collectives staged via host)")
     args = ap.parse_args()

@@ -53,7 +53,12 @@ class LmHeadUpdate:
     """Buffers + ABI sequence of the LM-head update pass for one shard."""
 
     def __init__(self, layout, V: int, d: int, cfg: dart.Config, device, shard: Optional[Shard] = None,
-                 chunk_rows: int = 8192):
+                 chunk_rows: int = 8192, dw_group: int = 1):
+        """dw_group: chunks whose dz rows are kept together for ONE dW GEMM
+        (K = their rows): the fp32 read-modify-write of dW [V, d] runs once
+        per group instead of once per chunk, for dw_group x the dz buffer.
+        Measured slower on B200 (update pass 191-193 ms with 2 or 4 vs 188
+        with 1, same box: the SM clock under the power cap fell), so 1."""
         if V % 8 or d % 8:
             raise dart.DartError("the LM-head update needs V % 8 == 0 and d % 8 == 0")
         self.L = dart.lib()
@@ -64,9 +69,12 @@ class LmHeadUpdate:
         self.meta = dart.Meta.from_layout(layout, dev)
         self.chunks = chunk_shard(layout, self.shard, chunk_rows)
         self.rows = max(c.T_loc for c in self.chunks)
+        self.dw_group = max(1, int(dw_group))
+        grp_rows = [sum(c.T_loc for c in self.chunks[i:i + self.dw_group])
+                    for i in range(0, len(self.chunks), self.dw_group)]
         f32 = dict(dtype=torch.float32, device=dev)
         self.z = torch.empty((self.rows, self.V), **f32)                          # fp32 logits of one chunk
-        self.dz = torch.empty((self.rows, self.V), dtype=torch.bfloat16, device=dev)
+        self.dz = torch.empty((max(grp_rows), self.V), dtype=torch.bfloat16, device=dev)   # dz of one dW group
         T, S = self.shard.T_loc, self.shard.S_loc
         self.lse, self.logp = torch.empty(T, **f32), torch.empty(T, **f32)
         self.ell, self.dell = torch.empty(T, **f32), torch.empty(T, **f32)
@@ -114,10 +122,13 @@ class LmHeadUpdate:
         meta, cfg = ctypes.byref(self.meta.c()), ctypes.byref(self.cfg.c())
         beta = self.cfg.beta_kl > 0
         launches = 0
+        g0, goff, ngrp = 0, 0, 0      # first row of the current dW group, its dz fill level, dW GEMMs so far
         for i, c in enumerate(self.chunks):
             r0, r1 = c.tok_begin - self.shard.tok_begin, c.tok_end - self.shard.tok_begin
             n = r1 - r0
-            z, dz, hc = self.z[:n], self.dz[:n], hidden[r0:r1]
+            if i % self.dw_group == 0:
+                g0, goff = r0, 0
+            z, dz, hc = self.z[:n], self.dz[goff:goff + n], hidden[r0:r1]
             dart.gemm_bf16(hc, weight, z)                                        # z_c = h_c W^T
             launches += self.L.dart_last_launch_count()
             b = self._batch(c, z, target[r0:r1], logp_old[r0:r1], logp_roll[r0:r1],
@@ -128,9 +139,13 @@ class LmHeadUpdate:
             launches += self.L.dart_last_launch_count()
             dart.gemm_bf16(dz, weight, dh[r0:r1], b_mn_major=True)               # dh_c = dz_c W
             launches += self.L.dart_last_launch_count()
-            mode = dart.GEMM_ACCUM_F32 if (accumulate_dW or i > 0) else dart.GEMM_STORE_F32
-            dart.gemm_bf16(dz, hc, dW, a_mn_major=True, b_mn_major=True, mode=mode)   # dW (+)= dz_c^T h_c
-            launches += self.L.dart_last_launch_count()
+            goff += n
+            if (i + 1) % self.dw_group == 0 or i + 1 == len(self.chunks):
+                mode = dart.GEMM_ACCUM_F32 if (accumulate_dW or ngrp > 0) else dart.GEMM_STORE_F32
+                dart.gemm_bf16(self.dz[:goff], hidden[g0:g0 + goff], dW, a_mn_major=True, b_mn_major=True,
+                               mode=mode)                                       # dW (+)= dz_g^T h_g
+                launches += self.L.dart_last_launch_count()
+                ngrp += 1
         self.launches += launches
         return dh, dW
 

@@ -199,3 +199,23 @@ def test_lmhead_update_full_size_sampled_rows():
     assert np.all(np.isfinite(dW[:4096].cpu().numpy()))
     st = up.stats_dict()
     assert st["n_kept_tok"] == tok_keep.sum()
+
+
+def test_lmhead_update_dw_group_invariance():
+    """Grouping chunks into one dW GEMM (dw_group) changes only the fp32
+    accumulation order of dW; dh is bitwise the same."""
+    lb = synth.make_lmhead("grid3x4x3x24@3000", 256, seed=27)
+    cfg = dart.Config()
+    old = old_pass(lb, cfg)
+    b = lb.batch
+    outs = []
+    for g in (1, 3):
+        up = lmhead.LmHeadUpdate(b.layout, b.V, 256, cfg, "cuda", chunk_rows=150, dw_group=g)
+        dh, dW = up.run(lb.hidden.cuda(), lb.weight.cuda(), b.target.cuda(), b.logp_old.cuda(),
+                        b.logp_rollout.cuda(), b.logp_ref.cuda(), old.keep, old.norm)
+        torch.cuda.synchronize()
+        up.check_status()
+        assert len(up.chunks) > 3
+        outs.append((dh, dW))
+    assert torch.equal(outs[0][0], outs[1][0])
+    assert torch.allclose(outs[0][1], outs[1][1], rtol=1e-5, atol=1e-7)
