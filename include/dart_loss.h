@@ -294,8 +294,14 @@ dart_status dart_lmhead_fwd(const dart_lmhead* head, const dart_batch* batch, co
  *   a_mn_major = 0: A is row-major [M, K] (lda >= K); 1: A^T is stored,
  *   row-major [K, M] (lda >= M).  Likewise B: 0 = [N, K], 1 = [K, N].
  * C: device, row-major [M, ldc] of fp32 (STORE_F32, ACCUM_F32) or bf16,
- * 16-byte aligned, ldc >= N, N % 8 == 0, ldc % 8 == 0.  Asynchronous on
- * `stream`; no workspace. */
+ * 16-byte aligned, ldc >= N, N % 8 == 0, ldc % 8 == 0.  The caller owns C's
+ * element type: the library sees only the pointer, so c_mode must match it
+ * (the Python binding checks).  Asynchronous on `stream`; no workspace.
+ * Kernel choice (results are bit-identical across them for exact operands):
+ * 256 x 256 tcgen05 CTA-pair tiles; 4-CTA clusters multicasting the A block
+ * to two pairs when N <= 64 * 256 and M >= 1024.  Environment override
+ * DART_GEMM_2SM: 0 = 1-CTA 128 x 256 tiles, 1 = pairs only, 2 = 256 x 512
+ * pair tiles, 4 = A-multicast clusters, 5 = B-multicast clusters. */
 typedef enum { DART_GEMM_STORE_F32 = 0, DART_GEMM_STORE_BF16 = 1, DART_GEMM_ACCUM_F32 = 2 } dart_gemm_mode;
 dart_status dart_gemm_bf16(const void* A, int32_t a_mn_major, int64_t lda, const void* B, int32_t b_mn_major,
                            int64_t ldb, void* C, int32_t c_mode, int64_t ldc, int64_t M, int64_t N, int64_t K,
