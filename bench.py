@@ -8,8 +8,10 @@ written, masked rows written as zeros) -> C2 stats all-reduce (N > 1).
 
 Usage:  python bench.py [--gpus N] [--steps K] [--warmup W] [--config single]
         python bench.py --impl reference ...   (the float64 CPU oracle arm)
-For N > 1 launch with torchrun (one rank per GPU, NCCL).  Weak scaling: every
-rank owns its own 8-task batch of the config (global G = 8 N).
+For N > 1 either launch with torchrun (one rank per GPU, NCCL; the driver's
+way) or run `python bench.py --gpus N`, which starts the N ranks itself the
+same way.  Weak scaling: every rank owns its own batch of the config (its own
+rewards, drawn with seed + 1000 r; global G = 8 N for `single`).
 """
 from __future__ import annotations
 
@@ -120,22 +122,116 @@ def dist_setup(args):
     return world, rank, local
 
 
-def global_layout(per_rank_layout, world):
-    """Weak scaling: concatenate `world` copies of the per-rank layout
-    (rewards re-drawn per rank by the caller)."""
-    from paper_2509_23866_b200 import synth
-    L = per_rank_layout
-    tg, tr, tso, sto, fk = [], [], [0], [0], []
+def rank_seed(seed, r):
+    """Seed of rank r's own batch (rank 0 keeps the N = 1 seed)."""
+    return seed + 1000 * r
+
+
+def weak_layouts(config, seed, world):
+    """Weak scaling: every rank owns its own batch of `config` (its own
+    rewards and, for ragged configs, its own lengths), drawn with
+    rank_seed(seed, r).  Returns (per-rank layouts, global layout = their
+    concatenation with group ids offset, shards = the per-rank blocks, V,
+    dtype).  All ranks compute the same global layout."""
+    from paper_2509_23866_b200 import dart, synth
+    lays = []
+    V = dtype = None
     for r in range(world):
-        tg.append(L.traj_group + r * L.G)
+        L, V, dtype, _ = synth.config_layout(config, seed=rank_seed(seed, r))
+        lays.append(L)
+    tg, tr, tso, sto, fk, shards = [], [], [0], [0], [], []
+    g0 = n0 = s0 = t0 = 0
+    for L in lays:
+        tg.append(L.traj_group + g0)
         tr.append(L.traj_reward)
-        tso.extend((L.traj_step_off[1:] + r * L.S).tolist())
-        sto.extend((L.step_tok_off[1:] + r * L.T).tolist())
+        tso.extend((L.traj_step_off[1:] + s0).tolist())
+        sto.extend((L.step_tok_off[1:] + t0).tolist())
         fk.append(L.step_fork)
-    return synth.Layout(G=L.G * world, traj_group=np.concatenate(tg).astype(np.int32),
-                        traj_reward=np.concatenate(tr).astype(np.float32),
-                        traj_step_off=np.asarray(tso, dtype=np.int64),
-                        step_tok_off=np.asarray(sto, dtype=np.int64), step_fork=np.concatenate(fk))
+        shards.append(dart.Shard(n0, n0 + L.N_traj, s0, s0 + L.S, t0, t0 + L.T))
+        g0, n0, s0, t0 = g0 + L.G, n0 + L.N_traj, s0 + L.S, t0 + L.T
+    glayout = synth.Layout(G=g0, traj_group=np.concatenate(tg).astype(np.int32),
+                           traj_reward=np.concatenate(tr).astype(np.float32),
+                           traj_step_off=np.asarray(tso, dtype=np.int64),
+                           step_tok_off=np.asarray(sto, dtype=np.int64), step_fork=np.concatenate(fk))
+    return lays, glayout, shards, V, dtype
+
+
+def _free_port():
+    import socket
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def self_launch(args, argv):
+    """`python bench.py --gpus N` without torchrun: launch N ranks the way the
+    driver does (torch.distributed.run, one process per GPU, 127.0.0.1) and
+    pass rank 0's JSON line through.  Returns the launcher's exit code."""
+    if args.backend == "nccl" and not args.dry_run:
+        n = torch.cuda.device_count()
+        if n < args.gpus:
+            log(f"--gpus {args.gpus} needs {args.gpus} visible GPUs for one NCCL rank per GPU, found {n}")
+            return 2
+        from paper_2509_23866_b200 import build as B      # build once, before the ranks start
+        B.build()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={_free_port()}", os.path.abspath(__file__)] + list(argv)
+    log("launching: " + " ".join(cmd))
+    return subprocess.call(cmd)
+
+
+def run_dry(args):
+    """--dry-run (CPU, any backend): the N-rank plumbing without kernels --
+    launch, weak-scaling layouts and shards, C1 (all-gather of per-rank
+    step values padded to S_pad) and C2 (all-reduce) over the process group,
+    max-over-ranks timing -- so the launcher and the collectives' shapes
+    can be tested on a host without a GPU.  Prints a JSON line with
+    "dry_run": true and no throughput."""
+    import torch.distributed as tdist
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if world > 1:
+        tdist.init_process_group("gloo")
+    lays, glayout, shards, V, _ = weak_layouts(args.config, args.seed, world)
+    me = shards[rank]
+    S_pad = max(s.S_loc for s in shards)
+    local = torch.full((S_pad,), -1.0, dtype=torch.float32)
+    local[:me.S_loc] = torch.arange(me.step_begin, me.step_end, dtype=torch.float32)
+    t0 = time.perf_counter()
+    if world > 1:
+        gathered = torch.empty(world * S_pad, dtype=torch.float32)
+        tdist.all_gather_into_tensor(gathered, local)
+        stats = torch.tensor([float(me.T_loc), float(me.S_loc)], dtype=torch.float64)
+        tdist.all_reduce(stats)
+    else:
+        gathered, stats = local, torch.tensor([float(me.T_loc), float(me.S_loc)], dtype=torch.float64)
+    ms = torch.tensor([(time.perf_counter() - t0) * 1e3], dtype=torch.float64)
+    if world > 1:
+        tdist.all_reduce(ms, op=tdist.ReduceOp.MAX)
+    # C1 delivered every rank's steps, in global step order, at rank r's padded slot
+    g = gathered.view(world, S_pad)
+    order_ok = all(bool(torch.equal(g[r, :s.S_loc], torch.arange(s.step_begin, s.step_end, dtype=torch.float32)))
+                   for r, s in enumerate(shards))
+    if rank == 0:
+        print(json.dumps({
+            "dry_run": True, "metric": METRIC, "value": None, "unit": "logit-tokens/s", "n_gpus": world,
+            "steps": 0, "warmup": 0, "ms_per_step": None, "collectives_ms_max_over_ranks": float(ms),
+            "backend": tdist.get_backend() if world > 1 else None,
+            "config": {"workload": args.config, "global_tokens": glayout.T, "groups": glayout.G,
+                       "steps_total": glayout.S, "tokens_per_rank": [s.T_loc for s in shards],
+                       "rewards_distinct_per_rank": world == 1 or any(
+                           not np.array_equal(lays[0].traj_reward, L.traj_reward) for L in lays[1:]),
+                       "parallelism": f"dp{world} (trajectory-sharded)"},
+            "c1_layout_ok": order_ok, "c2_sum_tokens": float(stats[0]), "c2_sum_steps": float(stats[1])}),
+            flush=True)
+    if world > 1:
+        tdist.barrier()
+        tdist.destroy_process_group()
+
+
+METRIC = "loss fwd+bwd logit-tokens/s at V=152064 bf16, % of HBM peak, 1/2/4/8 GPU"
 
 
 CONFIG_DESC = {
@@ -235,7 +331,7 @@ def run_streamed(args):
     peak, src = hbm_peak()
     gbs = byts / (ms * 1e-3) / 1e9
     if rank == 0:
-        line = {"metric": "loss fwd+bwd logit-tokens/s at V=152064 bf16, % of HBM peak, 1/2/4/8 GPU",
+        line = {"metric": METRIC,
                 "value": T / (ms * 1e-3), "unit": "logit-tokens/s", "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
                 "scaling": "strong" if world > 1 else "weak",
@@ -268,12 +364,8 @@ def run_dart(args):
         dist.barrier()
     from paper_2509_23866_b200 import dart, synth
     dev = torch.device("cuda", torch.cuda.current_device())
-    layout_r, V, dtype, _ = synth.config_layout(args.config, seed=args.seed)
-    glayout = global_layout(layout_r, world)
-    shards = []
-    for r in range(world):
-        shards.append(dart.Shard(r * layout_r.N_traj, (r + 1) * layout_r.N_traj, r * layout_r.S,
-                                 (r + 1) * layout_r.S, r * layout_r.T, (r + 1) * layout_r.T))
+    lays, glayout, shards, V, dtype = weak_layouts(args.config, args.seed, world)
+    layout_r = lays[rank]
     me = shards[rank]
     cfg = dart.Config(entropy_q=args.q, beta_kl=args.beta, zero_fill_masked=0 if args.compact else 1,
                       select_rule=dart.SEL_OFF if args.q <= 0 else dart.SEL_FLOOR,
@@ -484,7 +576,7 @@ def run_dart(args):
 
     if rank == 0:
         line = {
-            "metric": "loss fwd+bwd logit-tokens/s at V=152064 bf16, % of HBM peak, 1/2/4/8 GPU",
+            "metric": METRIC,
             "value": value, "unit": "logit-tokens/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "bf16", "data": "synthetic (seeded; DESIGN.md §5 recipe)",
@@ -553,10 +645,8 @@ def run_lmhead(args):
         dist.barrier()
     from paper_2509_23866_b200 import dart, synth
     dev = torch.device("cuda", torch.cuda.current_device())
-    layout_r, V, _, _ = synth.config_layout(args.config, seed=args.seed)
-    glayout = global_layout(layout_r, world)
-    shards = [dart.Shard(r * layout_r.N_traj, (r + 1) * layout_r.N_traj, r * layout_r.S, (r + 1) * layout_r.S,
-                         r * layout_r.T, (r + 1) * layout_r.T) for r in range(world)]
+    lays, glayout, shards, V, _ = weak_layouts(args.config, args.seed, world)
+    layout_r = lays[rank]
     me = shards[rank]
     d = args.hidden
     cfg = dart.Config(entropy_q=args.q, beta_kl=args.beta)
@@ -630,7 +720,8 @@ def run_lmhead(args):
     if not args.no_unfused and rank == 0:
         try:
             logits = torch.empty((me.T_loc, V), dtype=torch.bfloat16, device=dev)
-            dl2 = dart.DartLoss(glayout, me, V, cfg, dev, with_grad=False)
+            # this rank's own batch as a one-rank problem: the same rows and work
+            dl2 = dart.DartLoss(layout_r, dart.whole_shard(layout_r), V, cfg, dev, with_grad=False)
             k = max(3, min(args.steps, 10))
 
             def ustep():
@@ -1076,7 +1167,7 @@ def run_reference(args):
     finally:
         pool.close()
     value = ntok / dt
-    line = {"impl": "reference", "metric": "loss fwd+bwd logit-tokens/s at V=152064 bf16, % of HBM peak, 1/2/4/8 GPU",
+    line = {"impl": "reference", "metric": METRIC,
             "value": value, "unit": "logit-tokens/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": dt * 1e3, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
             "dtype": "f64", "data": "synthetic (seeded; DESIGN.md §5 recipe)",
@@ -1103,7 +1194,7 @@ def _first_traj_layout(L):
                         step_tok_off=sto, step_fork=L.step_fork[:S])
 
 
-def main():
+def main(argv=None):
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=50)
@@ -1136,11 +1227,22 @@ def main():
     ap.add_argument("--dw-group", type=int, default=1, help="--lmhead --update: chunks per dW GEMM")
     ap.add_argument("--backend", default="nccl", choices=["nccl", "gloo"],
                     help="gloo: test path (ranks may share a GPU; collectives staged via host)")
-    args = ap.parse_args()
+    ap.add_argument("--dry-run", action="store_true",
+                    help="N-rank plumbing only (launcher, shards, C1/C2 over gloo), no kernels: CPU tests")
+    args = ap.parse_args(argv)
     if args.warmup < 3:
         log("warning: --warmup < 3 violates the timing rules; using 3")
         args.warmup = 3
-    if args.impl == "reference":
+    argv = sys.argv[1:] if argv is None else list(argv)
+    env_world = os.environ.get("WORLD_SIZE")
+    if env_world is None and args.gpus > 1:
+        # not under torchrun: start one rank per GPU ourselves (the driver's launch)
+        raise SystemExit(self_launch(args, argv))
+    if env_world is not None and int(env_world) != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} does not match WORLD_SIZE={env_world} (one rank per GPU)")
+    if args.dry_run:
+        run_dry(args)
+    elif args.impl == "reference":
         run_reference(args)
     elif args.lmhead and args.update:
         run_lmhead_update(args)

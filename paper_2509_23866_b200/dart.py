@@ -191,6 +191,20 @@ def set_timing_events(fwd_begin=None, fwd_end=None, bwd_begin=None, bwd_end=None
     lib().dart_set_timing_events(*ev)
 
 
+def _check_token_inputs(cfg, T, target, logp_old, logp_roll, logp_ref):
+    """Per-token inputs: int32 targets and fp32 log-probs, contiguous, [T];
+    logp_ref only when the k3 KL term reads it (beta > 0, kl_mode = K3)."""
+    req = [("target", target, torch.int32), ("logp_old", logp_old, torch.float32),
+           ("logp_rollout", logp_roll, torch.float32)]
+    if cfg.beta_kl > 0 and cfg.kl_mode == KL_K3:
+        if logp_ref is None:
+            raise DartError("beta_kl > 0 with the k3 KL needs logp_ref")
+        req.append(("logp_ref", logp_ref, torch.float32))
+    for name, t, dt in req:
+        if t is None or t.dtype != dt or not t.is_contiguous() or t.numel() != T:
+            raise DartError(f"{name} must be a contiguous {dt} [{T}] tensor")
+
+
 # --------------------------------------------------------------------- config
 @dataclasses.dataclass
 class Config:
@@ -318,6 +332,9 @@ class DartLoss:
         self.dlogits = self.dlogits_store[:, :self.V] if with_grad else None
         # world layout for select (rank r owns global steps [rank_step_off[r], [r+1]))
         if world_shards is None:
+            if (shard.tok_begin, shard.tok_end, shard.step_begin, shard.step_end) != (0, layout.T, 0, layout.S):
+                # select() would read layout.S gathered entries from an S_loc buffer
+                raise DartError("a partial shard needs world_shards (every rank's shard) for the selection")
             world_shards = [shard]
         self.world = len(world_shards)
         self.S_pad = max(max(s.S_loc for s in world_shards), 1)
@@ -353,10 +370,7 @@ class DartLoss:
             raise DartError(f"logits shape {tuple(logits.shape)} != ({self.shard.T_loc}, {self.V})")
         if logits.stride(1) != 1 or logits.stride(0) != self.ld:
             raise DartError(f"logits must be row-major with row pitch ld={self.ld}")
-        for name, t, dt in (("target", target, torch.int32), ("logp_old", logp_old, torch.float32),
-                            ("logp_rollout", logp_roll, torch.float32)):
-            if t.dtype != dt or not t.is_contiguous() or t.numel() != self.shard.T_loc:
-                raise DartError(f"{name} must be a contiguous {dt} [{self.shard.T_loc}] tensor")
+        _check_token_inputs(self.cfg, self.shard.T_loc, target, logp_old, logp_roll, logp_ref)
 
     def _check_ref(self, ref_logits):
         if self.cfg.kl_mode == KL_EXACT and self.cfg.beta_kl > 0:
@@ -393,10 +407,7 @@ class DartLoss:
                 or hidden.shape[1] != weight.shape[1] or hidden.stride(1) != 1 or weight.stride(1) != 1:
             raise DartError(f"hidden [{T}, d] and weight [{self.V}, d] row-major expected, got "
                             f"{tuple(hidden.shape)} / {tuple(weight.shape)}")
-        for name, t, dt in (("target", target, torch.int32), ("logp_old", logp_old, torch.float32),
-                            ("logp_rollout", logp_roll, torch.float32)):
-            if t.dtype != dt or not t.is_contiguous() or t.numel() != T:
-                raise DartError(f"{name} must be a contiguous {dt} [{T}] tensor")
+        _check_token_inputs(self.cfg, T, target, logp_old, logp_roll, logp_ref)
         st = (stream or torch.cuda.current_stream(self.device)).cuda_stream
         use_k3 = self.cfg.beta_kl > 0 and self.cfg.kl_mode == KL_K3
         head = dart_lmhead(_ptr(hidden), _ptr(weight), int(hidden.shape[1]), int(hidden.stride(0)),

@@ -116,6 +116,11 @@ class LmHeadUpdate:
         if hidden.dtype != torch.bfloat16 or weight.dtype != torch.bfloat16 or hidden.shape != (T, self.d) \
                 or weight.shape != (self.V, self.d):
             raise dart.DartError(f"hidden [{T}, {self.d}] / weight [{self.V}, {self.d}] bf16 expected")
+        dart._check_token_inputs(self.cfg, T, target, logp_old, logp_roll, logp_ref)
+        if keep.dtype != torch.uint8 or not keep.is_contiguous() or keep.numel() < self.layout.S:
+            raise dart.DartError(f"keep must be a contiguous uint8 [{self.layout.S}] tensor")
+        if norm.dtype != torch.int64 or not norm.is_contiguous() or norm.numel() != 5:
+            raise dart.DartError("norm must be the int64 [5] dart_norm of the old-policy pass")
         dh = torch.empty((T, self.d), dtype=torch.float32, device=self.device) if dh is None else dh
         dW = torch.empty((self.V, self.d), dtype=torch.float32, device=self.device) if dW is None else dW
         s = torch.cuda.current_stream(self.device).cuda_stream

@@ -79,6 +79,10 @@ class StreamedPass:
     def __init__(self, layout, V: int, cfg: dart.Config, device, max_rows: int, pool: int = 3,
                  logits_dtype=torch.bfloat16, grad_dtype=torch.bfloat16, group=None,
                  world_shards: Optional[List[Shard]] = None):
+        if cfg.kl_mode == dart.KL_EXACT and cfg.beta_kl > 0:
+            # the pool holds only the policy's logits; the exact KL would also need the
+            # reference policy's rows streamed per chunk
+            raise dart.DartError("the streamed pass supports the k3 KL only (kl_mode=KL_K3 or beta_kl=0)")
         self.L = dart.lib()
         dev = torch.device(device)
         self.device, self.layout, self.V, self.cfg = dev, layout, int(V), cfg

@@ -156,6 +156,13 @@ def config_layout(name, seed=0, real_reward=False):
             cap = int(rng.integers(10, 51))
             groups.append(list(rng.integers(1, cap + 1, size=n)))
         return _layout(groups, lambda r: int(r.integers(16, 129)), rw, rng), V_QWEN, torch.bfloat16, 1.0
+    if name == "adaptive_mini":  # the adaptive recipe scaled down for whole-batch oracle parity
+        groups = []
+        for _ in range(6):
+            n = int(rng.integers(2, 9))
+            cap = int(rng.integers(2, 9))
+            groups.append(list(rng.integers(1, cap + 1, size=n)))
+        return _layout(groups, lambda r: int(r.integers(4, 41)), rw, rng), 4099, torch.bfloat16, 1.0
     if name.startswith("scale"):  # scale<k>: 2^k tokens in groups of 8 x 16 steps x 64 tokens
         k = int(name[5:])
         G = (1 << k) // (8 * 16 * 64)

@@ -147,69 +147,29 @@ def test_bad_metadata_status():
     assert int(dl.status.item()) & (1 << 4)
 
 
-def test_single_config_full_size_sampled():
-    """BASELINE.json single-GPU config at full size (T = 61440, V = 152064) in
-    the bench's launch configuration: sampled rows vs the oracle, properties
-    on everything else."""
-    b = synth.make_batch("single", seed=0, device="cuda")
+@pytest.mark.parametrize("seed", [0, 1])
+def test_single_config_full_size_vs_oracle(seed):
+    """BASELINE.json single-GPU config at full size (T = 61440, V = 152064,
+    960 steps, 8 groups) in the bench's launch configuration (seed 0 is the
+    bench's own batch): EVERY row through the float64 oracle on the host
+    cores -- every lse / H / log-prob / ell / dell, every step entropy, the
+    oracle's own per-group tau and mask (bit-exact except steps within 1e-6
+    of tau), the normaliser, loss, statistics and every dlogits row."""
+    b = synth.make_batch("single", seed=seed, device="cuda")
     cfg = dart.Config()
     dl = run_gpu(b, cfg)
     dl.check_status()
-    L = b.layout
-    rng = np.random.default_rng(1)
-    rows = sorted(rng.choice(L.T, 16, replace=False).tolist())
-    from oracle import dart_oracle as O
-    from tests.gpu_helpers import oracle_select_on, bf16_ulp, P_REL
-    cfgf = cfg.as_f32()
-    # selection decided identically from the same values; >= 80% kept per valid group
+    from tests.gpu_helpers import full_oracle_compare
+    rep = full_oracle_compare(dl, b, cfg)
+    print("full-size parity:", rep)
+    # the selection is non-degenerate: every valid group keeps >= 80% and drops some steps
     keep = dl.keep.cpu().numpy()
-    keep_same, _ = oracle_select_on(dl, b, cfgf)
-    assert np.array_equal(keep, keep_same)
     ok = dl.group_ok.cpu().numpy()
+    L = b.layout
     for g in range(L.G):
         steps = np.arange(L.traj_step_off[g * 8], L.traj_step_off[(g + 1) * 8])
         if ok[g]:
-            assert keep[steps].sum() >= np.ceil(0.8 * len(steps))
-    # sampled rows: per-token values and gradient rows against the oracle
-    A, _ = O.advantages(L.traj_reward, L.traj_group, L.traj_step_off, L.G)
-    s_of_t = O.step_of_token(L.step_tok_off, L.T)
-    tr_of_s = O.traj_of_step(L.traj_step_off, L.S)
-    c_tok_step = None
-    nd = dl.norm_dict()
-    for t in rows:
-        z = b.logits[t].float().cpu().numpy()
-        y = int(b.target[t])
-        lse, logp, H, p = O.token_row(z, y)
-        assert abs(float(dl.lse[t]) - lse) <= 1e-5 * abs(lse) + 1e-6
-        assert abs(float(dl.H[t]) - H) <= 1e-5 * H + 1e-6
-        assert abs(float(dl.logp[t]) - logp) <= 1e-5
-        ell, dell, w, r, clipped, kl = O.token_loss(logp, float(b.logp_old[t]), float(b.logp_rollout[t]),
-                                                    float(b.logp_ref[t]), A[tr_of_s[s_of_t[t]]], cfgf)
-        assert abs(float(dl.ell[t]) - ell) <= 1e-5 * abs(ell) + 2e-6
-        kept = keep[s_of_t[t]]
-        g = (nd["inv_norm"] * dell) if kept else 0.0
-        dz = dl.dlogits[t].float().cpu().numpy()
-        if g == 0.0:
-            assert np.all(dz == 0)
-            continue
-        onehot = np.zeros_like(p)
-        onehot[y] = 1.0
-        dref = g * (onehot - p)
-        dg = nd["inv_norm"] * (1e-5 * abs(dell) + 2e-6)
-        tol = bf16_ulp(dref) + dg * np.abs(onehot - p) + (abs(g) + dg) * P_REL * np.maximum(p, onehot) + abs(g) * 2.0 ** -125 + 1e-38
-        assert np.all(np.abs(dz - dref) <= tol), t
-    # masked rows all zero; every kept row sums to ~0 (softmax gradient)
-    tok_keep = np.repeat(keep, np.diff(L.step_tok_off)).astype(bool)
-    masked = np.nonzero(~tok_keep)[0][:64]
-    assert torch.all(dl.dlogits[torch.as_tensor(masked, device="cuda")] == 0)
-    sums = dl.dlogits[:4096].float().sum(dim=1).abs().cpu().numpy()
-    gs = np.abs(dl.dell[:4096].cpu().numpy()) * nd["inv_norm"]
-    assert np.all(sums <= gs * 0.01 + 1e-30)
-    # loss = sum over kept steps of c * step_ell (fp64, from the GPU's own per-token values)
-    st = dl.stats_dict()
-    ell_all = dl.ell.cpu().numpy().astype(np.float64)
-    L_chk = np.sum(ell_all[tok_keep]) * nd["inv_norm"]
-    assert abs(st["loss"] - L_chk) <= 1e-9 * np.sum(np.abs(ell_all[tok_keep])) * nd["inv_norm"] + 1e-15
+            assert np.ceil(0.8 * len(steps)) <= keep[steps].sum() < len(steps)
 
 
 def test_all_groups_skipped_gives_zero_loss_and_grads():

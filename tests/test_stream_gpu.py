@@ -1,14 +1,20 @@
 """Chunk-streamed pass (batches larger than HBM): forward over all
 chunks -> one selection -> backward over all chunks, with a pool of P logits
-buffers refilled per chunk.  Must reproduce the resident pass bitwise (mask,
-counts, dlogits) and the loss to 1e-12."""
+buffers refilled per chunk.  The streamed results (assembled over chunks and
+ranks) must pass compare() against the float64 oracle, and reproduce the
+resident pass bitwise (mask, counts, dlogits) and its loss to 1e-12."""
 import numpy as np
 import pytest
 import torch
 
 from paper_2509_23866_b200 import dart, synth
 from paper_2509_23866_b200.stream import StreamedPass, chunk_layout
-from tests.gpu_helpers import run_gpu
+from tests.gpu_helpers import Assembled, compare, run_gpu, stream_snapshot
+
+
+def _sample(b, seed, n=16):
+    rng = np.random.default_rng(seed)
+    return sorted(rng.choice(b.layout.T, n, replace=False).tolist())
 
 pytestmark = pytest.mark.gpu
 
@@ -36,6 +42,8 @@ def test_streamed_equals_resident(max_rows, pool):
            consume=consume)
     torch.cuda.synchronize()
     sp.check_status()
+    rows = _sample(b, max_rows)
+    compare(Assembled([stream_snapshot(sp, got, rows)], b.layout), b, cfg, rows=rows)
     assert torch.equal(sp.keep[:b.layout.S], ref.keep[:b.layout.S])
     assert torch.equal(sp.norm, ref.norm)
     assert torch.equal(got, ref.dlogits)
@@ -78,9 +86,10 @@ def _mr_worker(rank, world, port, max_rows, q, name="mid", seed=4):
         sp.check_status()
         q.put((rank, got.view(torch.int16 if gd == torch.bfloat16 else torch.int32).cpu().numpy(),
                sp.keep.cpu().numpy(), sp.norm.cpu().numpy(),
-               sp.stats_dict(), me.tok_begin, me.tok_end, len(sp.chunks)))
+               sp.stats_dict(), me.tok_begin, me.tok_end, len(sp.chunks),
+               stream_snapshot(sp, got, _sample(b, 1) if b.V > 4096 else None)))
     except Exception as e:  # pragma: no cover
-        q.put((rank, repr(e), None, None, None, 0, 0, 0))
+        q.put((rank, repr(e), None, None, None, 0, 0, 0, None))
     finally:
         dist.destroy_process_group()
 
@@ -109,13 +118,15 @@ def test_streamed_two_ranks_equal_resident(max_rows):
     for p in ps:
         p.join(timeout=60)
     L = ref.stats_dict()["loss"]
-    for rank, dz, keep, norm, st, t0, t1, nch in res:
+    for rank, dz, keep, norm, st, t0, t1, nch, snap in res:
         assert keep is not None, dz
         assert np.array_equal(keep[:b.layout.S], ref.keep.cpu().numpy()[:b.layout.S])
         assert np.array_equal(norm, ref.norm.cpu().numpy())
         assert np.array_equal(dz, ref_dz[t0:t1])
         assert abs(st["loss"] - L) <= 1e-12 * abs(L) + 1e-15       # all-reduced on every rank
         assert st["n_kept_tok"] == ref.stats_dict()["n_kept_tok"]
+    rows = _sample(b, 1)
+    compare(Assembled([r[-1] for r in res], b.layout), b, dart.Config(), rows=rows)
 
 
 def test_streamed_more_ranks_than_trajectories():
@@ -142,10 +153,11 @@ def test_streamed_more_ranks_than_trajectories():
     for p in ps:
         p.join(timeout=60)
     L = ref.stats_dict()["loss"]
-    for rank, dz, keep, norm, st, t0, t1, nch in res:
+    for rank, dz, keep, norm, st, t0, t1, nch, snap in res:
         assert keep is not None, dz
         assert np.array_equal(keep[:b.layout.S], ref.keep.cpu().numpy()[:b.layout.S])
         assert np.array_equal(norm, ref.norm.cpu().numpy())
         assert np.array_equal(dz, ref_dz[t0:t1])
         assert abs(st["loss"] - L) <= 1e-12 * abs(L) + 1e-15
+    compare(Assembled([r[-1] for r in res], b.layout, grad_dtype=torch.float32), b, dart.Config(is_cap=2.0))
 

@@ -1,15 +1,16 @@
 """Stand-in for the N > 1 path on one GPU: shard a batch into W trajectory
 ranges, run the three ABI calls per shard with the all-gather emulated by
-concatenation, and require bitwise equality with the unsharded pass (masks,
-counts, per-token values, dlogits) -- the canonical reduction order makes the
-result independent of the distribution -- and the loss to 1e-12."""
+concatenation; the assembled shards must pass compare() against the float64
+oracle, and equal the unsharded pass bitwise (masks, counts, per-token
+values, dlogits) -- the canonical reduction order makes the result
+independent of the distribution -- with the loss to 1e-12."""
 import numpy as np
 import pytest
 import torch
 
 from paper_2509_23866_b200 import dart, synth
 from paper_2509_23866_b200 import dist as D
-from tests.gpu_helpers import run_gpu
+from tests.gpu_helpers import Assembled, compare, run_gpu, snapshot
 
 pytestmark = pytest.mark.gpu
 
@@ -65,3 +66,8 @@ def test_sharded_equals_unsharded(name, W):
         loss += dl.stats_dict()["loss"]
     L = ref.stats_dict()["loss"]
     assert abs(loss - L) <= 1e-12 * max(abs(L), 1e-30) + 1e-15
+    rows = None
+    if b.V > 4096:
+        rows = sorted(np.random.default_rng(W).choice(b.layout.T, 16, replace=False).tolist())
+    compare(Assembled([snapshot(dl, rows) for dl in dls], b.layout, grad_dtype=gd, stats_reduced=False),
+            b, cfg, rows=rows)
