@@ -824,17 +824,23 @@ def run_lmhead(args):
 
 
 def run_lmhead_update(args):
-    """SURVEY §8(f) NEXT #3, training half: the update pass through the LM head
-    with the mask from the (untimed) old-log-prob pass.  One step = per chunk
-    z = h W^T, fused loss + dz, dh = dz W, dW += dz^T h (three tcgen05 GEMMs +
-    the fused sweep).  Timed beside it: cuBLAS (torch.matmul) for the three
-    products with the full [T, V] logits / gradient materialised + the same
-    fused loss kernel."""
+    """SURVEY §8(f) NEXT #3, training half: the update pass through the LM
+    head with the mask from the (untimed) old-log-prob pass.  One step =
+    LmHeadUpdate.run: dart_lmhead_fwd at theta (tcgen05 z + softmax epilogue)
+    -> dart_lmhead_bwd (kept rows gathered, z recomputed on tcgen05, bf16 dz
+    from the TMEM epilogue) -> dh = dz W, dW = dz^T h_kept (cuBLAS, kept rows
+    only).  Timed beside it, in the same process:
+      * the cuBLAS pipeline with the [T, V] logits materialised: torch.matmul
+        bf16 logits -> dart_loss_fused (dz) -> cuBLAS dh, dW over all rows;
+      * the whole LM-head training step at theta = theta_old (one update per
+        batch): ours = forward_lmhead + select + backward_lmhead +
+        the two GEMMs on ONE DartLoss; materialised = cuBLAS logits +
+        DartLoss.run (fwd + select + bwd sweeps) + cuBLAS dh, dW."""
     from paper_2509_23866_b200 import build as B
     B.build()
     world, rank, local = dist_setup(args)
     if world > 1:
-        raise SystemExit("--lmhead --update is single-GPU (chunks are virtual ranks)")
+        raise SystemExit("--lmhead --update is single-GPU")
     from paper_2509_23866_b200 import dart, lmhead, synth
     dev = torch.device("cuda", torch.cuda.current_device())
     layout, V, _, _ = synth.config_layout(args.config, seed=args.seed)
@@ -842,14 +848,14 @@ def run_lmhead_update(args):
     cfg = dart.Config(entropy_q=args.q, beta_kl=args.beta)
     lb = synth.make_lmhead(None, d, seed=args.seed * 1000, device=dev, layout=layout, V=V)
     b = lb.batch
+    T = layout.T
     old = dart.DartLoss(layout, dart.whole_shard(layout), V, cfg, dev, with_grad=False)
     old.forward_lmhead(lb.hidden, lb.weight, b.target, b.logp_old, b.logp_rollout, b.logp_ref)
     old.select()
     torch.cuda.synchronize()
     keep, norm = old.keep.clone(), old.norm.clone()
-    del old
-    up = lmhead.LmHeadUpdate(layout, V, d, cfg, dev, chunk_rows=args.chunk_rows, dw_group=args.dw_group)
-    dh = torch.empty((layout.T, d), dtype=torch.float32, device=dev)
+    up = lmhead.LmHeadUpdate(layout, V, d, cfg, dev, chunk_rows=args.chunk_rows or None)
+    dh = torch.empty((T, d), dtype=torch.float32, device=dev)
     dW = torch.empty((V, d), dtype=torch.float32, device=dev)
     args_in = (lb.hidden, lb.weight, b.target, b.logp_old, b.logp_rollout, b.logp_ref, keep, norm)
     stream = torch.cuda.current_stream()
@@ -874,17 +880,61 @@ def run_lmhead_update(args):
     clocks = clk.stop()
     up.check_status()
     ms = s0.elapsed_time(s1) / args.steps
-    flops = 3 * 2.0 * layout.T * d * V
-    peak_s, peak_b, peak_src = tensor_peak()
-    achieved = flops / (ms * 1e-3) / 1e12
     launches = up.launches // args.steps
+    K = up.last_n_kept
+    # per-kernel pass: events around the tcgen05 forward (dart_lmhead_fwd) and dz (dart_lmhead_bwd) kernels
+    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(args.steps)]
+    for e in ev:
+        for x in e:
+            x.record(stream)
+    torch.cuda.synchronize()
+    for k in range(args.steps):
+        dart.set_timing_events(*ev[k])
+        step()
+    torch.cuda.synchronize()
+    dart.set_timing_events()
+    fwd_ms = statistics.mean(e[0].elapsed_time(e[1]) for e in ev)
+    dz_ms = statistics.mean(e[2].elapsed_time(e[3]) for e in ev)
+    peak_s, peak_b, peak_src = tensor_peak()
+    f_fwd, f_dz = 2.0 * T * d * V, 2.0 * K * d * V
+    flops = f_fwd + 3 * f_dz          # forward + dz recompute + dh + dW
+    traffic = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+            traffic = json.load(f).get("lmhead_dz", {}).get("dram_bytes_per_launch")
+    except Exception:
+        traffic = None
+
+    # ---- theta = theta_old: the whole LM-head training step on one DartLoss (old pass = update forward)
+    full = dart.DartLoss(layout, dart.whole_shard(layout), V, cfg, dev, with_grad=False)
+
+    def whole_step():
+        full.forward_lmhead(lb.hidden, lb.weight, b.target, b.logp_old, b.logp_rollout, b.logp_ref)
+        full.select()
+        full.backward_lmhead(up.dz, up.h_kept, up.kept_rows, up.n_kept)
+        dh.zero_()
+        lmhead.backward_grads(up.dz, up.h_kept, up.kept_rows, up.n_kept, lb.weight, dh, dW)
+    for _ in range(2):
+        whole_step()
+    torch.cuda.synchronize()
+    kk = max(3, min(args.steps, 5))
+    a, c = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record(stream)
+    for _ in range(kk):
+        whole_step()
+    c.record(stream)
+    torch.cuda.synchronize()
+    whole_ms = a.elapsed_time(c) / kk
+    full.check_status()
+    del full
+    torch.cuda.empty_cache()
 
     unfused = None
     if not args.no_unfused:
         try:
-            logits = torch.empty((layout.T, V), dtype=torch.bfloat16, device=dev)
+            logits = torch.empty((T, V), dtype=torch.bfloat16, device=dev)
             dl2 = dart.DartLoss(layout, dart.whole_shard(layout), V, cfg, dev)
-            dh2 = torch.empty((layout.T, d), dtype=torch.bfloat16, device=dev)
+            dh2 = torch.empty((T, d), dtype=torch.bfloat16, device=dev)
             dW2 = torch.empty((V, d), dtype=torch.bfloat16, device=dev)
 
             def ustep():
@@ -892,42 +942,56 @@ def run_lmhead_update(args):
                 g = dl2.fused(logits, b.target, b.logp_old, b.logp_rollout, b.logp_ref, keep=keep, norm=norm)
                 torch.matmul(g, lb.weight, out=dh2)
                 torch.matmul(g.T, lb.hidden, out=dW2)
-            for _ in range(2):
-                ustep()
-            torch.cuda.synchronize()
-            k = max(3, min(args.steps, 5))
-            a, c = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            a.record(stream)
-            for _ in range(k):
-                ustep()
-            c.record(stream)
-            torch.cuda.synchronize()
-            u_ms = a.elapsed_time(c) / k
-            unfused = {"ms_per_step": u_ms, "tokens_per_s": layout.T / (u_ms * 1e-3),
-                       "tflops": flops / (u_ms * 1e-3) / 1e12,
-                       "hbm_bytes_materialised": 2 * layout.T * V * 2, "steps": k,
-                       "what": "torch.matmul (cuBLAS) bf16 logits [T, V] -> dart_loss_fused -> cuBLAS dh, dW"}
+
+            def uwhole():
+                torch.matmul(lb.hidden, lb.weight.T, out=logits)
+                g = dl2.run(logits, b.target, b.logp_old, b.logp_rollout, b.logp_ref)
+                torch.matmul(g, lb.weight, out=dh2)
+                torch.matmul(g.T, lb.hidden, out=dW2)
+            res = {}
+            for name, fn in (("update", ustep), ("whole", uwhole)):
+                for _ in range(2):
+                    fn()
+                torch.cuda.synchronize()
+                a, c = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a.record(stream)
+                for _ in range(kk):
+                    fn()
+                c.record(stream)
+                torch.cuda.synchronize()
+                res[name] = a.elapsed_time(c) / kk
+            unfused = {"ms_per_step": res["update"], "tokens_per_s": T / (res["update"] * 1e-3),
+                       "whole_step_ms": res["whole"], "hbm_bytes_materialised": 2 * T * V * 2, "steps": kk,
+                       "what": "update: torch.matmul (cuBLAS) bf16 logits [T, V] -> dart_loss_fused -> cuBLAS dh, dW; "
+                               "whole: cuBLAS logits -> DartLoss.run (fwd + select + bwd) -> cuBLAS dh, dW"}
             del logits, dl2, dh2, dW2
             torch.cuda.empty_cache()
         except torch.OutOfMemoryError:
             unfused = {"skipped": "out of memory for the [T, V] logits + gradient"}
 
     line = {
-        "metric": "LM-head update pass tokens/s (z = h W^T, fused loss + dz, dh = dz W, dW = dz^T h), "
-                  "V=152064, d=%d" % d,
-        "value": layout.T / (ms * 1e-3), "unit": "tokens/s", "n_gpus": 1, "steps": args.steps,
+        "metric": "LM-head update pass tokens/s (forward at theta, dz from the z-GEMM epilogue, dh = dz W, "
+                  "dW = dz^T h), V=152064, d=%d" % d,
+        "value": T / (ms * 1e-3), "unit": "tokens/s", "n_gpus": 1, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "bf16", "data": "synthetic (seeded; synth.make_lmhead recipe, DESIGN.md §9)",
         "config": {"workload": args.config + " (LM-head update pass: NEXT #3 training half)",
-                   "tokens": layout.T, "V": V, "d": d, "chunk_rows": args.chunk_rows, "chunks": len(up.chunks),
-                   "dw_group": up.dw_group,
-                   "kept_token_frac": float(up.stats_dict()["n_kept_tok"]) / layout.T,
-                   "l2": "inputs larger than L2 (W %.2f GB, hidden %.2f GB, chunk logits %.2f GB)" % (
-                       V * d * 2 / 1e9, layout.T * d * 2 / 1e9, up.rows * V * 4 / 1e9),
+                   "tokens": T, "kept_rows": K, "V": V, "d": d, "chunks": len(up.chunks),
+                   "kept_token_frac": float(up.stats_dict()["n_kept_tok"]) / T,
+                   "l2": "inputs larger than L2 (W %.2f GB, hidden %.2f GB, dz %.2f GB)" % (
+                       V * d * 2 / 1e9, T * d * 2 / 1e9, K * V * 2 / 1e9),
                    "parallelism": "dp1"},
-        "roofline": {"bound": "tensor", "kernel": "3 x gemm (whole step)", "achieved": achieved, "peak": peak_s,
-                     "peak_source": peak_src + " bf16_tflops_sustained", "unit": "TFLOP/s", "frac": achieved / peak_s,
-                     "traffic": None, "algorithmic_flops_per_step": flops},
+        "roofline": {"bound": "tensor", "kernel": "lmhead_kernel<DZ> (z recompute + dz epilogue, kept rows)",
+                     "achieved": f_dz / (dz_ms * 1e-3) / 1e12, "peak": peak_s,
+                     "peak_source": peak_src + " bf16_tflops_sustained (kernel inside a long step loop)",
+                     "unit": "TFLOP/s", "frac": f_dz / (dz_ms * 1e-3) / 1e12 / peak_s, "traffic": traffic,
+                     "traffic_source": "prior ncu capture (profiles/ncu_traffic.json)" if traffic else None,
+                     "algorithmic_flops_per_launch": f_dz, "avg_launch_ms": dz_ms},
+        "kernels": {"lmhead_fwd_ms": fwd_ms, "lmhead_fwd_tflops": f_fwd / (fwd_ms * 1e-3) / 1e12,
+                    "lmhead_dz_ms": dz_ms, "step_tflops": flops / (ms * 1e-3) / 1e12,
+                    "cublas_dh_dW_ms": ms - fwd_ms - dz_ms},
+        "theta_old_whole_step": {"ms": whole_ms, "what": "forward_lmhead + select + backward_lmhead + dh, dW "
+                                                         "(one object: the old pass's forward is the update's)"},
         "unfused_cublas_pipeline": unfused,
         "gpu_launches": launches,
         "clocks": clocks,
@@ -1223,8 +1287,7 @@ def main(argv=None):
     ap.add_argument("--hidden", type=int, default=3584, help="hidden size d for --lmhead (Qwen2.5-7B: 3584)")
     ap.add_argument("--no-unfused", action="store_true", help="--lmhead: skip the cuBLAS + logits comparison")
     ap.add_argument("--update", action="store_true", help="--lmhead: time the update pass (dh, dW) instead")
-    ap.add_argument("--chunk-rows", type=int, default=8192, help="--lmhead --update: rows per chunk")
-    ap.add_argument("--dw-group", type=int, default=1, help="--lmhead --update: chunks per dW GEMM")
+    ap.add_argument("--chunk-rows", type=int, default=0, help="--lmhead --update: rows per chunk (0: whole batch)")
     ap.add_argument("--backend", default="nccl", choices=["nccl", "gloo"],
                     help="gloo: test path (ranks may share a GPU; collectives staged via host)")
     ap.add_argument("--dry-run", action="store_true",

@@ -53,7 +53,7 @@
 extern "C" {
 #endif
 
-#define DART_ABI_VERSION 4
+#define DART_ABI_VERSION 5
 
 typedef enum {
   DART_OK = 0,
@@ -131,6 +131,10 @@ typedef struct {
                                0: masked rows are left untouched                   */
   int32_t ratio_level;    /* dart_ratio_level */
   int32_t kl_mode;        /* dart_kl_mode */
+  int32_t stats_accumulate; /* 0: dart_loss_bwd / dart_loss_fused / dart_lmhead_bwd overwrite *stats;
+                               1: they ADD this call's loss and statistics to *stats (fixed-order fp64
+                               adds in stream order: deterministic) -- a batch streamed as chunks
+                               (virtual ranks) then totals its statistics inside the library */
 } dart_cfg;
 
 /* GLOBAL batch metadata, replicated on every rank (device pointers). */
@@ -281,31 +285,41 @@ size_t dart_lmhead_workspace_size(const dart_lmhead* head, const dart_batch* bat
  * dart_loss_fwd.  Use: the theta_old "old log-prob" pass that produces the
  * token entropies, step entropies and (via dart_select_steps) the step mask
  * for dart_loss_fused.  DART_ERR_UNSUPPORTED for kl_mode == DART_KL_EXACT
- * with beta_kl > 0.  The LM-head backward (dh, dW) is not part of ABI v4. */
+ * with beta_kl > 0.  The backward through the head: dart_lmhead_bwd. */
 dart_status dart_lmhead_fwd(const dart_lmhead* head, const dart_batch* batch, const dart_meta* meta,
                             const dart_cfg* cfg, const dart_fwd_out* out, void* workspace, size_t ws_bytes,
                             void* stream);
 
-/* Plain GEMM step of the LM-head backward:
- *   C[M, N] = A[M, K] * B[N, K]^T   (c_mode STORE_F32 / STORE_BF16)
- *   C[M, N] += A[M, K] * B[N, K]^T  (c_mode ACCUM_F32)
- * bf16 operands, fp32 accumulation on the tensor cores.  Operand storage
- * (device, 16-byte aligned, row pitch in elements, pitch % 8 == 0):
- *   a_mn_major = 0: A is row-major [M, K] (lda >= K); 1: A^T is stored,
- *   row-major [K, M] (lda >= M).  Likewise B: 0 = [N, K], 1 = [K, N].
- * C: device, row-major [M, ldc] of fp32 (STORE_F32, ACCUM_F32) or bf16,
- * 16-byte aligned, ldc >= N, N % 8 == 0, ldc % 8 == 0.  The caller owns C's
- * element type: the library sees only the pointer, so c_mode must match it
- * (the Python binding checks).  Asynchronous on `stream`; no workspace.
- * Kernel choice (results are bit-identical across them for exact operands):
- * 256 x 256 tcgen05 CTA-pair tiles; 4-CTA clusters multicasting the A block
- * to two pairs when N <= 64 * 256 and M >= 1024.  Environment override
- * DART_GEMM_2SM: 0 = 1-CTA 128 x 256 tiles, 1 = pairs only, 2 = 256 x 512
- * pair tiles, 4 = A-multicast clusters, 5 = B-multicast clusters. */
-typedef enum { DART_GEMM_STORE_F32 = 0, DART_GEMM_STORE_BF16 = 1, DART_GEMM_ACCUM_F32 = 2 } dart_gemm_mode;
-dart_status dart_gemm_bf16(const void* A, int32_t a_mn_major, int64_t lda, const void* B, int32_t b_mn_major,
-                           int64_t ldb, void* C, int32_t c_mode, int64_t ldc, int64_t M, int64_t N, int64_t K,
-                           void* stream);
+/* SURVEY §8(f) NEXT #3, training half -- the loss gradient through the LM
+ * head with the logits still never in memory.  Call after dart_lmhead_fwd on
+ * the same head, shard, workspace and `fwd` outputs (the update pass's own
+ * forward at theta; at theta = theta_old it is the old-log-prob pass itself),
+ * with the step mask / normaliser (keep, norm) of dart_select_steps.
+ *   1. *stats: local loss partial and statistics (as dart_loss_bwd).
+ *   2. The KEPT rows of the shard (rows of masked steps have no gradient,
+ *      PAPER.md:256 indicator) are gathered in row order: kept_rows[i] = the
+ *      local row of compact row i, *n_kept = their count K (device scalar),
+ *      hidden_kept row i = hidden row kept_rows[i].
+ *   3. z = hidden_kept W^T is recomputed on the tensor cores tile by tile
+ *      (tcgen05, TMEM accumulators) and the epilogue writes
+ *        dz[i, v] = g_t (delta_{v, y_t} - exp(z_{t,v} invT - lse_t)),
+ *        g_t = c_s dell_t invT          (SURVEY Q11 c_s),
+ *      rounded to bf16 (RNE): dz = dL/dz of the kept rows.
+ * The model's backward through the head is then two plain GEMMs the caller
+ * runs (e.g. cuBLAS): dL/dh[kept_rows] = dz W, dL/dW = dz^T hidden_kept; all
+ * other rows of dL/dh are zero.
+ * Buffers (device, caller-owned, sized for T_loc rows since K is known on the
+ * device only): dz [T_loc, ldg] bf16 with ldg >= V, ldg % 8 == 0;
+ * hidden_kept [T_loc, ld_hk] bf16 with ld_hk >= d, ld_hk % 8 == 0; kept_rows
+ * int32 [T_loc]; n_kept int64 [1]; all 16-byte aligned.  Rows >= K of dz /
+ * hidden_kept / kept_rows are left untouched.  Workspace: the
+ * dart_lmhead_workspace_size buffer of the forward (its per-row state is
+ * read).  Same errors as dart_lmhead_fwd. */
+dart_status dart_lmhead_bwd(const dart_lmhead* head, const dart_batch* batch, const dart_meta* meta,
+                            const dart_cfg* cfg, const dart_fwd_out* fwd, const uint8_t* keep,
+                            const dart_norm* norm, void* dz, int64_t ldg, void* hidden_kept, int64_t ld_hk,
+                            int32_t* kept_rows, int64_t* n_kept, dart_stats* stats, void* workspace,
+                            size_t ws_bytes, void* stream);
 
 /* Single-rank convenience: fwd + select (world = 1) + bwd on one stream. */
 dart_status dart_loss_pass(const dart_batch* batch, const dart_meta* meta, const dart_cfg* cfg,

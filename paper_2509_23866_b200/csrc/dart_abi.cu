@@ -112,6 +112,7 @@ bool cfg_ok(const dart_cfg* c) {
   if (c->select_rule < DART_SEL_FLOOR || c->select_rule > DART_SEL_OFF) return false;
   if (c->ratio_level != DART_RATIO_TOKEN && c->ratio_level != DART_RATIO_STEP) return false;
   if (c->kl_mode != DART_KL_K3 && c->kl_mode != DART_KL_EXACT) return false;
+  if (c->stats_accumulate != 0 && c->stats_accumulate != 1) return false;
   return true;
 }
 
@@ -169,17 +170,6 @@ dart_status cuda_status(cudaError_t e) {
 // log2 of the number of warps a row is split over: only for few rows, and
 // only when every canonical segment is non-empty (rows >= KSEG chunks)
 inline bool exact_kl(const dart_cfg* c) { return c->kl_mode == DART_KL_EXACT && c->beta_kl > 0.f; }
-
-// dart_loss_fused kernel (env DART_FUSED_VARIANT):
-//   2 (default) L2 re-read kernel with rows split over a 2-CTA cluster: the
-//     pass-2 re-read hits L2 (DRAM reads 15.4 GB = algorithmic), 8.9 M tokens/s
-//   0 the same kernel, one CTA per row (20.6 GB read, 8.9 M tokens/s)
-//   1 cluster / distributed-shared-memory true single read (5.9 M tokens/s:
-//     per-row exchange and lock-stepped phases starve MUFU)
-int fused_variant() {
-  const char* e = getenv("DART_FUSED_VARIANT");
-  return (e && (e[0] == '0' || e[0] == '1')) ? e[0] - '0' : 2;
-}
 
 int choose_lg_nsplit(const dart_batch* b, const WsLayout& L, int64_t nvec) {
   if (!L.split_alloc || nvec < (int64_t)KSEG * FCH_VEC) return 0;
@@ -396,7 +386,7 @@ dart_status dart_lmhead_fwd(const dart_lmhead* h, const dart_batch* b, const dar
   DART_TRY(launch_tok_meta(tp, s));
 
   if (b->T_loc > 0) {
-    LmParams lp;
+    LmParams lp = {};
     lp.T_loc = b->T_loc; lp.V = b->V; lp.K = (int)h->d;
     lp.n_mb = LL.n_mb; lp.n_nt = LL.n_nt; lp.n_nc = LL.n_nc;
     lp.nt_per_chunk = LM_NT_PER_CHUNK; lp.group_nc = LM_GROUP_NC;
@@ -444,6 +434,77 @@ dart_status dart_lmhead_fwd(const dart_lmhead* h, const dart_batch* b, const dar
     sp.step_entropy = o->step_entropy; sp.step_ell = o->step_ell;
     sp.step_stats = at<double>(ws, L.step_stats);
     DART_TRY(launch_step_reduce(sp, s));
+  }
+  g_last_launches = g_launches;
+  return DART_OK;
+}
+
+dart_status dart_lmhead_bwd(const dart_lmhead* h, const dart_batch* b, const dart_meta* m, const dart_cfg* c,
+                            const dart_fwd_out* f, const uint8_t* keep, const dart_norm* norm, void* dz, int64_t ldg,
+                            void* hidden_kept, int64_t ld_hk, int32_t* kept_rows, int64_t* n_kept, dart_stats* stats,
+                            void* ws, size_t ws_bytes, void* stream) {
+  dart_status st = lmhead_check(h, b, m, c);
+  if (st != DART_OK) return st;
+  if ((st = fwd_out_check(b, m, f)) != DART_OK) return st;
+  if (!norm || !stats || !n_kept || (m->S > 0 && !keep)) return DART_ERR_INVALID_ARG;
+  if (b->T_loc > 0) {
+    if (!dz || !hidden_kept || !kept_rows || !aligned16(dz) || !aligned16(hidden_kept)) return DART_ERR_INVALID_ARG;
+    if (ldg < b->V || ldg % 8 != 0 || ld_hk < h->d || ld_hk % 8 != 0) return DART_ERR_INVALID_ARG;
+  }
+  const WsLayout L = ws_layout(b, m);
+  const LmLayout LL = lm_layout(b, m);
+  if (!ws || ws_bytes < LL.total) return DART_ERR_WORKSPACE;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  g_launches = 0;
+
+  // K6 with unit costs: step_cost = exclusive prefix of kept tokens per local step
+  BwdPrepParams pp = {};
+  pp.T_loc = b->T_loc; pp.tok_begin = b->tok_begin; pp.step_begin = b->step_begin; pp.S_loc = b->S_loc;
+  pp.nch = 1; pp.norm_mode = c->norm_mode; pp.zero_fill = 0; pp.ratio_level = c->ratio_level;
+  pp.kept_cost = 1;
+  pp.step_tok_off = m->step_tok_off; pp.keep = keep; pp.norm = norm;
+  pp.step_ell = f->step_ell; pp.step_stats = at<double>(ws, L.step_stats);
+  pp.step_scale = at<double>(ws, L.step_scale);
+  pp.step_cost = at<int64_t>(ws, L.step_cost);
+  pp.step_chunk = at<int64_t>(ws, L.step_chunk);
+  pp.stats = stats;
+  pp.no_stats = 0;
+  pp.accumulate = c->stats_accumulate ? 1 : 0;
+  DART_TRY(launch_bwd_prep(pp, s));
+
+  LmGatherParams gp;
+  gp.T_loc = b->T_loc; gp.V = b->V; gp.d = h->d; gp.ld_h = h->ld_h; gp.ld_hk = ld_hk;
+  gp.tok_begin = b->tok_begin; gp.step_begin = b->step_begin; gp.S_loc = b->S_loc;
+  gp.tok_step = at<int32_t>(ws, L.tok_step);
+  gp.step_tok_off = m->step_tok_off;
+  gp.keep = keep;
+  gp.kept_off = pp.step_cost;
+  gp.step_scale = pp.step_scale;
+  gp.dell = f->dell;
+  gp.lse2 = at<float>(ws, L.lse2);
+  gp.target = b->target;
+  gp.invT = (double)c->inv_temperature;
+  gp.hidden = static_cast<const uint8_t*>(h->hidden);
+  gp.hidden_kept = static_cast<uint8_t*>(hidden_kept);
+  gp.rec = at<int4>(ws, L.rec);
+  gp.kept_rows = kept_rows;
+  gp.n_kept = n_kept;
+  DART_TRY(launch_lmhead_gather(gp, s));
+
+  if (b->T_loc > 0) {
+    LmParams lp = {};
+    lp.T_loc = b->T_loc; lp.V = b->V; lp.K = (int)h->d;
+    lp.n_mb = LL.n_mb; lp.n_nt = LL.n_nt; lp.n_nc = LL.n_nc;
+    lp.nt_per_chunk = LM_NT_PER_CHUNK; lp.group_nc = LM_GROUP_NC;
+    lp.n_items = (int64_t)LL.n_mb * LL.n_nc;
+    lp.c2 = (float)((double)c->inv_temperature * LOG2E_D);
+    lp.DZ_n_kept = n_kept;
+    lp.DZ_rec = gp.rec;
+    lp.DZ_out = static_cast<uint8_t*>(dz);
+    lp.DZ_ldg_bytes = ldg * 2;
+    rec(2, s);
+    DART_TRY(launch_lmhead(hidden_kept, ld_hk, h->weight, h->ld_w, lp, sm_count(), s));
+    rec(3, s);
   }
   g_last_launches = g_launches;
   return DART_OK;
@@ -516,7 +577,7 @@ dart_status dart_loss_bwd(const dart_batch* b, const dart_meta* m, const dart_cf
   const int64_t chv = kx ? CH_VEC / 2 : BCH_VEC;           // exact KL: 2 KB of z + 2 KB of z_ref per slot
   const int64_t nch = (nvec + chv - 1) / chv;
 
-  BwdPrepParams pp;
+  BwdPrepParams pp = {};
   pp.T_loc = b->T_loc; pp.tok_begin = b->tok_begin; pp.step_begin = b->step_begin; pp.S_loc = b->S_loc;
   pp.nch = nch; pp.norm_mode = c->norm_mode; pp.zero_fill = c->zero_fill_masked ? 1 : 0;
   pp.ratio_level = c->ratio_level;
@@ -528,6 +589,7 @@ dart_status dart_loss_bwd(const dart_batch* b, const dart_meta* m, const dart_cf
   pp.step_chunk = at<int64_t>(ws, L.step_chunk);
   pp.stats = stats;
   pp.no_stats = 0;
+  pp.accumulate = c->stats_accumulate ? 1 : 0;
   DART_TRY(launch_bwd_prep(pp, s));
 
   if (b->T_loc > 0 && !loss_only) {
@@ -614,7 +676,7 @@ dart_status dart_loss_fused(const dart_batch* b, const dart_meta* m, const dart_
   tp.status = o->status;
   DART_TRY(launch_tok_meta(tp, s));
 
-  BwdPrepParams pp;   // per-step loss weights + chunk-cost prefix (the mask is known)
+  BwdPrepParams pp = {};   // per-step loss weights + chunk-cost prefix (the mask is known)
   pp.T_loc = b->T_loc; pp.tok_begin = b->tok_begin; pp.step_begin = b->step_begin; pp.S_loc = b->S_loc;
   pp.nch = nch; pp.norm_mode = c->norm_mode; pp.zero_fill = c->zero_fill_masked ? 1 : 0;
   pp.ratio_level = c->ratio_level;
@@ -626,10 +688,11 @@ dart_status dart_loss_fused(const dart_batch* b, const dart_meta* m, const dart_
   pp.step_chunk = at<int64_t>(ws, L.step_chunk);
   pp.stats = stats;
   pp.no_stats = b->T_loc > 0 ? 1 : 0;   // the step sums come from the sweep below; stats in the second call
+  pp.accumulate = c->stats_accumulate ? 1 : 0;
   DART_TRY(launch_bwd_prep(pp, s));
 
   if (b->T_loc > 0) {
-    FusedParams fp;
+    FusedParams fp = {};
     fp.logits = static_cast<const uint8_t*>(b->logits);
     fp.ld_bytes = b->ld * (int64_t)es;
     fp.V = b->V; fp.T_loc = b->T_loc; fp.nvec = nvec; fp.nch = nch;
@@ -648,15 +711,11 @@ dart_status dart_loss_fused(const dart_batch* b, const dart_meta* m, const dart_
     fp.aux_flags = at<uint8_t>(ws, L.aux_flags);
     fp.status = o->status;
     fp.rec = at<uint8_t>(ws, L.fused_rec);
-    fp.dbg = nullptr;
-    if (const char* d = getenv("DART_FC_DBG")) fp.dbg = reinterpret_cast<unsigned long long*>(strtoull(d, nullptr, 0));
     DART_TRY(launch_fused_rec(fp, s));
     rec(2, s);
-    const int fv = fused_variant();
-    if (fused_cluster_ok(fp) && fv == 1)
-      DART_TRY(launch_fused_cluster(fp, grad_dtype == DART_BF16, sm_count(), s));
-    else
-      DART_TRY(launch_fused_sweep(fp, fp.is_bf16, grad_dtype == DART_BF16, sm_count(), fv == 2 && fp.nch >= 2, s));
+    // rows split over a 2-CTA cluster (the pass-2 re-read then hits L2); one CTA per
+    // row for rows of a single chunk
+    DART_TRY(launch_fused_sweep(fp, fp.is_bf16, grad_dtype == DART_BF16, sm_count(), fp.nch >= 2, s));
     rec(3, s);
 
     StepReduceParams sp;
@@ -674,22 +733,6 @@ dart_status dart_loss_fused(const dart_batch* b, const dart_meta* m, const dart_
     pp.no_stats = 0;
     DART_TRY(launch_bwd_prep(pp, s));   // loss partial + statistics from the step sums
   }
-  g_last_launches = g_launches;
-  return DART_OK;
-}
-
-dart_status dart_gemm_bf16(const void* A, int32_t a_mn, int64_t lda, const void* B, int32_t b_mn, int64_t ldb,
-                           void* C, int32_t c_mode, int64_t ldc, int64_t M, int64_t N, int64_t K, void* stream) {
-  if (c_mode != DART_GEMM_STORE_F32 && c_mode != DART_GEMM_STORE_BF16 && c_mode != DART_GEMM_ACCUM_F32)
-    return DART_ERR_UNSUPPORTED;
-  const int64_t lim = (int64_t)1 << 31;
-  if (M < 1 || N < 1 || K < 1 || M >= lim || N >= lim || K >= lim) return DART_ERR_INVALID_ARG;
-  if (!A || !B || !C || !aligned16(A) || !aligned16(B) || !aligned16(C)) return DART_ERR_INVALID_ARG;
-  if (lda % 8 != 0 || ldb % 8 != 0 || ldc % 8 != 0 || N % 8 != 0 || ldc < N) return DART_ERR_INVALID_ARG;
-  if (lda < (a_mn ? M : K) || ldb < (b_mn ? N : K)) return DART_ERR_INVALID_ARG;
-  g_launches = 0;
-  DART_TRY(launch_gemm_bf16(A, a_mn != 0, lda, B, b_mn != 0, ldb, C, c_mode, ldc, M, N, K, sm_count(),
-                            static_cast<cudaStream_t>(stream)));
   g_last_launches = g_launches;
   return DART_OK;
 }

@@ -15,9 +15,6 @@
 #include "dart_common.cuh"
 #include "dart_internal.h"
 
-#ifndef DART_BWD_STYLE
-#define DART_BWD_STYLE 1
-#endif
 
 namespace dart {
 
@@ -122,18 +119,11 @@ __global__ void __launch_bounds__(1024) bwd_prep_kernel(BwdPrepParams p) {
     __syncthreads();
   }
   if (tid == 0 && !p.no_stats) {
-    dart_stats* o = reinterpret_cast<dart_stats*>(p.stats);
-    o->loss = tot[0];
-    o->n_tok = tot[1];
-    o->n_kept_tok = tot[2];
-    o->n_kept_step = tot[3];
-    o->sum_clip = tot[4];
-    o->sum_trunc = tot[5];
-    o->sum_w = tot[6];
-    o->sum_adv = tot[7];
-    o->sum_adv2 = tot[8];
-    o->sum_H = tot[9];
-    o->sum_kl = tot[10];
+    // dart_stats is NV doubles in field order (loss, n_tok, n_kept_tok, n_kept_step, sum_clip,
+    // sum_trunc, sum_w, sum_adv, sum_adv2, sum_H, sum_kl)
+    double* o = reinterpret_cast<double*>(p.stats);
+#pragma unroll
+    for (int i = 0; i < NV; ++i) o[i] = p.accumulate ? o[i] + tot[i] : tot[i];
   }
 }
 
@@ -309,84 +299,28 @@ __device__ __forceinline__ void bwd_issue(OCur& pc, const BwdParams& p, uint64_t
   ocur_to_kept(pc, p, WARPS);
 }
 
-#ifndef DART_BWD_MINB
-#define DART_BWD_MINB 1
-#endif
-// DART_BWD_FULL=1 takes an unpredicated path for full chunks: fewer
-// instructions, but measured 14% SLOWER on B200 (6.17 vs 5.41 ms, store
-// drain stalls: long_scoreboard on STG source registers + lg_throttle), so
-// the per-vector guarded path is the default.
-#ifndef DART_BWD_FULL
-#define DART_BWD_FULL 0
-#endif
-// DART_BWD_TMAST=1: bf16 -> bf16 full chunks are written by one bulk
-// shared->global copy per 4 KB chunk (TMA store, SASS UBLKCP) from a per-warp
-// double-buffered staging area instead of 8 STG.128 per lane; masked chunks
-// are bulk-stored from a zero page.  Correct (parity + racecheck/memcheck
-// clean) but measured SLOWER on B200: bwd sweep 6.16 vs 5.48 ms (84.6% vs
-// 95.1% of the copy peak) -- the staging STS + proxy fence + bulk-group waits
-// cost more than the streaming STG.128 they replace.  Off by default.
-#ifndef DART_BWD_TMAST
-#define DART_BWD_TMAST 0
-#endif
-// DART_BWD_V8=1: bf16 -> bf16 full chunks (all 256 vectors inside the row, no
-// tail) run without per-vector guards and each lane owns PAIRS of adjacent
-// 16-byte input vectors, so its 16 gradients leave in one 32-byte store
-// (st.global.v8.b32, SASS STG.E.256): 31% fewer instructions than the guarded
-// STG.128 path (1.68e9 vs 2.43e9 per launch, ncu) -- and SLOWER on B200:
-// 6.07 vs 5.35 ms isolated.  ncu: 26% of warp stalls become long_scoreboard
-// on the STG.256 source registers (ptxas reuses them for the next pair's
-// unpack right after the store, so each warp waits for the LSU to drain its
-// 1 KB store).  =2 spreads the stores (one opaque uniform branch per pair):
-// 6.07 ms, same.  DART_BWD_FULL=2 (STG.128, no per-lane guards, spread the
-// same way): 6.2 ms.  The guarded path stays the default.  Needs 32-byte
-// aligned gradient rows (checked per launch).
-#ifndef DART_BWD_V8
-#define DART_BWD_V8 0
-#endif
-__device__ __forceinline__ void stg256_cs(void* p, uint4 a, uint4 b) {
-  asm volatile("st.global.cs.v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(p), "r"(a.x), "r"(a.y), "r"(a.z),
-               "r"(a.w), "r"(b.x), "r"(b.y), "r"(b.z), "r"(b.w)
-               : "memory");
-}
-__device__ __forceinline__ void bulk_s2g(void* gdst, const void* ssrc, uint32_t bytes) {
-  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(gdst), "r"(smem_u32(ssrc)),
-               "r"(bytes)
-               : "memory");
-}
-__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
-template <int N>
-__device__ __forceinline__ void bulk_wait_read() { asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory"); }
-__device__ __forceinline__ void sts128(void* p, uint4 v) {
-  asm volatile("st.shared.v4.u32 [%0], {%1,%2,%3,%4};" ::"r"(smem_u32(p)), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w)
-               : "memory");
-}
+// The sweep's code shape is part of its performance: every
+// 16-byte input vector's gradient is computed and stored inside its own
+// guarded region, so the eight 128-bit stores of a chunk leave interleaved
+// with the math (an unguarded loop bursts them and stalls on the store queue;
+// wider 32-byte stores and TMA bulk stores from shared memory were both
+// measured slower).  Per vector the only bookkeeping is one compare against
+// the chunk's vector count and an immediate store offset from the lane's
+// first output vector; vocabulary tails (V % EPV != 0) take a generic path.
 template <typename Tin, typename Tout, int WARPS, int STAGES>
-__global__ void __launch_bounds__(WARPS * 32, DART_BWD_MINB)
+__global__ void __launch_bounds__(WARPS * 32, 1)
 bwd_sweep_kernel(const BwdParams p) {
   extern __shared__ __align__(128) uint8_t smem[];
   constexpr int EPV = 16 / sizeof(Tin);       // logits per 16-byte input vector
   constexpr bool OUT_BF16 = sizeof(Tout) == 2;
+  constexpr int OUTV = EPV * (int)sizeof(Tout);   // output bytes per input vector
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   uint8_t* ring = smem + (size_t)warp * STAGES * BCH_BYTES;
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + (size_t)WARPS * STAGES * BCH_BYTES) + warp * STAGES;
-  constexpr bool TMAST = DART_BWD_TMAST && sizeof(Tin) == 2 && sizeof(Tout) == 2;
-  constexpr bool V8T = DART_BWD_V8 && !DART_BWD_TMAST && sizeof(Tin) == 2 && sizeof(Tout) == 2;
-  const bool v8_ok = V8T && ((p.ldg_bytes & 31) == 0) && ((reinterpret_cast<uintptr_t>(p.dlogits) & 31) == 0);
-  // TMA-store staging: [WARPS][2][BCH_BYTES] then one zero page (after the barriers, 1 KB aligned)
-  uint8_t* stage_base = smem + (((size_t)WARPS * STAGES * BCH_BYTES + (size_t)WARPS * STAGES * 8 + 1023) & ~(size_t)1023);
-  uint8_t* stg_buf = stage_base + (size_t)warp * 2 * BCH_BYTES;
-  uint8_t* zero_page = stage_base + (size_t)WARPS * 2 * BCH_BYTES;
-  int sbuf = 0;
   if (lane == 0) {
 #pragma unroll
     for (int s = 0; s < STAGES; ++s) mbar_init(&bars[s], 1);
     fence_mbar_init();
-  }
-  if (TMAST) {
-    for (int i = threadIdx.x; i < BCH_BYTES / 16; i += blockDim.x) sts128(zero_page + i * 16, make_uint4(0u, 0u, 0u, 0u));
-    fence_proxy_async_smem();
-    __syncthreads();
   }
   __syncwarp();
 
@@ -416,7 +350,6 @@ bwd_sweep_kernel(const BwdParams p) {
   int64_t cur_t = -1, pre_t = -1;
   const int64_t nvec = p.nvec, T_loc = p.T_loc, ldg_bytes = p.ldg_bytes;
   uint8_t* const dlog = p.dlogits;
-  constexpr int64_t OUTV = EPV * (int64_t)sizeof(Tout);   // output bytes per input vector
   int4 cur = make_int4(0, 0, -1, 0), pre = make_int4(0, 0, -1, 0);
 
 #pragma unroll 1
@@ -424,11 +357,9 @@ bwd_sweep_kernel(const BwdParams p) {
     const int64_t t = cc.t;
     const int64_t v0 = (int64_t)cc.c * BCH_VEC;
     const int nv = (int)min((int64_t)BCH_VEC, nvec - v0);
-    // full chunk: all lanes hold BVPL complete vectors (no tail, no predicates)
-    const bool full8 = v8_ok && (nv == BCH_VEC) && !(tail_elems && v0 + nv == nvec);
-    const bool full = !full8 && DART_BWD_FULL && (nv == BCH_VEC) && !(tail_elems && v0 + nv == nvec);
-    uint8_t* orow = dlog + t * ldg_bytes;
-    uint8_t* olane = orow + (v0 + lane) * OUTV;    // this lane's first output vector
+    const bool tailc = tail_elems && v0 + nv == nvec;     // the row's last, partial vector is in this chunk
+    uint8_t* const orow = dlog + t * ldg_bytes;
+    uint8_t* const olane = orow + (v0 + lane) * OUTV;     // this lane's first output vector
     if (cc.kept) {
       if (t != cur_t) {
         cur = (t == pre_t) ? pre : rec[t];
@@ -444,120 +375,36 @@ bwd_sweep_kernel(const BwdParams p) {
       const uint8_t* sp = ring + (size_t)slot * BCH_BYTES;
       const float2 cc2 = make_float2(c2, c2), nl = make_float2(nl2, nl2), ng = make_float2(-g, -g);
       uint4 x[BVPL];
-      if (V8T && full8) {       // lane owns vector pairs (lane + 32 k): 32 contiguous bytes each
 #pragma unroll
-        for (int k = 0; k < BVPL / 2; ++k) {
-          x[2 * k] = lds128(sp + (lane + 32 * k) * 32);
-          x[2 * k + 1] = lds128(sp + (lane + 32 * k) * 32 + 16);
-        }
-      } else if (full) {
-#pragma unroll
-        for (int k = 0; k < BVPL; ++k) x[k] = lds128(sp + (lane + 32 * k) * 16);
-      } else {
-#pragma unroll
-        for (int k = 0; k < BVPL; ++k) {
-          const int vi = lane + 32 * k;
-          x[k] = (vi < nv) ? lds128(sp + vi * 16) : make_uint4(0u, 0u, 0u, 0u);
-        }
-      }
-      // consume every loaded word before the slot is handed back to the copy
-      // engine (read-then-async-write: the reads have completed)
+      for (int k = 0; k < BVPL; ++k) x[k] = lds128(sp + (lane + 32 * k) * 16);   // past nv: unused
+      // every LDS has landed in registers before the slot goes back to the copy
+      // engine (read-then-async-write; one register per LDS.128 is enough)
       uint32_t dep = 0;
 #pragma unroll
-      for (int k = 0; k < BVPL; ++k) dep |= x[k].x | x[k].y | x[k].z | x[k].w;
+      for (int k = 0; k < BVPL; ++k) dep ^= x[k].x;
       asm volatile("" ::"r"(dep));
       __syncwarp();
       if (pc.valid) bwd_issue<Tin, WARPS, STAGES>(pc, p, bars, ring, slot, lane, pol);
       if (++slot == STAGES) { slot = 0; phase ^= 1u; }
-      if (V8T && full8) {
-#pragma unroll
-        for (int k = 0; k < BVPL / 2; ++k) {
-          float o[16];
-#if DART_BWD_V8 == 2
-          // always true on a full chunk, but opaque to the compiler: one branch
-          // region per pair keeps each pair's stores next to its math
-          if ((nv >> 6) <= k) break;
-#endif
-          grad_vec<Tin>(x[2 * k], cc2, nl, ng, o);
-          grad_vec<Tin>(x[2 * k + 1], cc2, nl, ng, o + 8);
-          stg256_cs(orow + (v0 + 2 * (lane + 32 * k)) * 16,
-                    make_uint4(pack_bf16x2(o[0], o[1]), pack_bf16x2(o[2], o[3]), pack_bf16x2(o[4], o[5]),
-                               pack_bf16x2(o[6], o[7])),
-                    make_uint4(pack_bf16x2(o[8], o[9]), pack_bf16x2(o[10], o[11]), pack_bf16x2(o[12], o[13]),
-                               pack_bf16x2(o[14], o[15])));
-        }
-        if (y >= 0) {           // target element g (1 - p_y), after its pair's store (same thread)
-          const int64_t yv = y / EPV;
-          if (yv >= v0 && yv < v0 + BCH_VEC && lane == (int)(((yv - v0) >> 1) & 31)) {
-            const float py = ex2(fmaf(zy, c2, nl2));
-            reinterpret_cast<__nv_bfloat16*>(orow)[y] = __float2bfloat16_rn(fmaf(-g, py, g));
-          }
-        }
-        ocur_advance(cc, p, WARPS);
-        continue;
-      }
-      if (TMAST && nv == BCH_VEC && !(tail_elems && v0 + nv == nvec)) {
-        // gradient of the chunk into this warp's staging buffer, then one bulk store
-        if (lane == 0) bulk_wait_read<1>();         // the buffer's previous bulk store has read it
-        __syncwarp();
-        uint8_t* sb = stg_buf + (size_t)sbuf * BCH_BYTES;
+      if (!tailc) {
 #pragma unroll
         for (int k = 0; k < BVPL; ++k) {
-          float o[EPV];
-          grad_vec<Tin>(x[k], cc2, nl, ng, o);
-          sts128(sb + (lane + 32 * k) * 16, make_uint4(pack_bf16x2(o[0], o[1]), pack_bf16x2(o[2], o[3]),
-                                                       pack_bf16x2(o[4], o[5]), pack_bf16x2(o[6], o[7])));
-        }
-        if (y >= 0) {                               // target element: g (1 - p_y)
-          const int64_t yv = y / EPV;
-          if (yv >= v0 && yv < v0 + nv && lane == (int)((yv - v0) & 31)) {
-            const float py = ex2(fmaf(zy, c2, nl2));
-            reinterpret_cast<__nv_bfloat16*>(sb)[y - v0 * EPV] = __float2bfloat16_rn(fmaf(-g, py, g));
+          if (lane + 32 * k < nv) {   // keeps each vector's math and store together (see above)
+            float o[EPV];
+            grad_vec<Tin>(x[k], cc2, nl, ng, o);
+            store_full<Tout, EPV>(olane + k * 32 * OUTV, o);
           }
-        }
-        fence_proxy_async_smem();                   // generic-proxy smem writes -> visible to the bulk copy
-        __syncwarp();
-        if (lane == 0) {
-          bulk_s2g(orow + v0 * OUTV, sb, (uint32_t)BCH_BYTES);
-          bulk_commit();
-        }
-        sbuf ^= 1;
-        ocur_advance(cc, p, WARPS);
-        continue;
-      }
-      if (full) {
-#pragma unroll
-        for (int k = 0; k < BVPL; ++k) {
-#if DART_BWD_FULL == 2
-          if ((nv >> 5) <= k) break;   // always true here; one branch region per vector (spreads the stores)
-#endif
-#if DART_BWD_STYLE == 1
-          if (lane + 32 * k < nv) {   // always true here: keeps compute/store of each vector together
-#endif
-          float o[EPV];
-#if DART_BWD_STYLE == 2
-          if (k > 0) {  // order: store(k-1) before the math of vector k (spreads the stores)
-            asm volatile("" : "+r"(x[k].x), "+r"(x[k].y), "+r"(x[k].z), "+r"(x[k].w));
-          }
-#endif
-          grad_vec<Tin>(x[k], cc2, nl, ng, o);
-          store_full<Tout, EPV>(olane + k * 32 * OUTV, o);
-#if DART_BWD_STYLE == 1
-          }
-#endif
         }
       } else {
 #pragma unroll
         for (int k = 0; k < BVPL; ++k) {
           const int vi = lane + 32 * k;
           if (vi < nv) {
-            const int64_t gv = v0 + vi;
             float o[EPV];
             grad_vec<Tin>(x[k], cc2, nl, ng, o);
-            const int nvalid = (tail_elems && gv == nvec - 1) ? tail_elems : EPV;
-            uint8_t* dst = orow + gv * OUTV;
-            if (OUT_BF16) store_vals_bf16(dst, o, nvalid, EPV);
-            else store_vals_f32(dst, o, nvalid, EPV);
+            const int nvalid = (vi == nv - 1) ? tail_elems : EPV;
+            if (OUT_BF16) store_vals_bf16(olane + k * 32 * OUTV, o, nvalid, EPV);
+            else store_vals_f32(olane + k * 32 * OUTV, o, nvalid, EPV);
           }
         }
       }
@@ -573,45 +420,22 @@ bwd_sweep_kernel(const BwdParams p) {
       }
     } else {
       // masked step: zeros, no read
-      if (V8T && full8) {
-        const uint4 zz = make_uint4(0u, 0u, 0u, 0u);
-#pragma unroll
-        for (int k = 0; k < BVPL / 2; ++k) stg256_cs(orow + (v0 + 2 * (lane + 32 * k)) * 16, zz, zz);
-        ocur_advance(cc, p, WARPS);
-        continue;
-      }
-      if (TMAST && nv == BCH_VEC && !(tail_elems && v0 + nv == nvec)) {
-        if (lane == 0) {
-          bulk_s2g(orow + v0 * OUTV, zero_page, (uint32_t)BCH_BYTES);
-          bulk_commit();
-        }
-        ocur_advance(cc, p, WARPS);
-        continue;
-      }
       float o[EPV];
 #pragma unroll
       for (int e = 0; e < EPV; ++e) o[e] = 0.f;
-      if (full) {
 #pragma unroll
-        for (int k = 0; k < BVPL; ++k) store_full<Tout, EPV>(olane + k * 32 * OUTV, o);
-      } else {
-#pragma unroll
-        for (int k = 0; k < BVPL; ++k) {
-          const int vi = lane + 32 * k;
-          if (vi < nv) {
-            const int64_t gv = v0 + vi;
-            const int nvalid = (tail_elems && gv == nvec - 1) ? tail_elems : EPV;
-            uint8_t* dst = orow + gv * OUTV;
-            if (OUT_BF16) store_vals_bf16(dst, o, nvalid, EPV);
-            else store_vals_f32(dst, o, nvalid, EPV);
-          }
+      for (int k = 0; k < BVPL; ++k) {
+        const int vi = lane + 32 * k;
+        if (vi < nv) {
+          const int nvalid = (tailc && vi == nv - 1) ? tail_elems : EPV;
+          if (nvalid == EPV) store_full<Tout, EPV>(olane + k * 32 * OUTV, o);
+          else if (OUT_BF16) store_vals_bf16(olane + k * 32 * OUTV, o, nvalid, EPV);
+          else store_vals_f32(olane + k * 32 * OUTV, o, nvalid, EPV);
         }
       }
     }
     ocur_advance(cc, p, WARPS);
   }
-  if (TMAST && lane == 0) bulk_wait_read<0>();     // smem must outlive the last bulk stores' reads
-  if (TMAST) __syncthreads();
 }
 
 // ============================================================== launchers
@@ -630,9 +454,7 @@ cudaError_t launch_rowrec(const RowRecParams& p, cudaStream_t st) {
 
 template <typename Tin, typename Tout, int WARPS, int STAGES>
 static cudaError_t launch_bwd_t(const BwdParams& p, int num_sms, cudaStream_t st) {
-  constexpr bool TMAST = DART_BWD_TMAST && sizeof(Tin) == 2 && sizeof(Tout) == 2;
-  size_t smem = (size_t)WARPS * STAGES * BCH_BYTES + (size_t)WARPS * STAGES * 8;
-  if (TMAST) smem = ((smem + 1023) & ~(size_t)1023) + (size_t)WARPS * 2 * BCH_BYTES + BCH_BYTES + 1024;
+  const size_t smem = (size_t)WARPS * STAGES * BCH_BYTES + (size_t)WARPS * STAGES * 8;
   auto kern = bwd_sweep_kernel<Tin, Tout, WARPS, STAGES>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;

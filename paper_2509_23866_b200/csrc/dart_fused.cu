@@ -35,12 +35,6 @@ namespace dart {
 // two CTAs per SM (each 8 consumer warps + 1 producer, 96 KB ring): while one
 // CTA sits in its row barrier / epilogue / L2-fed pass 2, the other streams
 // its next row from HBM
-#ifndef DART_FU_REV
-#define DART_FU_REV 0      // 1: pass 2 walks the row backwards (freshest L2 lines first)
-#endif
-#ifndef DART_FU_P1LAST
-#define DART_FU_P1LAST 1   // pass-1 bulk copies with the L2 evict_last policy
-#endif
 constexpr int FU_NC = DART_FU_NC;         // consumer warps
 constexpr int FU_SW = DART_FU_SW;         // ring slots per consumer warp
 constexpr int FU_SLOTS = FU_NC * FU_SW;   // ring slots of CH_BYTES
@@ -266,10 +260,10 @@ __global__ void __launch_bounds__(FU_THREADS, DART_FU_CTAS) fused_sweep_kernel(c
         const uint8_t* row = p.logits + t * p.ld_bytes;
         for (int pass = 0; pass < 2; ++pass) {
           for (int64_t ji = 0; ji < nch; ++ji) {
-            const int64_t j = (DART_FU_REV && pass == 1) ? nch - 1 - ji : ji;
+            const int64_t j = ji;
             const int w = (int)(j % FU_NC);
             const int64_t cw = (nch - w + FU_NC - 1) / FU_NC;          // chunks of warp w per pass
-            const int64_t pos = (DART_FU_REV && pass == 1) ? cw - 1 - j / FU_NC : j / FU_NC;
+            const int64_t pos = j / FU_NC;
             const int64_t idx = (2 * nrow + pass) * cw + pos;            // warp w's chunk ordinal
             const int slot = w * FU_SW + (int)(idx % FU_SW);
             const uint32_t use = (uint32_t)(idx / FU_SW);
@@ -277,11 +271,9 @@ __global__ void __launch_bounds__(FU_THREADS, DART_FU_CTAS) fused_sweep_kernel(c
             const int64_t v0 = (j * CL + rank) * CH_VEC;
             const uint32_t nv = (uint32_t)min((int64_t)CH_VEC, nvec - v0);
             mbar_arrive_expect_tx(&sh.full[slot], nv * 16u);
-            if (pass == 0 && !DART_FU_P1LAST)
-              bulk_g2s(ring + (size_t)slot * CH_BYTES, row + v0 * 16, nv * 16u, &sh.full[slot]);
-            else
-              bulk_g2s_hint(ring + (size_t)slot * CH_BYTES, row + v0 * 16, nv * 16u, &sh.full[slot],
-                            pass == 0 ? pol_last : pol_first);
+            // pass 1 evict_last (the row must survive in L2 until pass 2), pass 2 evict_first
+            bulk_g2s_hint(ring + (size_t)slot * CH_BYTES, row + v0 * 16, nv * 16u, &sh.full[slot],
+                          pass == 0 ? pol_last : pol_first);
           }
         }
         ++nrow;
@@ -481,7 +473,7 @@ __global__ void __launch_bounds__(FU_THREADS, DART_FU_CTAS) fused_sweep_kernel(c
     // ---------------- pass 2: gradient over this warp's chunks
     const float2 cc2 = make_float2(c2, c2), nl = make_float2(nl2, nl2), ng = make_float2(-g, -g);
     for (int64_t ji = 0; ji < cw; ++ji) {
-      const int64_t j = DART_FU_REV ? warp + (cw - 1 - ji) * FU_NC : warp + ji * FU_NC;
+      const int64_t j = warp + ji * FU_NC;
       const int64_t idx = (2 * nrow + 1) * cw + ji;
       const int slot = warp * FU_SW + (int)(idx % FU_SW);
       mbar_wait(&sh.full[slot], (uint32_t)((idx / FU_SW) & 1));
@@ -551,403 +543,6 @@ __global__ void __launch_bounds__(FU_THREADS, DART_FU_CTAS) fused_sweep_kernel(c
     par ^= 1;
   }
   if (CL > 1) cluster_sync_all();                 // no CTA exits with mailbox traffic pending
-}
-
-// ============================================================== K7c cluster variant
-// A true single read per kept row: a cluster of FC_CL CTAs (one per SM) holds
-// each row in distributed shared memory -- CTA q of the cluster owns the q-th
-// quarter of every row of the cluster's cost-balanced row range (SURVEY §8(f)
-// #1's cluster-DSMEM design).  HBM traffic = 2V read + 2V written per kept
-// row, 2V written per masked row.
-//
-// Software pipeline over the kept rows k of the range (3 row buffers, 3
-// mailbox slots):
-//   iteration k:  pass 1 of row k (each warp reduces its segment of the
-//                 quarter to (m, s); the CTA partial goes to every cluster
-//                 CTA's mailbox with st.async, completing on the receiver's
-//                 mailbox mbarrier -- no cluster-wide barrier)
-//                 -> fold the FC_CL partials of row k-1 (sent one pass ago, so
-//                 normally already there) in rank order: identical lse and g
-//                 in every CTA -> pass 2 of row k-1 (gradient from shared
-//                 memory, streaming stores)
-//   the quarter of row k+2 is requested once row k-1's buffer is free, so two
-//   rows are always in flight while a third is being reduced.
-// bf16 logits with 3 * ceil(nvec / FC_CL) * 16 B of buffers <= the opt-in
-// shared memory (V <= ~154K); else the L2 re-read kernel above.
-// Measured (single config): 10.4 ms = 5.9 M tokens/s vs 6.9 ms for the L2
-// re-read kernel, although its DRAM traffic is exactly algorithmic: per kept
-// row every warp of the CTA moves in lock step through max / sum / exchange /
-// epilogue / gradient phases (clock64 breakdown per row: pass 1 4.9K cycles
-// against a 2.4K MUFU bound, exchange + epilogue 2.5K, pass 2 4.3K), so MUFU
-// idles a third of the time; 8-CTA clusters at 2 CTAs/SM measured the same.
-// Opt-in (DART_FUSED_VARIANT=1); kept for its exact traffic and its tests.
-#ifndef DART_FC_EXP
-#define DART_FC_EXP 0   // timing experiments only: 2 no loads, 3 no gradient stores, 5 per-phase clock64 totals
-#endif
-#ifndef DART_FC_CL
-#define DART_FC_CL 4
-#endif
-#ifndef DART_FC_WARPS
-#define DART_FC_WARPS 15
-#endif
-#ifndef DART_FC_MINB
-#define DART_FC_MINB 1
-#endif
-constexpr int FC_CL = DART_FC_CL;             // CTAs per cluster (row slices)
-constexpr int FC_WARPS = DART_FC_WARPS;       // consumer warps (+1 producer warp)
-constexpr int FC_THREADS = (FC_WARPS + 1) * 32;   // + one producer warp
-constexpr int FC_NBUF = 3;                    // row buffers (pipeline depth)
-constexpr int FC_NMB = 3;                     // mailbox slots
-constexpr size_t FC_SMEM_MAX = DART_FC_MINB == 1 ? 232448 : 115712;   // opt-in smem per block (1 or 2 CTAs/SM)
-constexpr int FC_MAXK = DART_FC_CL == 4 ? 10 : 11;   // 32-vector groups per warp (vectors per lane)
-
-struct FcShared {
-  uint64_t full[FC_NBUF][FC_WARPS];
-  uint64_t empty[FC_NBUF];                    // FC_WARPS arrivals: the buffer's pass 2 is done
-  uint64_t mbx[FC_NMB];                       // mailbox barriers: FC_CL * 12 bytes per use
-  double mb_s[FC_NMB][FC_CL];                 // mailbox, written by st.async from every cluster CTA
-  float mb_m[FC_NMB][FC_CL];
-  float wm[2][FC_WARPS];                      // warp partials, double-buffered by kept-row parity
-  double wsum[2][FC_WARPS];
-  uint32_t wbad[2][FC_WARPS];
-  float row_g, row_nl2;
-};
-
-// next kept row in [t, rb) (rb if none)
-__device__ __forceinline__ int64_t fc_next_kept(const FusedRec* recs, int64_t t, int64_t rb) {
-  while (t < rb && !(recs[t].flags & 1u)) ++t;
-  return t;
-}
-
-// fixed left fold of (M, S) partials (log2 domain), skipping empty ones
-__device__ __forceinline__ void fc_fold(double& Mr, double& Sr, double Mk, double Sk) {
-  if (Sk == 0.0) return;
-  if (Mr == -INFINITY) { Mr = Mk; Sr = Sk; return; }
-  const double mn = fmax(Mr, Mk);
-  Sr = Sr * (double)ex2((float)(Mr - mn)) + Sk * (double)ex2((float)(Mk - mn));
-  Mr = mn;
-}
-
-template <typename Tout>
-__global__ void __launch_bounds__(FC_THREADS, DART_FC_MINB) fused_cluster_kernel(const FusedParams p) {
-  extern __shared__ __align__(128) uint8_t smem[];
-  constexpr bool OUT_BF16 = sizeof(Tout) == 2;
-  constexpr int64_t OUTV = 8 * (int64_t)sizeof(Tout);
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const uint32_t q = cluster_rank();
-  const int64_t cl = cluster_id(), ncl = cluster_count();
-  const int64_t nvec = p.nvec;
-  const int64_t qv0 = (nvec * q) / FC_CL, qv1 = (nvec * (q + 1)) / FC_CL;
-  const int nq = (int)(qv1 - qv0);
-  const size_t bstride = (size_t)((((nvec + FC_CL - 1) / FC_CL) * 16 + 127) & ~(int64_t)127);
-  uint8_t* buf = smem;
-  FcShared& sh = *reinterpret_cast<FcShared*>(smem + FC_NBUF * bstride);
-  // warp w owns the 32-vector groups [gw0, gw1) of the quarter: lane l holds vectors (g*32 + l)
-  const int ngrp = (nq + 31) / 32;
-  const int gw0 = (int)(((int64_t)ngrp * warp) / FC_WARPS), gw1 = (int)(((int64_t)ngrp * (warp + 1)) / FC_WARPS);
-  const int cntk = gw1 - gw0;                                      // <= FC_MAXK (fused_cluster_ok)
-  const int sv0 = min(gw0 * 32, nq), sv1 = min(gw1 * 32, nq);
-  const int tail_elems = (int)(p.V % 8);
-  const float c2 = p.c2;
-  if (threadIdx.x == 0) {
-    for (int b = 0; b < FC_NBUF; ++b)
-      for (int w = 0; w < FC_WARPS; ++w) mbar_init(&sh.full[b][w], 1);
-    for (int i = 0; i < FC_NMB; ++i) mbar_init(&sh.mbx[i], 1);
-    for (int b = 0; b < FC_NBUF; ++b) mbar_init(&sh.empty[b], FC_WARPS);
-    fence_mbar_init();
-  }
-  __syncthreads();
-  cluster_sync_all();                                              // remote mailboxes initialised
-
-  const FusedRec* recs = reinterpret_cast<const FusedRec*>(p.rec);
-  const int64_t total = p.step_cost[p.S_loc];
-  const int64_t ra = fu_row_at_cost(p, (total * cl) / ncl);
-  const int64_t rb = fu_row_at_cost(p, (total * (cl + 1)) / ncl);
-
-  auto issue = [&](int b, int64_t t) {                             // thread 0: quarter of row t -> buffer b
-    uint64_t pol;
-    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
-    const uint8_t* src = p.logits + t * p.ld_bytes + qv0 * 16;
-    uint8_t* dst = buf + (size_t)b * bstride;
-    for (int w = 0; w < FC_WARPS; ++w) {
-      const int a = min((int)(((int64_t)ngrp * w) / FC_WARPS) * 32, nq);
-      const int e = min((int)(((int64_t)ngrp * (w + 1)) / FC_WARPS) * 32, nq);
-      if (e > a) {
-        if (DART_FC_EXP == 2) { mbar_arrive(&sh.full[b][w]); continue; }
-        mbar_arrive_expect_tx(&sh.full[b][w], (uint32_t)(e - a) * 16u);
-        bulk_g2s_hint(dst + (size_t)a * 16, src + (size_t)a * 16, (uint32_t)(e - a) * 16u, &sh.full[b][w], pol);
-      }
-    }
-  };
-
-  if (warp == FC_WARPS) {
-    // ---------------- producer warp: request every kept row's quarter as soon as a buffer frees
-    if (lane == 0) {
-      int64_t n = 0;
-      for (int64_t t = fc_next_kept(recs, ra, rb); t < rb; t = fc_next_kept(recs, t + 1, rb), ++n) {
-        const int b = (int)(n % FC_NBUF);
-        if (n >= FC_NBUF) mbar_wait(&sh.empty[b], (uint32_t)(((n / FC_NBUF) - 1) & 1));
-        issue(b, t);
-      }
-    }
-    __syncwarp();
-    cluster_sync_all();
-    return;
-  }
-
-  // pass 2 of one kept row: gradient of this warp's segment from buffer `sb`
-  auto pass2 = [&](int64_t t, const FusedRec& rc, const uint8_t* sb, float g, float nl2) {
-    uint8_t* orow = p.dlogits + t * p.ldg_bytes;
-    const float2 cc2 = make_float2(c2, c2), nl = make_float2(nl2, nl2), ng = make_float2(-g, -g);
-#pragma unroll
-    for (int k = 0; k < FC_MAXK; ++k) {
-      const int v = sv0 + 32 * k + lane;
-      if (!(k < cntk && v < sv1)) continue;
-      const uint4 xv = lds128(sb + (size_t)v * 16);
-      const int64_t gv = qv0 + v;
-      float z[8], o[8];
-      unpack<__nv_bfloat16>(xv, z);
-#pragma unroll
-      for (int e = 0; e < 8; e += 2) {
-        const float2 d = __ffma2_rn(make_float2(z[e], z[e + 1]), cc2, nl);
-        const float2 dz = __fmul2_rn(make_float2(ex2(d.x), ex2(d.y)), ng);
-        o[e] = dz.x;
-        o[e + 1] = dz.y;
-      }
-      const int y = rc.y;
-      if (y >= 0 && (int64_t)(y >> 3) == gv) {                     // target element: g (1 - p_y)
-        const float dzy = fmaf(-g, ex2(fmaf(rc.zy, c2, nl2)), g);
-#pragma unroll
-        for (int e = 0; e < 8; ++e) o[e] = (e == (y & 7)) ? dzy : o[e];
-      }
-      const int nvalid = (tail_elems && gv == nvec - 1) ? tail_elems : 8;
-      uint8_t* dst = orow + gv * OUTV;
-      if (DART_FC_EXP == 3) {
-        if (o[0] == 12345.f) *reinterpret_cast<float*>(dst) = o[1] + o[2] + o[3] + o[4] + o[5] + o[6] + o[7];
-        continue;
-      }
-      if (nvalid == 8) {
-        if (OUT_BF16) {
-          stg128_cs(dst, make_uint4(pack_bf16x2(o[0], o[1]), pack_bf16x2(o[2], o[3]), pack_bf16x2(o[4], o[5]),
-                                    pack_bf16x2(o[6], o[7])));
-        } else {
-          stg128_cs(dst, make_uint4(__float_as_uint(o[0]), __float_as_uint(o[1]), __float_as_uint(o[2]),
-                                    __float_as_uint(o[3])));
-          stg128_cs(dst + 16, make_uint4(__float_as_uint(o[4]), __float_as_uint(o[5]), __float_as_uint(o[6]),
-                                         __float_as_uint(o[7])));
-        }
-      } else {
-        for (int e = 0; e < nvalid; ++e) {
-          if (OUT_BF16) reinterpret_cast<__nv_bfloat16*>(dst)[e] = __float2bfloat16_rn(o[e]);
-          else reinterpret_cast<float*>(dst)[e] = o[e];
-        }
-      }
-    }
-  };
-
-  // every consumer warp: wait for row (kidx)'s FC_CL partials, fold them (lanes
-  // 0..FC_CL-1, fixed butterfly: the same bits in every warp and every CTA of
-  // the cluster), row epilogue -> (g, nl2); only CTA 0's warp 0 writes outputs
-  auto finish_row = [&](int64_t kidx, int64_t t, const FusedRec& rc, float& g, float& nl2) {
-    const int mb = (int)(kidx % FC_NMB);
-    mbar_wait(&sh.mbx[mb], (uint32_t)((kidx / FC_NMB) & 1));
-    const float mk = lane < FC_CL ? sh.mb_m[mb][lane] : -INFINITY;
-    const double sk = lane < FC_CL ? sh.mb_s[mb][lane] : 0.0;
-    const float Mf = warp_max_f(sk > 0.0 ? mk : -INFINITY);
-    const double Sr = warp_sum_d(sk > 0.0 ? sk * (double)ex2(mk - Mf) : 0.0);
-    const double Mr = (double)Mf;
-    const double L2s = log2(Sr);
-    g = fused_epilogue(p, t, rc, Mr, L2s, q == 0 && warp == 0 && lane == 0);
-    nl2 = (float)(-(Mr + L2s));
-  };
-
-  int64_t kidx = 0;                 // kept rows reduced so far (pass 1 done)
-  int64_t prev_t = -1;              // the kept row awaiting pass 2
-  FusedRec prev_rc;
-  unsigned long long tm[8] = {0, 0, 0, 0, 0, 0, 0, 0}, c0 = 0, c1 = 0;
-  (void)tm; (void)c0; (void)c1;
-#define FC_T(i) do { if (DART_FC_EXP == 5 && threadIdx.x == 0) { c1 = clock64(); tm[i] += c1 - c0; c0 = c1; } } while (0)
-  if (DART_FC_EXP == 5) c0 = clock64();
-  for (int64_t t = ra; t < rb; ++t) {
-    const FusedRec rc = recs[t];
-    FC_T(0);
-    if (!(rc.flags & 1u)) {
-      if (!p.zero_fill) continue;
-      uint8_t* orow = p.dlogits + t * p.ldg_bytes;
-      for (int64_t vi = qv0 + threadIdx.x; vi < qv1; vi += FC_WARPS * 32) {
-        const int nvalid = (tail_elems && vi == nvec - 1) ? tail_elems : 8;
-        uint8_t* dst = orow + vi * OUTV;
-        if (nvalid == 8) {
-          stg128_cs(dst, make_uint4(0u, 0u, 0u, 0u));
-          if (!OUT_BF16) stg128_cs(dst + 16, make_uint4(0u, 0u, 0u, 0u));
-        } else {
-          for (int e = 0; e < nvalid; ++e) {
-            if (OUT_BF16) reinterpret_cast<__nv_bfloat16*>(dst)[e] = __float2bfloat16_rn(0.f);
-            else reinterpret_cast<float*>(dst)[e] = 0.f;
-          }
-        }
-      }
-      FC_T(6);
-      continue;
-    }
-    const int b = (int)(kidx % FC_NBUF);
-    const uint32_t ph = (uint32_t)((kidx / FC_NBUF) & 1);
-    const uint8_t* sb = buf + (size_t)b * bstride;
-    // ---------------- pass 1 of row t: (m, s) of this warp's segment
-    float m = NEG_CLAMP * c2;
-    float2 s01 = make_float2(0.f, 0.f), s23 = make_float2(0.f, 0.f);
-    uint32_t bad = 0;
-    if (sv1 > sv0) {
-      mbar_wait(&sh.full[b][warp], ph);
-      FC_T(5);
-      // this lane's vectors, -inf for slots past the segment and for the padding of the row's last vector
-      auto load_vec = [&](int k) -> uint4 {
-        const int v = sv0 + 32 * k + lane;
-        uint4 xv = (k < cntk && v < sv1) ? lds128(sb + (size_t)v * 16)
-                                         : make_uint4(0xff80ff80u, 0xff80ff80u, 0xff80ff80u, 0xff80ff80u);
-        if (tail_elems && qv0 + v == nvec - 1) {
-          uint32_t w4[4] = {xv.x, xv.y, xv.z, xv.w};
-#pragma unroll
-          for (int e = 0; e < 8; ++e)
-            if (e >= tail_elems) {
-              if (e & 1) w4[e >> 1] = (w4[e >> 1] & 0x0000ffffu) | 0xff800000u;
-              else w4[e >> 1] = (w4[e >> 1] & 0xffff0000u) | 0x0000ff80u;
-            }
-          xv = make_uint4(w4[0], w4[1], w4[2], w4[3]);
-        }
-        return xv;
-      };
-      // exact per-lane max over the lane's vectors, then one sum from shared
-      // memory again: no rescale (-inf logits give 2^-inf = 0; no 0*inf term here)
-      uint32_t mx = 0xff80ff80u;
-#pragma unroll
-      for (int k = 0; k < FC_MAXK; ++k) {
-        const uint4 xv = load_vec(k);
-        mx = bmax2_nan(mx, xv.x);
-        mx = bmax2_nan(mx, xv.y);
-        mx = bmax2_nan(mx, xv.z);
-        mx = bmax2_nan(mx, xv.w);
-      }
-      const float cmr = fmax_nan(bf16lo(mx), bf16hi(mx));
-      if (!(cmr < INFINITY)) bad |= DART_STATUS_NONFINITE_LOGIT;
-      m = fmaxf(cmr, NEG_CLAMP) * c2;
-      const float2 cc = make_float2(c2, c2), nm = make_float2(-m, -m);
-#pragma unroll
-      for (int k = 0; k < FC_MAXK; ++k) {
-        const uint4 xv = load_vec(k);
-        const float2 d0 = __ffma2_rn(make_float2(bf16lo(xv.x), bf16hi(xv.x)), cc, nm);
-        const float2 d1 = __ffma2_rn(make_float2(bf16lo(xv.y), bf16hi(xv.y)), cc, nm);
-        const float2 d2 = __ffma2_rn(make_float2(bf16lo(xv.z), bf16hi(xv.z)), cc, nm);
-        const float2 d3 = __ffma2_rn(make_float2(bf16lo(xv.w), bf16hi(xv.w)), cc, nm);
-        s01 = __fadd2_rn(s01, make_float2(ex2(d0.x), ex2(d0.y)));
-        s23 = __fadd2_rn(s23, make_float2(ex2(d1.x), ex2(d1.y)));
-        s01 = __fadd2_rn(s01, make_float2(ex2(d2.x), ex2(d2.y)));
-        s23 = __fadd2_rn(s23, make_float2(ex2(d3.x), ex2(d3.y)));
-      }
-    }
-    {
-      const float M = warp_max_f(m);
-      const float sl = (s01.x + s01.y) + (s23.x + s23.y);
-      const double sd = warp_sum_d((double)sl * (double)ex2(m - M));
-      bad = warp_or(bad);
-      if (lane == 0) {
-        sh.wm[kidx & 1][warp] = M;
-        sh.wsum[kidx & 1][warp] = sd;
-        sh.wbad[kidx & 1][warp] = bad;
-      }
-    }
-    FC_T(1);
-    named_bar_sync(1, FC_WARPS * 32);                              // S1: warp partials of row t ready
-    FC_T(2);
-    if (warp == 0) {                                               // CTA partial of row t -> every mailbox
-      const float mw = lane < FC_WARPS ? sh.wm[kidx & 1][lane] : -INFINITY;
-      const double sw = lane < FC_WARPS ? sh.wsum[kidx & 1][lane] : 0.0;
-      const uint32_t bq = warp_or(lane < FC_WARPS ? sh.wbad[kidx & 1][lane] : 0u);
-      const float Mq = warp_max_f(sw > 0.0 ? mw : -INFINITY);
-      const double Sq = warp_sum_d(sw > 0.0 ? sw * (double)ex2(mw - Mq) : 0.0);
-      const int mb = (int)(kidx % FC_NMB);
-      if (lane == 0) {
-        if (bq) status_or(p.status, bq);
-        mbar_arrive_expect_tx(&sh.mbx[mb], (uint32_t)FC_CL * 12u);   // arm this row's mailbox
-      }
-      if (lane < FC_CL) {
-        const uint32_t r = lane;
-        const uint32_t rbar = map_rank(&sh.mbx[mb], r);
-        st_async_b32(map_rank(&sh.mb_m[mb][q], r), __float_as_uint(Mq), rbar);
-        st_async_b64(map_rank(&sh.mb_s[mb][q], r), (uint64_t)__double_as_longlong(Sq), rbar);
-      }
-    }
-    FC_T(3);
-    if (prev_t >= 0) {
-      float g, nl2;
-      finish_row(kidx - 1, prev_t, prev_rc, g, nl2);
-      FC_T(4);
-      const int pbi = (int)((kidx - 1) % FC_NBUF);
-      pass2(prev_t, prev_rc, buf + (size_t)pbi * bstride, g, nl2);
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&sh.empty[pbi]);                  // buffer back to the producer
-    }
-    FC_T(7);
-    prev_t = t;
-    prev_rc = rc;
-    ++kidx;
-  }
-  // drain: pass 2 of the last kept row
-  if (prev_t >= 0) {
-    float g, nl2;
-    finish_row(kidx - 1, prev_t, prev_rc, g, nl2);
-    pass2(prev_t, prev_rc, buf + (size_t)((kidx - 1) % FC_NBUF) * bstride, g, nl2);
-  }
-  __syncwarp();
-  if (DART_FC_EXP == 5 && threadIdx.x == 0 && p.dbg) {
-    for (int i = 0; i < 8; ++i) atomicAdd(&p.dbg[i], tm[i]);
-    atomicAdd(&p.dbg[8], (unsigned long long)kidx);
-    atomicAdd(&p.dbg[9], (unsigned long long)(rb - ra));
-  }
-  cluster_sync_all();                                              // no CTA exits with mailbox traffic pending
-}
-
-size_t fused_cluster_smem(const FusedParams& p) {
-  const size_t bstride = (size_t)((((p.nvec + FC_CL - 1) / FC_CL) * 16 + 127) & ~(int64_t)127);
-  return FC_NBUF * bstride + sizeof(FcShared);
-}
-
-bool fused_cluster_ok(const FusedParams& p) {
-  const int64_t nqmax = (p.nvec + FC_CL - 1) / FC_CL;
-  const int64_t gmax = ((nqmax + 31) / 32 + FC_WARPS - 1) / FC_WARPS;
-  return p.is_bf16 && p.nvec >= FC_CL * FC_WARPS && gmax <= FC_MAXK && fused_cluster_smem(p) <= FC_SMEM_MAX;
-}
-
-template <typename Tout>
-static cudaError_t launch_fused_cluster_t(const FusedParams& p, int num_sms, cudaStream_t st) {
-  const size_t smem = fused_cluster_smem(p);
-  auto kern = fused_cluster_kernel<Tout>;
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (e != cudaSuccess) return e;
-  cudaLaunchConfig_t cfg = {};
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = FC_CL;
-  attr[0].val.clusterDim.y = 1;
-  attr[0].val.clusterDim.z = 1;
-  cfg.blockDim = dim3(FC_THREADS);
-  cfg.dynamicSmemBytes = smem;
-  cfg.stream = st;
-  cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  cfg.gridDim = dim3((unsigned)(num_sms / FC_CL * FC_CL));
-  int n = 0;
-  if (cudaOccupancyMaxActiveClusters(&n, kern, &cfg) != cudaSuccess || n <= 0) {
-    (void)cudaGetLastError();
-    n = num_sms / FC_CL;
-  }
-  cfg.gridDim = dim3((unsigned)(n * FC_CL));
-  return cudaLaunchKernelEx(&cfg, kern, p);
-}
-
-cudaError_t launch_fused_cluster(const FusedParams& p, bool out_bf16, int num_sms, cudaStream_t st) {
-  if (out_bf16) return launch_fused_cluster_t<__nv_bfloat16>(p, num_sms, st);
-  return launch_fused_cluster_t<float>(p, num_sms, st);
 }
 
 cudaError_t launch_fused_rec(const FusedParams& p, cudaStream_t st) {

@@ -144,6 +144,7 @@ struct BwdPrepParams {
   int64_t* step_chunk;   // [S_loc+1] prefix of chunks that need work
   void* stats;           // dart_stats*
   int no_stats;          // 1: step_scale / step_cost / step_chunk only (step sums not yet written)
+  int accumulate;        // 1: add the loss / statistics to *stats instead of overwriting (cfg.stats_accumulate)
 };
 
 struct RowRecParams {
@@ -203,7 +204,6 @@ struct FusedParams {
   uint8_t* aux_flags;
   uint32_t* status;
   void* rec;                    // [T_loc] 32-byte row records (fused_rec_kernel)
-  unsigned long long* dbg;      // timing experiments only (DART_FC_EXP == 5), else NULL
 };
 
 // LM-head-fused forward (dart_lmhead.cu)
@@ -221,6 +221,29 @@ struct LmParams {
   float* part_m;            // [T_loc * n_nc]
   double *part_s, *part_u;  // [T_loc * n_nc]
   float* zy;                // [T_loc] fp32 target logit
+  // backward (dz epilogue) mode: non-NULL DZ_n_kept selects it
+  const int64_t* DZ_n_kept;   // device count of gathered rows (the A operand's valid rows)
+  const void* DZ_rec;         // int4 [n_kept] {g, -lse2, y, local row}
+  uint8_t* DZ_out;            // bf16 dz rows [n_kept, ldg]
+  int64_t DZ_ldg_bytes;
+};
+
+struct LmGatherParams {
+  int64_t T_loc, V, d, ld_h, ld_hk, tok_begin, step_begin, S_loc;
+  const int32_t* tok_step;
+  const int64_t* step_tok_off;
+  const uint8_t* keep;        // [S] global
+  const int64_t* kept_off;    // [S_loc + 1] exclusive prefix of kept tokens per local step
+  const double* step_scale;
+  const float* dell;
+  const float* lse2;
+  const int32_t* target;
+  double invT;
+  const uint8_t* hidden;      // bf16 [T_loc, ld_h]
+  uint8_t* hidden_kept;       // bf16 [>= n_kept, ld_hk]
+  void* rec;                  // int4 [T_loc]
+  int32_t* kept_rows;         // [T_loc]
+  int64_t* n_kept;            // device scalar
 };
 
 struct LmCombineParams {
@@ -232,13 +255,10 @@ struct LmCombineParams {
 
 cudaError_t launch_lmhead(const void* hidden, int64_t ld_h, const void* weight, int64_t ld_w, const LmParams& p,
                           int num_sms, cudaStream_t st);
+cudaError_t launch_lmhead_gather(const LmGatherParams& p, cudaStream_t st);
 cudaError_t launch_lmhead_combine(const FwdParams& p, const LmCombineParams& c, cudaStream_t st);
-cudaError_t launch_gemm_bf16(const void* A, bool a_mn, int64_t lda, const void* B, bool b_mn, int64_t ldb, void* C,
-                             int c_mode, int64_t ldc, int64_t M, int64_t N, int64_t K, int num_sms, cudaStream_t st);
 
 cudaError_t launch_fused_rec(const FusedParams& p, cudaStream_t st);
-bool fused_cluster_ok(const FusedParams& p);      // bf16 logits and a row quarter fits one row buffer
-cudaError_t launch_fused_cluster(const FusedParams& p, bool out_bf16, int num_sms, cudaStream_t st);
 cudaError_t launch_fwd_kl(const FwdParams& p, bool bf16, int num_sms, cudaStream_t st);
 cudaError_t launch_rowrec_kl(const RowRecParams& p, cudaStream_t st);
 cudaError_t launch_bwd_kl(const BwdParams& p, bool in_bf16, bool out_bf16, int num_sms, cudaStream_t st);

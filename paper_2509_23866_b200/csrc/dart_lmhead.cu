@@ -1,27 +1,36 @@
 // dart_lmhead.cu -- SURVEY §8(f) NEXT #3: the LM head fused into the loss
-// pass's forward sweep.
+// pass, forward and backward.
 //
 // z_{t,v} = sum_k h_{t,k} W_{v,k} (the logits whose softmax / T is
 // pi_theta(a|h,s), Eq. 1) is computed on the 5th-generation
 // tensor cores: tcgen05.mma (bf16 x bf16 -> fp32) with both operands staged
 // into shared memory by TMA (128-byte swizzle) and the accumulator in TMEM.
-// The epilogue reads each 128 x 256 accumulator tile back with tcgen05.ld and
-// folds it straight into the per-row online softmax statistics (m, s, u) of
-// the log2 domain (the same (m, s, u) algebra as the logits sweep
-// entropy) plus the target's logit -- the [T, V] logits never touch memory.
+// The [T, V] logits never touch memory; the epilogue reads each 128 x 256
+// accumulator tile back with tcgen05.ld and
+//   forward  (DZ = false): folds it into the per-row online softmax statistics
+//            (m, s, u) of the log2 domain (the logits sweep's algebra,
+//            PAPER.md:238 entropy) plus the target's logit;
+//   backward (DZ = true):  turns it into the loss gradient of the row,
+//            dz_v = g_t (delta_{v,y} - 2^(z_v c2 - lse2_t)) (PAPER.md:256-259,
+//            g_t = c_s dell_t invT), rounded to bf16 and stored -- the rows are
+//            the KEPT rows only (masked steps have no gradient),
+//            gathered into a compact block first (lmhead_gather_kernel).
 //
 // Work item = (128-row block mb, vocabulary chunk nc of LM_NT_PER_CHUNK
-// 256-column tiles); each item leaves one (m, s, u) partial per row, folded in
-// chunk order by lmhead_combine_kernel (dart_fwd.cu).  Persistent CTAs (one
-// per SM) walk the items in a super-column raster: LM_GROUP_NC chunks x all
-// row blocks, chunks innermost, so the ~148 concurrently active items touch
-// ~37 hidden blocks and ~4 weight chunks at a time (L2 resident).
+// 256-column tiles); in the forward each item leaves one (m, s, u) partial per
+// row, folded in chunk order by lmhead_combine_kernel (dart_fwd.cu).
+// Persistent CTAs (one per SM) walk the items in a super-column raster:
+// LM_GROUP_NC chunks x all row blocks, chunks innermost, so the ~148
+// concurrently active items touch ~37 hidden blocks and ~4 weight chunks at a
+// time (L2 resident).
 //
 // Warp roles (192 threads): warp 0 = TMA producer (one lane), warp 1 = TMEM
 // allocator + MMA issuer (one lane), warps 2..5 = epilogue (warp w reads TMEM
 // lanes 32*(w%4) .. +31, i.e. accumulator rows).  Pipelines: LM_STAGES smem
 // stages (full/empty mbarriers), two TMEM accumulators of 256 fp32 columns
 // (tfull/tempty), so the epilogue of tile i overlaps the MMAs of tile i+1.
+// (A CTA-pair cta_group::2 form was measured slower under the 1 kW power cap,
+// DESIGN.md §9, and is not shipped.)
 #include <cstdio>
 #include <cstdlib>
 
@@ -40,12 +49,6 @@ constexpr uint32_t LM_STAGE_BYTES = LM_A_BYTES + LM_B_BYTES;
 constexpr size_t LM_SMEM = 1024 + (size_t)LM_STAGES * LM_STAGE_BYTES + 256;
 constexpr uint32_t LM_TMEM_COLS = LM_ACC * LM_BN;     // 512: the whole TMEM of the SM
 constexpr float LM_MASKED = -1.0e30f;                 // raw logit for columns >= V
-// CTA-pair mode (cta_group::2): 256-row items, each CTA stages 128 rows of h
-// and 128 of the 256 W rows of a tile, 6 stages of 32 KB
-constexpr int LM2_STAGES = 6;
-constexpr uint32_t LM2_A_BYTES = 128 * LM_BK * 2, LM2_B_BYTES = 128 * LM_BK * 2;
-constexpr uint32_t LM2_STAGE_BYTES = LM2_A_BYTES + LM2_B_BYTES;
-constexpr size_t LM2_SMEM = 1024 + (size_t)LM2_STAGES * LM2_STAGE_BYTES + 256;
 
 using tc::fence_after;
 using tc::fence_before;
@@ -75,73 +78,47 @@ __device__ __forceinline__ void lm_item(const LmParams& p, int64_t it, int& mb, 
   nc = sc * p.group_nc + rem % gn;
 }
 
-__device__ __forceinline__ uint32_t lm_cluster_rank() {
-  uint32_t r;
-  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
-  return r;
-}
-__device__ __forceinline__ uint32_t lm_cluster_id() {
-  uint32_t r;
-  asm volatile("mov.u32 %0, %%clusterid.x;" : "=r"(r));
-  return r;
-}
-__device__ __forceinline__ uint32_t lm_cluster_count() {
-  uint32_t r;
-  asm volatile("mov.u32 %0, %%nclusterid.x;" : "=r"(r));
-  return r;
-}
-__device__ __forceinline__ void lm_cluster_sync() {
-  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
-}
+// Rows of the A operand: the forward runs over the shard's T_loc rows; the
+// backward over the n_kept gathered rows (a device count: items past it are
+// skipped by every role, so the launch needs no host sync).
+__device__ __forceinline__ int64_t lm_rows(const LmParams& p) { return p.DZ_n_kept ? *p.DZ_n_kept : p.T_loc; }
 
-// PAIR = false: one CTA per 128-row item (cta_group::1).  PAIR = true: a 2-CTA
-// cluster per 256-row item (cta_group::2; p.n_mb counts 256-row blocks).
-template <bool PAIR>
+template <bool DZ>
 __global__ void __launch_bounds__(LM_THREADS, 1)
-    lmhead_fwd_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                      const LmParams p) {
-  constexpr int STAGES = PAIR ? LM2_STAGES : LM_STAGES;
-  constexpr uint32_t A_BYTES = PAIR ? LM2_A_BYTES : LM_A_BYTES, B_BYTES = PAIR ? LM2_B_BYTES : LM_B_BYTES;
-  constexpr uint32_t STAGE_BYTES = A_BYTES + B_BYTES;
-  constexpr int IBM = PAIR ? 256 : LM_BM;           // rows per item
+    lmhead_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                  const LmParams p) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
   uint8_t* sA = smem;
-  uint8_t* sB = smem + STAGES * A_BYTES;
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
-  uint64_t* empty = full + STAGES;
-  uint64_t* tfull = empty + STAGES;
+  uint8_t* sB = smem + LM_STAGES * LM_A_BYTES;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + LM_STAGES * LM_STAGE_BYTES);
+  uint64_t* empty = full + LM_STAGES;
+  uint64_t* tfull = empty + LM_STAGES;
   uint64_t* tempty = tfull + LM_ACC;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + LM_ACC);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const uint32_t rank = PAIR ? lm_cluster_rank() : 0u;
-  const bool leader = rank == 0;
-  const int64_t unit0 = PAIR ? (int64_t)lm_cluster_id() : (int64_t)blockIdx.x;
-  const int64_t nunits = PAIR ? (int64_t)lm_cluster_count() : (int64_t)gridDim.x;
+  const int64_t unit0 = blockIdx.x, nunits = gridDim.x;
   if (threadIdx.x == 0) {
-    for (int s = 0; s < STAGES; ++s) {
+    for (int s = 0; s < LM_STAGES; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
     }
     for (int a = 0; a < LM_ACC; ++a) {
       mbar_init(&tfull[a], 1);
-      mbar_init(&tempty[a], PAIR ? 8 : 4);   // epilogue warps (x 2 CTAs in pair mode, leader's copy used)
+      mbar_init(&tempty[a], 4);   // the four epilogue warps
     }
     fence_mbar_init();
     tma_prefetch_desc(&tmA);
     tma_prefetch_desc(&tmB);
   }
-  if (warp == 1) {
-    if (PAIR) tc::tmem_alloc_2sm(tmem_slot, LM_TMEM_COLS);
-    else tc::tmem_alloc(tmem_slot, LM_TMEM_COLS);
-  }
+  if (warp == 1) tc::tmem_alloc(tmem_slot, LM_TMEM_COLS);
   tc_fence_before();
   __syncthreads();
-  if (PAIR) lm_cluster_sync();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
   const int KB = (p.K + LM_BK - 1) / LM_BK;
+  const int64_t M = lm_rows(p);
 
   if (warp == 0) {
     // ---------------------------------------------------------- TMA producer
@@ -151,20 +128,15 @@ __global__ void __launch_bounds__(LM_THREADS, 1)
       for (int64_t it = unit0; it < p.n_items; it += nunits) {
         int mb, nc;
         lm_item(p, it, mb, nc);
+        if ((int64_t)mb * LM_BM >= M) continue;
         const int nt0 = nc * p.nt_per_chunk, nt1 = min(nt0 + p.nt_per_chunk, p.n_nt);
         for (int nt = nt0; nt < nt1; ++nt) {
           for (int kb = 0; kb < KB; ++kb) {
             mbar_wait(&empty[stage], ph ^ 1u);
-            if (PAIR) {
-              if (leader) mbar_arrive_expect_tx(&full[stage], 2 * STAGE_BYTES);   // both CTAs' bytes
-              tc::tma_load_2d_2sm(sA + stage * A_BYTES, &tmA, &full[stage], kb * LM_BK, mb * IBM + 128 * (int)rank);
-              tc::tma_load_2d_2sm(sB + stage * B_BYTES, &tmB, &full[stage], kb * LM_BK, nt * LM_BN + 128 * (int)rank);
-            } else {
-              mbar_arrive_expect_tx(&full[stage], STAGE_BYTES);
-              tma_load_2d(sA + stage * A_BYTES, &tmA, &full[stage], kb * LM_BK, mb * LM_BM);
-              tma_load_2d(sB + stage * B_BYTES, &tmB, &full[stage], kb * LM_BK, nt * LM_BN);
-            }
-            if (++stage == STAGES) {
+            mbar_arrive_expect_tx(&full[stage], LM_STAGE_BYTES);
+            tma_load_2d(sA + stage * LM_A_BYTES, &tmA, &full[stage], kb * LM_BK, mb * LM_BM);
+            tma_load_2d(sB + stage * LM_B_BYTES, &tmB, &full[stage], kb * LM_BK, nt * LM_BN);
+            if (++stage == LM_STAGES) {
               stage = 0;
               ph ^= 1u;
             }
@@ -174,12 +146,13 @@ __global__ void __launch_bounds__(LM_THREADS, 1)
     }
   } else if (warp == 1) {
     // ---------------------------------------------------------- MMA issuer
-    if (lane == 0 && leader) {
+    if (lane == 0) {
       int stage = 0, acc = 0;
       uint32_t ph = 0, aph = 0;
       for (int64_t it = unit0; it < p.n_items; it += nunits) {
         int mb, nc;
         lm_item(p, it, mb, nc);
+        if ((int64_t)mb * LM_BM >= M) continue;
         const int nt0 = nc * p.nt_per_chunk, nt1 = min(nt0 + p.nt_per_chunk, p.n_nt);
         for (int nt = nt0; nt < nt1; ++nt) {
           mbar_wait(&tempty[acc], aph ^ 1u);
@@ -188,25 +161,18 @@ __global__ void __launch_bounds__(LM_THREADS, 1)
           for (int kb = 0; kb < KB; ++kb) {
             mbar_wait(&full[stage], ph);
             tc_fence_after();
-            const uint64_t da = sw128_kmajor_desc(smem_u32(sA + stage * A_BYTES));
-            const uint64_t db = sw128_kmajor_desc(smem_u32(sB + stage * B_BYTES));
+            const uint64_t da = sw128_kmajor_desc(smem_u32(sA + stage * LM_A_BYTES));
+            const uint64_t db = sw128_kmajor_desc(smem_u32(sB + stage * LM_B_BYTES));
 #pragma unroll
-            for (int k = 0; k < LM_BK / 16; ++k) {  // UMMA_K = 16 bf16 = 32 B along the swizzled row
-              if (PAIR)
-                tc::umma_bf16_2sm(d_tmem, da + (uint64_t)(2 * k), db + (uint64_t)(2 * k),
-                                  tc::idesc_bf16_f32(256, LM_BN, false, false), (kb | k) != 0 ? 1u : 0u);
-              else
-                umma_bf16(d_tmem, da + (uint64_t)(2 * k), db + (uint64_t)(2 * k), (kb | k) != 0 ? 1u : 0u);
-            }
-            if (PAIR) tc::umma_commit_2sm(&empty[stage], 0x3);   // frees the smem stage in both CTAs
-            else umma_commit(&empty[stage]);        // frees the smem stage when these MMAs retire
-            if (++stage == STAGES) {
+            for (int k = 0; k < LM_BK / 16; ++k)   // UMMA_K = 16 bf16 = 32 B along the swizzled row
+              umma_bf16(d_tmem, da + (uint64_t)(2 * k), db + (uint64_t)(2 * k), (kb | k) != 0 ? 1u : 0u);
+            umma_commit(&empty[stage]);            // frees the smem stage when these MMAs retire
+            if (++stage == LM_STAGES) {
               stage = 0;
               ph ^= 1u;
             }
           }
-          if (PAIR) tc::umma_commit_2sm(&tfull[acc], 0x3);
-          else umma_commit(&tfull[acc]);            // accumulator tile complete
+          umma_commit(&tfull[acc]);                // accumulator tile complete
           if (++acc == LM_ACC) {
             acc = 0;
             aph ^= 1u;
@@ -224,13 +190,19 @@ __global__ void __launch_bounds__(LM_THREADS, 1)
     for (int64_t it = unit0; it < p.n_items; it += nunits) {
       int mb, nc;
       lm_item(p, it, mb, nc);
+      if ((int64_t)mb * LM_BM >= M) continue;
       const int nt0 = nc * p.nt_per_chunk, nt1 = min(nt0 + p.nt_per_chunk, p.n_nt);
-      const int64_t row = (int64_t)mb * IBM + 128 * (int64_t)rank + r;
-      const bool valid = row < p.T_loc;
-      const int64_t y = valid ? (int64_t)p.target[row] : -1;
+      const int64_t row = (int64_t)mb * LM_BM + r;
+      const bool valid = row < M;
+      // forward state
       float m_run = LM_MASKED;         // running max of z*c2 (log2 units); any real logit exceeds it
       double S = 0.0, U = 0.0;         // sum 2^(x-m), sum 2^(x-m)(x-m)
       float zy = 0.0f;
+      // backward row record {g, -lse2, y, local row}
+      int4 rr = make_int4(0, 0, -1, 0);
+      if (DZ && valid) rr = reinterpret_cast<const int4*>(p.DZ_rec)[row];
+      const int64_t y = DZ ? (int64_t)rr.z : (valid ? (int64_t)p.target[row] : -1);
+      uint8_t* const orow = DZ ? p.DZ_out + row * p.DZ_ldg_bytes : nullptr;
       for (int nt = nt0; nt < nt1; ++nt) {
         mbar_wait(&tfull[acc], aph);
         tc_fence_after();
@@ -240,6 +212,34 @@ __global__ void __launch_bounds__(LM_THREADS, 1)
           float x[32];
           tmem_ld32(tbase + (uint32_t)(j * 32), x);
           const int64_t col0 = (int64_t)nt * LM_BN + j * 32;
+          if (DZ) {
+            // dz_v = -g 2^(z_v c2 - lse2) for v != y, g (1 - p_y) at the target
+            if (!valid || col0 >= p.V) continue;
+            const float g = __int_as_float(rr.x), nl2 = __int_as_float(rr.y);
+            const int jy = (int)(y - col0);   // in [0, 32) iff the target is in this group
+            uint32_t o[16];
+#pragma unroll
+            for (int i = 0; i < 32; i += 2) {
+              const float p0 = ex2(fmaf(x[i], c2, nl2)), p1 = ex2(fmaf(x[i + 1], c2, nl2));
+              const float d0 = (i == jy) ? fmaf(-g, p0, g) : -g * p0;
+              const float d1 = (i + 1 == jy) ? fmaf(-g, p1, g) : -g * p1;
+              o[i / 2] = pack_bf16x2(d0, d1);
+            }
+            uint8_t* dst = orow + col0 * 2;
+            if (col0 + 32 <= p.V) {
+              stg128_cs(dst, make_uint4(o[0], o[1], o[2], o[3]));
+              stg128_cs(dst + 16, make_uint4(o[4], o[5], o[6], o[7]));
+              stg128_cs(dst + 32, make_uint4(o[8], o[9], o[10], o[11]));
+              stg128_cs(dst + 48, make_uint4(o[12], o[13], o[14], o[15]));
+            } else {                        // vocabulary tail
+              const int nv = (int)(p.V - col0);
+#pragma unroll
+              for (int i = 0; i < 32; ++i)
+                if (i < nv)
+                  reinterpret_cast<uint16_t*>(dst)[i] = (uint16_t)((i & 1) ? (o[i / 2] >> 16) : (o[i / 2] & 0xffffu));
+            }
+            continue;
+          }
           if (col0 + 32 > p.V) {       // vocabulary tail (TMA zero-filled columns >= V)
             const int nv = (int)max((int64_t)0, p.V - col0);
 #pragma unroll
@@ -285,16 +285,13 @@ __global__ void __launch_bounds__(LM_THREADS, 1)
         }
         tc_fence_before();
         __syncwarp();
-        if (lane == 0) {
-          if (PAIR) tc::mbar_arrive_remote(&tempty[acc], 0);   // the leader's accumulator-empty barrier
-          else mbar_arrive(&tempty[acc]);
-        }
+        if (lane == 0) mbar_arrive(&tempty[acc]);
         if (++acc == LM_ACC) {
           acc = 0;
           aph ^= 1u;
         }
       }
-      if (valid) {
+      if (!DZ && valid) {
         const int64_t idx = row * p.n_nc + nc;
         p.part_m[idx] = m_run;
         p.part_s[idx] = S;
@@ -306,12 +303,41 @@ __global__ void __launch_bounds__(LM_THREADS, 1)
 
   tc_fence_before();
   __syncthreads();
-  if (PAIR) lm_cluster_sync();
   if (warp == 1) {
     tc_fence_after();
-    if (PAIR) tc::tmem_dealloc_2sm(tmem, LM_TMEM_COLS);
-    else tc::tmem_dealloc(tmem, LM_TMEM_COLS);
+    tc::tmem_dealloc(tmem, LM_TMEM_COLS);
   }
+}
+
+// Backward gather (K_lm_g): the kept rows of the shard, in row order, into a
+// compact block -- row i of the block is local row t with
+// i = kept_off[s(t)] + (t - t0(s)) (kept_off = the exclusive prefix of kept
+// tokens over the local steps, bwd_prep's step_cost with unit costs) -- with
+// its 16-byte record {g = c_s dell_t invT, -lse2_t, y_t, t} and its hidden
+// state (one warp per row, 16-byte vectors).
+__global__ void lmhead_gather_kernel(const LmGatherParams p) {
+  const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  const int lane = threadIdx.x & 31;
+  for (int64_t t = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); t < p.T_loc; t += warps) {
+    const int32_t s = p.tok_step[t];
+    if (!p.keep[p.step_begin + s]) continue;
+    const int64_t t0 = p.step_tok_off[p.step_begin + s] - p.tok_begin;
+    const int64_t i = p.kept_off[s] + (t - t0);
+    if (lane == 0) {
+      int4 r;
+      r.x = __float_as_int((float)(p.step_scale[s] * (double)p.dell[t] * p.invT));
+      r.y = __float_as_int(-p.lse2[t]);
+      const int32_t y = p.target[t];
+      r.z = (y >= 0 && y < p.V) ? y : -1;
+      r.w = (int32_t)t;
+      reinterpret_cast<int4*>(p.rec)[i] = r;
+      p.kept_rows[i] = (int32_t)t;
+    }
+    const uint4* src = reinterpret_cast<const uint4*>(p.hidden + t * p.ld_h * 2);
+    uint4* dst = reinterpret_cast<uint4*>(p.hidden_kept + i * p.ld_hk * 2);
+    for (int64_t v = lane; v < p.d / 8; v += 32) dst[v] = src[v];
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) *p.n_kept = p.kept_off[p.S_loc];
 }
 
 }  // namespace
@@ -320,46 +346,22 @@ cudaError_t launch_lmhead(const void* hidden, int64_t ld_h, const void* weight, 
                           int num_sms, cudaStream_t st) {
   if (p.T_loc <= 0 || p.n_items <= 0) return cudaSuccess;
   CUtensorMap tmA, tmB;
-  const char* e2 = getenv("DART_LMHEAD_2SM");
-  if (e2 && e2[0] == '1') {
-    // opt-in: CTA pairs (cta_group::2), 256-row items, 128-row boxes for h and W.  Correct
-    // (tests pass) but measured slower in the bench loop: 60-63 ms vs 50 ms, the SM clock
-    // falling to 1.0-1.1 GHz under the power cap (vs 1.37 GHz for the 1-CTA kernel)
-    if (!tc::make_map_bf16(&tmA, hidden, p.T_loc, p.K, ld_h, LM_BK, 128)) return cudaErrorInvalidValue;
-    if (!tc::make_map_bf16(&tmB, weight, p.V, p.K, ld_w, LM_BK, 128)) return cudaErrorInvalidValue;
-    auto kern = lmhead_fwd_kernel<true>;
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)LM2_SMEM);
-    if (e != cudaSuccess) return e;
-    LmParams q = p;
-    q.n_mb = (int)((p.T_loc + 255) / 256);
-    q.n_items = (int64_t)q.n_mb * q.n_nc;
-    cudaLaunchConfig_t cfg = {};
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = 2;
-    attr[0].val.clusterDim.y = 1;
-    attr[0].val.clusterDim.z = 1;
-    cfg.blockDim = dim3(LM_THREADS);
-    cfg.dynamicSmemBytes = LM2_SMEM;
-    cfg.stream = st;
-    cfg.attrs = attr;
-    cfg.numAttrs = 1;
-    int64_t pairs = num_sms / 2;
-    cfg.gridDim = dim3((unsigned)(2 * pairs));
-    int nclu = 0;   // persistent pairs: never more clusters than can be co-resident
-    if (cudaOccupancyMaxActiveClusters(&nclu, kern, &cfg) == cudaSuccess && nclu > 0 && nclu < pairs) pairs = nclu;
-    (void)cudaGetLastError();
-    if (pairs > q.n_items) pairs = q.n_items;
-    cfg.gridDim = dim3((unsigned)(2 * pairs));
-    return cudaLaunchKernelEx(&cfg, kern, tmA, tmB, q);
-  }
   if (!tc::make_map_bf16(&tmA, hidden, p.T_loc, p.K, ld_h, LM_BK, LM_BM)) return cudaErrorInvalidValue;
   if (!tc::make_map_bf16(&tmB, weight, p.V, p.K, ld_w, LM_BK, LM_BN)) return cudaErrorInvalidValue;
-  cudaError_t e = cudaFuncSetAttribute(lmhead_fwd_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       (int)LM_SMEM);
+  const bool dz = p.DZ_n_kept != nullptr;
+  auto kern = dz ? lmhead_kernel<true> : lmhead_kernel<false>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)LM_SMEM);
   if (e != cudaSuccess) return e;   // (per call: the attribute is per device)
   const int64_t grid = p.n_items < num_sms ? p.n_items : num_sms;
-  lmhead_fwd_kernel<false><<<(unsigned)grid, LM_THREADS, LM_SMEM, st>>>(tmA, tmB, p);
+  kern<<<(unsigned)grid, LM_THREADS, LM_SMEM, st>>>(tmA, tmB, p);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_lmhead_gather(const LmGatherParams& p, cudaStream_t st) {
+  int64_t blocks = (p.T_loc + 7) / 8;
+  if (blocks > 4096) blocks = 4096;
+  if (blocks < 1) blocks = 1;
+  lmhead_gather_kernel<<<(unsigned)blocks, 256, 0, st>>>(p);
   return cudaGetLastError();
 }
 

@@ -31,7 +31,7 @@ STATUS_BITS = {
     1 << 0: "NONFINITE_LOGIT", 1 << 1: "TARGET_RANGE", 1 << 2: "ROW_ALL_NEGINF",
     1 << 3: "NONFINITE_LOGP", 1 << 4: "EMPTY", 1 << 5: "BAD_CSR", 1 << 6: "TARGET_NEGINF",
 }
-ABI_VERSION = 4
+ABI_VERSION = 5
 RATIO_TOKEN, RATIO_STEP = 0, 1
 KL_K3, KL_EXACT = 0, 1
 
@@ -42,7 +42,7 @@ class dart_cfg(ctypes.Structure):
                 ("inv_temperature", ctypes.c_float), ("adv_eps", ctypes.c_float),
                 ("norm_mode", ctypes.c_int32), ("select_rule", ctypes.c_int32),
                 ("zero_fill_masked", ctypes.c_int32), ("ratio_level", ctypes.c_int32),
-                ("kl_mode", ctypes.c_int32)]
+                ("kl_mode", ctypes.c_int32), ("stats_accumulate", ctypes.c_int32)]
 
 
 class dart_meta(ctypes.Structure):
@@ -78,37 +78,8 @@ STATS_FIELDS = ["loss", "n_tok", "n_kept_tok", "n_kept_step", "sum_clip", "sum_t
 _lib = None
 
 EXPORTED = ["dart_workspace_size", "dart_loss_fwd", "dart_select_steps", "dart_loss_bwd", "dart_loss_fused",
-            "dart_loss_pass", "dart_lmhead_workspace_size", "dart_lmhead_fwd", "dart_gemm_bf16",
+            "dart_loss_pass", "dart_lmhead_workspace_size", "dart_lmhead_fwd", "dart_lmhead_bwd",
             "dart_status_str", "dart_abi_version", "dart_last_launch_count", "dart_set_timing_events"]
-
-
-GEMM_STORE_F32, GEMM_STORE_BF16, GEMM_ACCUM_F32 = 0, 1, 2
-
-
-def gemm_bf16(A, B, C, a_mn_major=False, b_mn_major=False, mode=None, stream=None):
-    """C (+)= A_op @ B_op^T on the tensor cores (dart_gemm_bf16).  A_op is A
-    ([M, K]) or, with a_mn_major, A.T where A is stored [K, M]; likewise B_op
-    ([N, K] or B stored [K, N]).  C: fp32 (STORE_F32 / ACCUM_F32) or bf16
-    (STORE_BF16) [M, N]; mode=None picks the store mode from C's dtype, and a
-    mode that does not match C's dtype is refused (the ABI sees only a
-    pointer: an fp32 store into a bf16 buffer would run past its end)."""
-    _require_cuda(A, B, C)
-    if A.dtype != torch.bfloat16 or B.dtype != torch.bfloat16:
-        raise DartError("gemm_bf16 takes bf16 operands")
-    if mode is None:
-        mode = GEMM_STORE_BF16 if C.dtype == torch.bfloat16 else GEMM_STORE_F32
-    want = torch.bfloat16 if mode == GEMM_STORE_BF16 else torch.float32
-    if mode not in (GEMM_STORE_F32, GEMM_STORE_BF16, GEMM_ACCUM_F32) or C.dtype != want:
-        raise DartError(f"gemm_bf16 mode {mode} needs a {want} C, got {C.dtype}")
-    if A.stride(1) != 1 or B.stride(1) != 1 or C.stride(1) != 1:
-        raise DartError("row-major operands expected")
-    M, K = (A.shape[1], A.shape[0]) if a_mn_major else (A.shape[0], A.shape[1])
-    N, Kb = (B.shape[1], B.shape[0]) if b_mn_major else (B.shape[0], B.shape[1])
-    if K != Kb or tuple(C.shape) != (M, N):
-        raise DartError(f"shape mismatch: A_op [{M}, {K}], B_op [{N}, {Kb}], C {tuple(C.shape)}")
-    st = (stream or torch.cuda.current_stream(C.device)).cuda_stream
-    _check(lib().dart_gemm_bf16(_ptr(A), int(a_mn_major), A.stride(0), _ptr(B), int(b_mn_major), B.stride(0),
-                                _ptr(C), int(mode), C.stride(0), M, N, K, ctypes.c_void_p(st)))
 
 
 class DartError(RuntimeError):
@@ -153,10 +124,11 @@ def lib():
     L.dart_lmhead_fwd.restype = ctypes.c_int
     L.dart_lmhead_fwd.argtypes = [P(dart_lmhead), P(dart_batch), P(dart_meta), P(dart_cfg), P(dart_fwd_out),
                                   ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p]
-    L.dart_gemm_bf16.restype = ctypes.c_int
-    L.dart_gemm_bf16.argtypes = [ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64, ctypes.c_void_p, ctypes.c_int32,
-                                 ctypes.c_int64, ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64, ctypes.c_int64,
-                                 ctypes.c_int64, ctypes.c_int64, ctypes.c_void_p]
+    L.dart_lmhead_bwd.restype = ctypes.c_int
+    L.dart_lmhead_bwd.argtypes = [P(dart_lmhead), P(dart_batch), P(dart_meta), P(dart_cfg), P(dart_fwd_out),
+                                  ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p,
+                                  ctypes.c_int64, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
+                                  ctypes.c_size_t, ctypes.c_void_p]
     L.dart_status_str.restype = ctypes.c_char_p
     L.dart_status_str.argtypes = [ctypes.c_int]
     L.dart_abi_version.restype = ctypes.c_int32
@@ -221,11 +193,12 @@ class Config:
     zero_fill_masked: int = 1
     ratio_level: int = RATIO_TOKEN
     kl_mode: int = KL_K3
+    stats_accumulate: int = 0     # 1: bwd calls add into the stats buffer (chunked passes)
 
     def c(self):
         return dart_cfg(self.eps_low, self.eps_high, self.is_cap, self.beta_kl, self.entropy_q,
                         self.inv_temperature, self.adv_eps, self.norm_mode, self.select_rule,
-                        self.zero_fill_masked, self.ratio_level, self.kl_mode)
+                        self.zero_fill_masked, self.ratio_level, self.kl_mode, self.stats_accumulate)
 
     def as_f32(self):
         """The values the library actually sees (float32-rounded), for the oracle."""
@@ -419,9 +392,44 @@ class DartLoss:
             self.ws = torch.empty(need, dtype=torch.uint8, device=self.device)
             self.ws_bytes = need
         self._inputs = (b, None, target, logp_old, logp_roll, logp_ref)
+        self._head = (head, hidden, weight)
         _check(self.L.dart_lmhead_fwd(ctypes.byref(head), ctypes.byref(b), ctypes.byref(self.meta.c()),
                                       ctypes.byref(self.cfg.c()), ctypes.byref(self._fwd_out()), _ptr(self.ws),
                                       self.ws_bytes, ctypes.c_void_p(st)))
+        self.launches += self.L.dart_last_launch_count()
+
+    def backward_lmhead(self, dz, hidden_kept, kept_rows, n_kept, keep=None, norm=None, stream=None):
+        """dart_lmhead_bwd after forward_lmhead (training half):
+        loss + statistics into self.stats, and for the K kept rows of the
+        shard (device count -> n_kept [1] int64): kept_rows[:K] (int32 local
+        rows), hidden_kept[:K] = hidden[kept_rows] and dz[:K] = dL/dz of those
+        rows in bf16, from z = h W^T recomputed on the tensor cores (the
+        logits never exist).  dz [T_loc, >= V] bf16, hidden_kept [T_loc, >= d]
+        bf16, kept_rows [T_loc] int32.  keep / norm default to this object's
+        (e.g. after select(); the update pass passes the old pass's)."""
+        if getattr(self, "_head", None) is None:
+            raise DartError("backward_lmhead needs forward_lmhead first (same object, same workspace)")
+        head, hidden, weight = self._head
+        T = self.shard.T_loc
+        _require_cuda(dz, hidden_kept, kept_rows, n_kept)
+        if dz.dtype != torch.bfloat16 or dz.dim() != 2 or dz.shape[0] < T or dz.shape[1] < self.V or dz.stride(1) != 1:
+            raise DartError(f"dz must be a row-major bf16 [>= {T}, >= {self.V}] tensor")
+        if hidden_kept.dtype != torch.bfloat16 or hidden_kept.dim() != 2 or hidden_kept.shape[0] < T \
+                or hidden_kept.shape[1] < head.d or hidden_kept.stride(1) != 1:
+            raise DartError(f"hidden_kept must be a row-major bf16 [>= {T}, >= {head.d}] tensor")
+        if kept_rows.dtype != torch.int32 or kept_rows.numel() < T or not kept_rows.is_contiguous():
+            raise DartError(f"kept_rows must be a contiguous int32 [>= {T}] tensor")
+        if n_kept.dtype != torch.int64 or n_kept.numel() < 1:
+            raise DartError("n_kept must be an int64 [1] tensor")
+        keep = self.keep if keep is None else keep
+        norm = self.norm if norm is None else norm
+        st = (stream or torch.cuda.current_stream(self.device)).cuda_stream
+        b = self._inputs[0]
+        _check(self.L.dart_lmhead_bwd(ctypes.byref(head), ctypes.byref(b), ctypes.byref(self.meta.c()),
+                                      ctypes.byref(self.cfg.c()), ctypes.byref(self._fwd_out()), _ptr(keep),
+                                      _ptr(norm), _ptr(dz), dz.stride(0), _ptr(hidden_kept), hidden_kept.stride(0),
+                                      _ptr(kept_rows), _ptr(n_kept), _ptr(self.stats), _ptr(self.ws), self.ws_bytes,
+                                      ctypes.c_void_p(st)))
         self.launches += self.L.dart_last_launch_count()
 
     def gather(self):

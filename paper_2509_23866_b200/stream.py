@@ -31,6 +31,7 @@ calls and owns the buffers.
 from __future__ import annotations
 
 import ctypes
+import dataclasses
 from typing import Callable, List, Optional
 
 import numpy as np
@@ -85,7 +86,9 @@ class StreamedPass:
             raise dart.DartError("the streamed pass supports the k3 KL only (kl_mode=KL_K3 or beta_kl=0)")
         self.L = dart.lib()
         dev = torch.device(device)
-        self.device, self.layout, self.V, self.cfg = dev, layout, int(V), cfg
+        # every chunk's dart_loss_bwd adds its loss / statistics into self.stats (in chunk order)
+        self.device, self.layout, self.V = dev, layout, int(V)
+        self.cfg = dataclasses.replace(cfg, stats_accumulate=1)
         self.logits_dtype, self.grad_dtype = logits_dtype, grad_dtype
         self.meta = dart.Meta.from_layout(layout, dev)
         self.group = group
@@ -119,7 +122,6 @@ class StreamedPass:
         self.local_H = torch.zeros(self.C_max * self.S_pad, **f32)       # this rank's block of C1
         self.gathered = torch.zeros(self.n_virtual * self.S_pad, **f32)
         self.rank_step_off = torch.as_tensor(rso, dtype=torch.int64).to(dev)
-        self.stats_all = torch.zeros((max(n, 1), len(dart.STATS_FIELDS)), dtype=torch.float64, device=dev)
         self.stats = torch.zeros(len(dart.STATS_FIELDS), dtype=torch.float64, device=dev)
         # per-chunk state: forward outputs + workspace (tens of bytes per token)
         self.state = []
@@ -181,6 +183,7 @@ class StreamedPass:
                                         ctypes.c_void_p(s)))
         self.launches += self.L.dart_last_launch_count()
         gdt = DART_BF16 if self.grad_dtype == torch.bfloat16 else DART_F32
+        self.stats.zero_()
         for i, c in enumerate(self.chunks):           # sweep 2: gradient over every chunk
             if fill is not None and len(self.chunks) > self.P:
                 fill(i, self.pool_logits[i % self.P])  # re-materialise an evicted chunk
@@ -188,12 +191,11 @@ class StreamedPass:
             st = self.state[i]
             _check(self.L.dart_loss_bwd(ctypes.byref(batches[i]), meta, cfg, ctypes.byref(self._out(st)),
                                         _ptr(self.keep), _ptr(self.norm), _ptr(out), gdt, self.V,
-                                        _ptr(self.stats_all[i]), _ptr(st["ws"]), st["ws_bytes"],
+                                        _ptr(self.stats), _ptr(st["ws"]), st["ws_bytes"],
                                         ctypes.c_void_p(s)))
             self.launches += self.L.dart_last_launch_count()
             if consume is not None:
                 consume(i, out[:c.T_loc])
-        torch.sum(self.stats_all, dim=0, out=self.stats)
         if self.world > 1:                             # C2: statistics all-reduce
             from . import dist as D
             D.all_reduce(self.stats, group=self.group)

@@ -299,7 +299,8 @@ def _fo_work(span):
     return r0, out, bad, worst
 
 
-def full_oracle_compare(dl, batch, cfg, chunk=4096, procs=None, dlogits=None, tol_report=None):
+def full_oracle_compare(dl, batch, cfg, chunk=4096, procs=None, dlogits=None, tol_report=None, mask_given=False,
+                        keep=None):
     """compare() for batches too large for one oracle process: every row of
     `batch` (logits may live on the GPU) goes through the float64 oracle on
     all host cores, chunk by chunk through shared memory, and EVERY GPU
@@ -307,6 +308,9 @@ def full_oracle_compare(dl, batch, cfg, chunk=4096, procs=None, dlogits=None, to
     [T, V] gradient, default dl.dlogits).  Then, on the whole batch: step
     entropies, advantages, the oracle's own selection (mask bit-exact except
     steps within SEL_BAND of tau), tau, normaliser, loss and statistics.
+    mask_given: the pass took its mask as an input (dart_loss_fused): per-token
+    values are checked on the kept rows only, and entropies / the selection
+    (computed by the pass that made the mask) are not part of this call.
     Returns a dict of error summaries (for the test log)."""
     import multiprocessing as mp
     cf = cfg.as_f32()
@@ -321,7 +325,7 @@ def full_oracle_compare(dl, batch, cfg, chunk=4096, procs=None, dlogits=None, to
     assert np.allclose(dl.adv.cpu().numpy()[:L.N_traj], A_traj, rtol=1e-6, atol=1e-7)
     t_step = O.step_of_token(L.step_tok_off, T)
     A_tok = A_traj[O.traj_of_step(L.traj_step_off, L.S)[t_step]]
-    keep_gpu = dl.keep.cpu().numpy()[:L.S]
+    keep_gpu = (dl.keep if keep is None else keep).cpu().numpy()[:L.S]
     c_tok = O.step_weights(keep_gpu, L.step_tok_off, cf["norm_mode"])[t_step]
     ch = min(chunk, max(T, 1))
     zbuf = torch.empty((ch, V), dtype=batch.logits.dtype).share_memory_()
@@ -359,15 +363,49 @@ def full_oracle_compare(dl, batch, cfg, chunk=4096, procs=None, dlogits=None, to
     near = res[:, 9] >= 2
     rep = {}
     # per-token forward values
-    lse, H, logp = dl.lse.cpu().numpy(), dl.H.cpu().numpy(), dl.logp.cpu().numpy()
-    ell, dell = dl.ell.cpu().numpy(), dl.dell.cpu().numpy()
-    assert np.all(np.abs(lse - lse_r) <= RTOL_ENT * np.abs(lse_r) + ATOL_ENT), "lse"
+    kb = keep_gpu.astype(bool)
+    rows_chk = kb[t_step] if mask_given else np.ones(T, dtype=bool)
+    lse, logp = dl.lse.cpu().numpy()[rows_chk], dl.logp.cpu().numpy()[rows_chk]
+    ell, dell = dl.ell.cpu().numpy()[rows_chk], dl.dell.cpu().numpy()[rows_chk]
+    assert np.all(np.abs(lse - lse_r[rows_chk]) <= RTOL_ENT * np.abs(lse_r[rows_chk]) + ATOL_ENT), "lse"
+    assert np.all(np.abs(logp - logp_r[rows_chk]) <= ATOL_LOGP), "logp"
+    ok = ~near[rows_chk]
+    er, dr = ell_r[rows_chk][ok], dell_r[rows_chk][ok]
+    assert np.all(np.abs(ell[ok] - er) <= RTOL_TOK * np.abs(er) + ATOL_TOK), "ell"
+    assert np.all(np.abs(dell[ok] - dr) <= RTOL_TOK * np.abs(dr) + ATOL_TOK), "dell"
+    rep.update(max_grad_err_over_tol=worst, near_clip_rows=int(near.sum()), checked_rows=int(rows_chk.sum()))
+    if not mask_given:
+        _check_entropies_and_selection(dl, L, H_r, ok_ref, keep_gpu, cf, rep)
+    # normaliser (integers, exact) and loss with the GPU's mask (= the oracle's when no flip)
+    nd = dl.norm_dict() if not mask_given else None
+    n = np.diff(L.step_tok_off)
+    if nd is not None:
+        assert nd["n_keep_step"] == int(kb.sum()) and nd["n_keep_tok"] == int(n[kb].sum())
+    st = dl.stats_dict()
+    loss_r = float(np.sum(c_tok * ell_r))
+    scale = float(np.sum(np.abs(c_tok * ell_r))) + 1e-300
+    assert abs(st["loss"] - loss_r) <= RTOL_ENT * scale + 1e-12, (st["loss"], loss_r)
+    rep.update(loss=st["loss"], loss_oracle=loss_r, loss_rel_err=abs(st["loss"] - loss_r) / scale)
+    kt = kb[t_step]
+    assert st["n_tok"] == T and st["n_kept_tok"] == int(kt.sum()) and st["n_kept_step"] == int(kb.sum())
+    sums = [("sum_w", w_r[kt].sum()), ("sum_adv", A_tok[kt].sum()), ("sum_adv2", (A_tok[kt] ** 2).sum()),
+            ("sum_kl", kl_r[kt].sum())] + ([] if mask_given else [("sum_H", H_r.sum())])
+    for k, v in sums:
+        assert abs(st[k] - v) <= 1e-5 * (abs(v) + 1.0), (k, st[k], v)
+    assert abs(st["sum_clip"] - clipped_r[kt].sum()) <= int(near.sum())
+    assert abs(st["sum_trunc"] - trunc_r[kt].sum()) <= 1
+    if tol_report is not None:
+        tol_report.update(rep)
+    return rep
+
+
+def _check_entropies_and_selection(dl, L, H_r, ok_ref, keep_gpu, cf, rep):
+    """Token and step entropies against the oracle, then the oracle's own
+    selection on its float64 step entropies: the GPU mask may differ only at
+    steps within SEL_BAND of tau; tau within the entropy tolerance."""
+    H = dl.H.cpu().numpy()
     eH = np.abs(H - H_r)
     assert np.all(eH <= RTOL_ENT * np.abs(H_r) + ATOL_ENT), f"H max err {eH.max()}"
-    assert np.all(np.abs(logp - logp_r) <= ATOL_LOGP), "logp"
-    ok = ~near
-    assert np.all(np.abs(ell[ok] - ell_r[ok]) <= RTOL_TOK * np.abs(ell_r[ok]) + ATOL_TOK), "ell"
-    assert np.all(np.abs(dell[ok] - dell_r[ok]) <= RTOL_TOK * np.abs(dell_r[ok]) + ATOL_TOK), "dell"
     # step entropies, the oracle's own selection, tau
     sH_r = O.step_entropy(H_r, L.step_tok_off)
     sH = dl.step_H.cpu().numpy()[:L.S].astype(np.float64)
@@ -388,25 +426,4 @@ def full_oracle_compare(dl, batch, cfg, chunk=4096, procs=None, dlogits=None, to
     d_tau = np.abs(sH_r - tau_r[g_of_s])
     rep.update(max_err_H=float(eH.max()), max_err_step_H=float(esH.max()), mask_flips=int(flips.size),
                min_gap_to_tau_nonzero=float(d_tau[d_tau > 0].min()) if np.any(d_tau > 0) else None,
-               max_err_tau=float(np.max(np.abs(tau[okt] - tau_r[okt]))) if okt.any() else 0.0,
-               max_grad_err_over_tol=worst, near_clip_rows=int(near.sum()))
-    # normaliser (integers, exact) and loss with the GPU's mask (= the oracle's when no flip)
-    nd = dl.norm_dict()
-    n = np.diff(L.step_tok_off)
-    kb = keep_gpu.astype(bool)
-    assert nd["n_keep_step"] == int(kb.sum()) and nd["n_keep_tok"] == int(n[kb].sum())
-    st = dl.stats_dict()
-    loss_r = float(np.sum(c_tok * ell_r))
-    scale = float(np.sum(np.abs(c_tok * ell_r))) + 1e-300
-    assert abs(st["loss"] - loss_r) <= RTOL_ENT * scale + 1e-12, (st["loss"], loss_r)
-    rep.update(loss=st["loss"], loss_oracle=loss_r, loss_rel_err=abs(st["loss"] - loss_r) / scale)
-    kt = kb[t_step]
-    assert st["n_tok"] == T and st["n_kept_tok"] == int(kt.sum()) and st["n_kept_step"] == int(kb.sum())
-    for k, v in (("sum_w", w_r[kt].sum()), ("sum_adv", A_tok[kt].sum()), ("sum_adv2", (A_tok[kt] ** 2).sum()),
-                 ("sum_H", H_r.sum()), ("sum_kl", kl_r[kt].sum())):
-        assert abs(st[k] - v) <= 1e-5 * (abs(v) + 1.0), (k, st[k], v)
-    assert abs(st["sum_clip"] - clipped_r[kt].sum()) <= int(near.sum())
-    assert abs(st["sum_trunc"] - trunc_r[kt].sum()) <= 1
-    if tol_report is not None:
-        tol_report.update(rep)
-    return rep
+               max_err_tau=float(np.max(np.abs(tau[okt] - tau_r[okt]))) if okt.any() else 0.0)

@@ -47,7 +47,7 @@ def test_sm100a_cubin_inside():
 
 def test_version_and_status_strings(L):
     from paper_2509_23866_b200 import dart
-    assert L.dart_abi_version() == dart.ABI_VERSION == 4
+    assert L.dart_abi_version() == dart.ABI_VERSION == 5
     for c in range(5):
         assert L.dart_status_str(c).startswith(b"DART_")
     assert L.dart_status_str(99) == b"DART_UNKNOWN_STATUS"
@@ -170,21 +170,29 @@ def test_binding_refuses_cpu_tensors():
         dart._require_cuda(torch.zeros(3))
 
 
-def test_gemm_validation(L):
-    """dart_gemm_bf16 rejects bad shapes / pitches / pointers before any launch."""
-    from paper_2509_23866_b200 import dart
-    f = ctypes.c_void_p(0x100000)
+def test_lmhead_bwd_validation(L):
+    """dart_lmhead_bwd (training half) rejects bad buffers
+    before any launch; stats_accumulate must be 0 or 1."""
+    dart, cfg, meta, batch, out = _structs()
     E = dart.DART_ERR_INVALID_ARG
+    fake = ctypes.c_void_p(0x100000)
+    head = dart.dart_lmhead(fake, ctypes.c_void_p(0x300000), 64, 64, 72)
+    b = dart.dart_batch.from_buffer_copy(batch); b.logits = None
 
-    def g(A=f, a_mn=0, lda=64, B=f, b_mn=0, ldb=64, C=f, mode=0, ldc=64, M=64, N=64, K=64):
-        return L.dart_gemm_bf16(A, a_mn, lda, B, b_mn, ldb, C, mode, ldc, M, N, K, None)
-    assert g(mode=7) == dart.DART_ERR_UNSUPPORTED
-    assert g(M=0) == E
-    assert g(N=60, ldc=64) == E                      # N % 8
-    assert g(lda=60) == E                            # pitch % 8
-    assert g(lda=32) == E                            # K-major A: lda < K
-    assert g(a_mn=1, lda=32, M=64) == E              # MN-major A: lda < M
-    assert g(b_mn=1, ldb=32, N=64) == E
-    assert g(C=None) == E
-    assert g(A=ctypes.c_void_p(0x100008)) == E       # misaligned
-    assert g(ldc=32) == E                            # ldc < N
+    def call(dz=fake, ldg=512, hk=fake, ld_hk=64, rows=fake, nk=fake, norm=fake, stats=fake, c=cfg, ws_bytes=1 << 40):
+        return L.dart_lmhead_bwd(ctypes.byref(head), ctypes.byref(b), ctypes.byref(meta), ctypes.byref(c),
+                                 ctypes.byref(out), fake, norm, dz, ldg, hk, ld_hk, rows, nk, stats,
+                                 ctypes.c_void_p(0x200000), ws_bytes, None)
+    assert call(ws_bytes=8) == dart.DART_ERR_WORKSPACE      # everything else valid
+    assert call(dz=None) == E
+    assert call(ldg=500) == E                                # < V
+    assert call(ldg=516) == E                                # % 8
+    assert call(dz=ctypes.c_void_p(0x100008)) == E           # misaligned
+    assert call(hk=None) == E
+    assert call(ld_hk=32) == E                               # < d
+    assert call(rows=None) == E
+    assert call(nk=None) == E
+    assert call(norm=None) == E
+    assert call(stats=None) == E
+    c = dart.dart_cfg.from_buffer_copy(cfg); c.stats_accumulate = 2
+    assert call(c=c) == E

@@ -13,14 +13,6 @@ from tests.gpu_helpers import ATOL_ENT, ATOL_LOGP, ATOL_TOK, P_REL, RTOL_ENT, RT
 pytestmark = pytest.mark.gpu
 
 
-@pytest.fixture(params=["1", "0", "2"], ids=["cluster", "l2reread", "l2split"], autouse=True)
-def fused_variant(request, monkeypatch):
-    """Both dart_loss_fused kernels: the cluster / distributed-shared-memory
-    single read (default for bf16 logits) and the L2 re-read variant."""
-    monkeypatch.setenv("DART_FUSED_VARIANT", request.param)
-    return request.param
-
-
 def _fused_case(name, cfg, seed=0, grad_dtype=None, rows=None, **kw):
     b = synth.make_batch(name, seed=seed, **kw)
     old = run_gpu(b, cfg, grad_dtype=grad_dtype)          # old-policy pass -> mask + norm
@@ -114,19 +106,18 @@ def test_fused_matches_two_pass_gradient_closely():
     assert abs(dl.stats_dict()["loss"] - two.stats_dict()["loss"]) <= 1e-6 * abs(two.stats_dict()["loss"])
 
 
-def test_fused_single_config_full_size_sampled(fused_variant):
+def test_fused_single_config_full_size_vs_oracle():
     """BASELINE.json single config at full size (T = 61440, V = 152064 bf16)
     as `bench.py --fused` runs it: the mask and normaliser from a regular
-    forward + select, then the fused call; 12 sampled rows against the oracle
-    row by row (oracle primitives composed as in `loss_pass`), properties on
-    the rest (masked rows zero, loss = sum of the GPU's own kept terms)."""
+    forward + select (the old-policy pass), then the fused call.  Every row
+    through the float64 oracle on the host cores: lse / log-prob / ell / dell
+    of every kept row, every dlogits row (masked rows exactly zero), loss and
+    statistics."""
     b = synth.make_batch("single", seed=0, device="cuda")
     cfg = dart.Config()
-    cfgf = cfg.as_f32()
     old = run_gpu(b, cfg)
     old.check_status()
     keep, norm = old.keep.clone(), old.norm.clone()
-    nd = old.norm_dict()
     del old
     dev = torch.device("cuda")
     dl = dart.DartLoss(b.layout, dart.whole_shard(b.layout), b.V, cfg, dev)
@@ -134,42 +125,7 @@ def test_fused_single_config_full_size_sampled(fused_variant):
     dl.fused(b.logits, b.target, b.logp_old, b.logp_rollout, b.logp_ref, keep=keep, norm=norm)
     torch.cuda.synchronize()
     dl.check_status()
-    L = b.layout
-    keep_np = keep.cpu().numpy()[:L.S]
-    tok_keep = np.repeat(keep_np, np.diff(L.step_tok_off)).astype(bool)
-    A, _ = O.advantages(L.traj_reward, L.traj_group, L.traj_step_off, L.G)
-    s_of_t = O.step_of_token(L.step_tok_off, L.T)
-    tr_of_s = O.traj_of_step(L.traj_step_off, L.S)
-    rng = np.random.default_rng(7)
-    kept_rows = rng.choice(np.nonzero(tok_keep)[0], 10, replace=False).tolist()
-    masked_rows = rng.choice(np.nonzero(~tok_keep)[0], 2, replace=False).tolist()
-    for t in sorted(kept_rows):
-        z = b.logits[t].float().cpu().numpy()
-        y = int(b.target[t])
-        lse, logp, H, p = O.token_row(z, y)
-        ell, dell, w, r, clipped, kl = O.token_loss(logp, float(b.logp_old[t]), float(b.logp_rollout[t]),
-                                                    float(b.logp_ref[t]), A[tr_of_s[s_of_t[t]]], cfgf)
-        assert abs(float(dl.lse[t]) - lse) <= RTOL_ENT * abs(lse) + ATOL_ENT
-        assert abs(float(dl.logp[t]) - logp) <= ATOL_LOGP
-        near = min(abs(r - (1 - cfgf["eps_low"])), abs(r - (1 + cfgf["eps_high"]))) < 1e-5 * r
-        if near:
-            continue
-        assert abs(float(dl.ell[t]) - ell) <= RTOL_TOK * abs(ell) + ATOL_TOK
-        assert abs(float(dl.dell[t]) - dell) <= RTOL_TOK * abs(dell) + ATOL_TOK
-        g = nd["inv_norm"] * dell
-        onehot = np.zeros_like(p)
-        onehot[y] = 1.0
-        dref = g * (onehot - p)
-        dg = nd["inv_norm"] * (RTOL_TOK * abs(dell) + ATOL_TOK)
-        tol = grad_tol(dref, np.maximum(p, onehot), g, dg, torch.bfloat16)
-        dz = dl.dlogits[t].float().cpu().numpy()
-        assert np.all(np.abs(dz - dref) <= tol), t
-    for t in masked_rows:
-        assert torch.all(dl.dlogits[t] == 0)
-    masked = torch.as_tensor(np.nonzero(~tok_keep)[0][:128], device="cuda")
-    assert torch.all(dl.dlogits[masked] == 0)
-    st = dl.stats_dict()
-    ell_all = dl.ell.cpu().numpy().astype(np.float64)
-    L_chk = np.sum(ell_all[tok_keep]) * nd["inv_norm"]
-    assert abs(st["loss"] - L_chk) <= 1e-9 * np.sum(np.abs(ell_all[tok_keep])) * nd["inv_norm"] + 1e-15
-    assert st["n_kept_tok"] == nd["n_keep_tok"]
+    from tests.gpu_helpers import full_oracle_compare
+    rep = full_oracle_compare(dl, b, cfg, mask_given=True, keep=keep)
+    print("fused full-size parity:", rep)
+    assert rep["checked_rows"] == int(dl.stats_dict()["n_kept_tok"])
