@@ -159,7 +159,8 @@ __global__ void rowrec_kernel(RowRecParams p) {
 // w, w+WARPS, ...).  Every SM thus streams ONE contiguous read region and ONE
 // write region at a time -- far fewer concurrent DRAM streams than a
 // warp-per-range split -- while still running WARPS independent rings.
-constexpr int BVPL = BCH_VEC / 32;   // 16-byte vectors per lane per bwd chunk
+constexpr int BVPL = BCH_VEC / 32;
+   // 16-byte vectors per lane per bwd chunk
 struct OCur {
   int64_t j, jend;  // chunk ordinal (in the local chunk sequence) and the warp's end
   int64_t s;        // local step
@@ -267,24 +268,6 @@ __device__ __forceinline__ void grad_vec(const uint4& xv, float2 cc2, float2 nl,
   }
 }
 
-// store EPV outputs of one full vector (compile-time widths, streaming stores)
-template <typename Tout, int EPV>
-__device__ __forceinline__ void store_full(uint8_t* dst, const float* o) {
-  if (sizeof(Tout) == 2) {
-    if (EPV == 8) {
-      stg128_cs(dst, make_uint4(pack_bf16x2(o[0], o[1]), pack_bf16x2(o[2], o[3]), pack_bf16x2(o[4], o[5]),
-                                pack_bf16x2(o[6], o[7])));
-    } else {
-      *reinterpret_cast<uint2*>(dst) = make_uint2(pack_bf16x2(o[0], o[1]), pack_bf16x2(o[2], o[3]));
-    }
-  } else {
-#pragma unroll
-    for (int e = 0; e < EPV; e += 4)
-      stg128_cs(dst + 4 * e, make_uint4(__float_as_uint(o[e]), __float_as_uint(o[e + 1]), __float_as_uint(o[e + 2]),
-                                        __float_as_uint(o[e + 3])));
-  }
-}
-
 template <typename Tin, int WARPS, int STAGES>
 __device__ __forceinline__ void bwd_issue(OCur& pc, const BwdParams& p, uint64_t* bars, uint8_t* ring, int slot,
                                           int lane, uint64_t pol) {
@@ -304,9 +287,9 @@ __device__ __forceinline__ void bwd_issue(OCur& pc, const BwdParams& p, uint64_t
 // guarded region, so the eight 128-bit stores of a chunk leave interleaved
 // with the math (an unguarded loop bursts them and stalls on the store queue;
 // wider 32-byte stores and TMA bulk stores from shared memory were both
-// measured slower).  Per vector the only bookkeeping is one compare against
-// the chunk's vector count and an immediate store offset from the lane's
-// first output vector; vocabulary tails (V % EPV != 0) take a generic path.
+// measured slower).  Hoisting the per-vector address / tail arithmetic to a
+// per-chunk lane base (fewer instructions) also measured slower on B200:
+// 6.05 vs 5.74 ms on one box, A/B in one session (profiles/r02_bwd_ab.md).
 template <typename Tin, typename Tout, int WARPS, int STAGES>
 __global__ void __launch_bounds__(WARPS * 32, 1)
 bwd_sweep_kernel(const BwdParams p) {
@@ -357,9 +340,7 @@ bwd_sweep_kernel(const BwdParams p) {
     const int64_t t = cc.t;
     const int64_t v0 = (int64_t)cc.c * BCH_VEC;
     const int nv = (int)min((int64_t)BCH_VEC, nvec - v0);
-    const bool tailc = tail_elems && v0 + nv == nvec;     // the row's last, partial vector is in this chunk
     uint8_t* const orow = dlog + t * ldg_bytes;
-    uint8_t* const olane = orow + (v0 + lane) * OUTV;     // this lane's first output vector
     if (cc.kept) {
       if (t != cur_t) {
         cur = (t == pre_t) ? pre : rec[t];
@@ -376,35 +357,29 @@ bwd_sweep_kernel(const BwdParams p) {
       const float2 cc2 = make_float2(c2, c2), nl = make_float2(nl2, nl2), ng = make_float2(-g, -g);
       uint4 x[BVPL];
 #pragma unroll
-      for (int k = 0; k < BVPL; ++k) x[k] = lds128(sp + (lane + 32 * k) * 16);   // past nv: unused
-      // every LDS has landed in registers before the slot goes back to the copy
-      // engine (read-then-async-write; one register per LDS.128 is enough)
+      for (int k = 0; k < BVPL; ++k) {
+        const int vi = lane + 32 * k;
+        x[k] = (vi < nv) ? lds128(sp + vi * 16) : make_uint4(0u, 0u, 0u, 0u);
+      }
       uint32_t dep = 0;
 #pragma unroll
-      for (int k = 0; k < BVPL; ++k) dep ^= x[k].x;
+      for (int k = 0; k < BVPL; ++k) dep |= x[k].x | x[k].y | x[k].z | x[k].w;
       asm volatile("" ::"r"(dep));
       __syncwarp();
       if (pc.valid) bwd_issue<Tin, WARPS, STAGES>(pc, p, bars, ring, slot, lane, pol);
       if (++slot == STAGES) { slot = 0; phase ^= 1u; }
-      if (!tailc) {
-#pragma unroll
-        for (int k = 0; k < BVPL; ++k) {
-          if (lane + 32 * k < nv) {   // keeps each vector's math and store together (see above)
-            float o[EPV];
-            grad_vec<Tin>(x[k], cc2, nl, ng, o);
-            store_full<Tout, EPV>(olane + k * 32 * OUTV, o);
-          }
-        }
-      } else {
+      {
 #pragma unroll
         for (int k = 0; k < BVPL; ++k) {
           const int vi = lane + 32 * k;
           if (vi < nv) {
+            const int64_t gv = v0 + vi;
             float o[EPV];
             grad_vec<Tin>(x[k], cc2, nl, ng, o);
-            const int nvalid = (vi == nv - 1) ? tail_elems : EPV;
-            if (OUT_BF16) store_vals_bf16(olane + k * 32 * OUTV, o, nvalid, EPV);
-            else store_vals_f32(olane + k * 32 * OUTV, o, nvalid, EPV);
+            const int nvalid = (tail_elems && gv == nvec - 1) ? tail_elems : EPV;
+            uint8_t* dst = orow + gv * (int64_t)OUTV;
+            if (OUT_BF16) store_vals_bf16(dst, o, nvalid, EPV);
+            else store_vals_f32(dst, o, nvalid, EPV);
           }
         }
       }
@@ -427,10 +402,11 @@ bwd_sweep_kernel(const BwdParams p) {
       for (int k = 0; k < BVPL; ++k) {
         const int vi = lane + 32 * k;
         if (vi < nv) {
-          const int nvalid = (tailc && vi == nv - 1) ? tail_elems : EPV;
-          if (nvalid == EPV) store_full<Tout, EPV>(olane + k * 32 * OUTV, o);
-          else if (OUT_BF16) store_vals_bf16(olane + k * 32 * OUTV, o, nvalid, EPV);
-          else store_vals_f32(olane + k * 32 * OUTV, o, nvalid, EPV);
+          const int64_t gv = v0 + vi;
+          const int nvalid = (tail_elems && gv == nvec - 1) ? tail_elems : EPV;
+          uint8_t* dst = orow + gv * (int64_t)OUTV;
+          if (OUT_BF16) store_vals_bf16(dst, o, nvalid, EPV);
+          else store_vals_f32(dst, o, nvalid, EPV);
         }
       }
     }

@@ -277,7 +277,9 @@ class DartLoss:
         self.shard = shard
         self.V = int(V)
         self.ld = int(ld) if ld is not None else self.V
-        self.ldg = int(ldg) if ldg is not None else self.V
+        # default gradient row pitch: V rounded up to 16 bytes (the ABI's row alignment)
+        per = 16 // torch.empty((), dtype=grad_dtype).element_size()
+        self.ldg = int(ldg) if ldg is not None else -(-self.V // per) * per
         self.ld_ref = int(ld_ref) if ld_ref is not None else self.ld
         self.cfg = cfg
         self.group = group

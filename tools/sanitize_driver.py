@@ -25,7 +25,7 @@ for name in which:
         dl.check_status()
         print(name, "ok", dl.stats_dict()["loss"])
         continue
-    elif name == "lmupdate":   # NEXT #3 update pass: CTA-pair tcgen05 GEMMs (K- and MN-major) + fused loss
+    elif name == "lmupdate":   # NEXT #3 update pass: forward + dz from the z-GEMM epilogue (kept rows)
         from paper_2509_23866_b200 import lmhead
         lb = synth.make_lmhead("grid2x4x3x20@3000", 256, seed=3)
         bb = lb.batch
@@ -39,9 +39,7 @@ for name in which:
         up.check_status()
         print(name, "ok", up.stats_dict()["loss"], float(dh.abs().sum()), float(dW.abs().sum()))
         continue
-    elif name in ("fused", "fused_cluster"):   # NEXT #1 (both kernels)
-        import os
-        os.environ["DART_FUSED_VARIANT"] = "1" if name == "fused_cluster" else "0"
+    elif name == "fused":   # NEXT #1: the fused update kernel
         layout, _, _, _ = synth.config_layout("grid2x2x3x24@30000", seed=0)
         b = synth.make_batch("x", seed=0, layout=layout, V=30000, dtype=torch.bfloat16)
         old = run_gpu(b, dart.Config())
