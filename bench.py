@@ -592,7 +592,10 @@ def run_dart(args):
                        "parallelism": f"dp{world} (trajectory-sharded)"},
             "roofline": {"bound": "hbm", "kernel": dom[0], "achieved": dom[1], "peak": peak,
                          "peak_source": peak_src, "unit": "GB/s", "frac": dom[1] / peak,
-                         "traffic": traffic, "algorithmic_bytes_per_launch": dom[2],
+                         "traffic": traffic,
+                         "traffic_source": ("prior ncu --set full capture of this kernel at this config "
+                                            "(profiles/ncu_traffic.json, not measured in this run)") if traffic else None,
+                         "algorithmic_bytes_per_launch": dom[2],
                          "avg_launch_ms": dom[3]},
             "kernels": {"fwd_sweep": {"avg_ms": fwd_avg, "median_ms": statistics.median(fwd_ms) if not args.fused else None,
                                       "best_ms": min(fwd_ms) if not args.fused else None,
@@ -810,6 +813,7 @@ def run_lmhead(args):
                          "peak_source": peak_src + " bf16_tflops_sustained (kernel inside a long step loop)",
                          "unit": "TFLOP/s", "frac": achieved / peak_s, "frac_of_burst_peak": achieved / peak_b,
                          "traffic": traffic, "traffic_unit": "DRAM bytes per launch (ncu); the tensor-bound kernel's operand re-reads hit L2 95%",
+                         "traffic_source": "prior ncu capture (profiles/ncu_traffic.json)" if traffic else None,
                          "algorithmic_flops_per_launch": flops, "avg_launch_ms": gemm_ms},
             "unfused_cublas_pipeline": unfused,
             "gpu_launches": launches,
@@ -1074,7 +1078,9 @@ def run_e2e(args, dl, batch, stream, world, inputs):
     value = dl.layout.T / (ms * 1e-3)
     del host, dev_bufs
     return {"value": value, "unit": "logit-tokens/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-            "steps": steps, "ms_per_step": ms}
+            "steps": steps, "ms_per_step": ms,
+            "d2h_what": "the step's loss + statistics (dart_stats, 11 float64); dlogits stay in HBM for the "
+                        "model's backward (a trainer never copies them to the host)"}
 
 
 # ------------------------------------------------------------------ oracle arms
@@ -1190,6 +1196,26 @@ def oracle_samples(batch, per_sample_tokens, n):
     return out, ntok
 
 
+def cpu_model():
+    """The host CPU's model name (lscpu / /proc/cpuinfo), for the cpu_baseline record."""
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    try:
+        import subprocess
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for line in out.splitlines():
+            if line.startswith("Model name"):
+                return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return None
+
+
 def cpu_baseline(args, batch, cfg):
     per = args.cpu_tokens
     procs = oracle_procs(per * batch.V * 4) if args.cpu_procs <= 0 else args.cpu_procs
@@ -1199,7 +1225,8 @@ def cpu_baseline(args, batch, cfg):
         dt = pool.run()
     finally:
         pool.close()
-    return {"value": ntok / dt, "unit": "logit-tokens/s", "cores": procs, "kind": "oracle",
+    return {"value": ntok / dt, "unit": "logit-tokens/s", "cores": procs, "cpu_model": cpu_model(),
+            "host_cores": os.cpu_count(), "kind": "oracle",
             "sample": f"{procs} independent samples run concurrently, one per process, each <= {per} tokens "
                       f"of whole steps of one task group (groups cycled; {ntok} tokens in all, V={batch.V}); "
                       f"full fwd+select+bwd incl. dlogits, float64 NumPy, one thread per process",
@@ -1239,7 +1266,8 @@ def run_reference(args):
                        + (" (exact full-vocabulary KL from reference logits: NEXT #4)" if args.kl == "exact" else ""),
                        "desc": CONFIG_DESC.get(args.config, args.config),
                        "sample_tokens": ntok},
-            "cpu_baseline": {"value": value, "unit": "logit-tokens/s", "cores": procs, "kind": "oracle",
+            "cpu_baseline": {"value": value, "unit": "logit-tokens/s", "cores": procs, "cpu_model": cpu_model(),
+                             "host_cores": os.cpu_count(), "kind": "oracle",
                              "sample": f"per step: {procs} concurrent runs (one process per core) of one sample of "
                                        f"{ntok1} tokens of {args.config} ({ntraj} trajectories of task 0, whole "
                                        f"steps), float64 NumPy oracle, one thread per process"},

@@ -5,12 +5,21 @@
 #include <cstdlib>
 #include <cstring>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "dart_common.cuh"
 #include "dart_internal.h"
 
 using namespace dart;
 
 namespace {
+
+// NVTX range over one ABI call (header-only NVTX3: a no-op unless a profiler
+// such as nsys / ncu --nvtx injects itself), so timelines show the phases.
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+};
 
 thread_local int32_t g_launches = 0;
 thread_local int32_t g_last_launches = 0;
@@ -265,6 +274,7 @@ size_t dart_workspace_size(const dart_batch* b, const dart_meta* m, const dart_c
 
 dart_status dart_loss_fwd(const dart_batch* b, const dart_meta* m, const dart_cfg* c, const dart_fwd_out* o,
                           void* ws, size_t ws_bytes, void* stream) {
+  NvtxRange nvtx_("dart_loss_fwd");
   dart_status st = batch_check(b, m, c);
   if (st != DART_OK) return st;
   if ((st = fwd_out_check(b, m, o)) != DART_OK) return st;
@@ -356,6 +366,7 @@ size_t dart_lmhead_workspace_size(const dart_lmhead* h, const dart_batch* b, con
 
 dart_status dart_lmhead_fwd(const dart_lmhead* h, const dart_batch* b, const dart_meta* m, const dart_cfg* c,
                             const dart_fwd_out* o, void* ws, size_t ws_bytes, void* stream) {
+  NvtxRange nvtx_("dart_lmhead_fwd");
   dart_status st = lmhead_check(h, b, m, c);
   if (st != DART_OK) return st;
   if ((st = fwd_out_check(b, m, o)) != DART_OK) return st;
@@ -443,6 +454,7 @@ dart_status dart_lmhead_bwd(const dart_lmhead* h, const dart_batch* b, const dar
                             const dart_fwd_out* f, const uint8_t* keep, const dart_norm* norm, void* dz, int64_t ldg,
                             void* hidden_kept, int64_t ld_hk, int32_t* kept_rows, int64_t* n_kept, dart_stats* stats,
                             void* ws, size_t ws_bytes, void* stream) {
+  NvtxRange nvtx_("dart_lmhead_bwd");
   dart_status st = lmhead_check(h, b, m, c);
   if (st != DART_OK) return st;
   if ((st = fwd_out_check(b, m, f)) != DART_OK) return st;
@@ -513,6 +525,7 @@ dart_status dart_lmhead_bwd(const dart_lmhead* h, const dart_batch* b, const dar
 dart_status dart_select_steps(const float* gathered, const int64_t* rank_step_off, int32_t world, int64_t S_pad,
                               const dart_meta* m, const dart_cfg* c, const uint8_t* group_ok, uint8_t* keep,
                               float* tau, dart_norm* norm, void* ws, size_t ws_bytes, void* stream) {
+  NvtxRange nvtx_("dart_select_steps");
   if (!meta_ok(m) || !cfg_ok(c)) return DART_ERR_INVALID_ARG;
   if (world < 1 || S_pad < 0) return DART_ERR_INVALID_ARG;
   if (!norm || (m->S > 0 && (!gathered || !keep)) || (m->G > 0 && (!group_ok || !tau))) return DART_ERR_INVALID_ARG;
@@ -557,6 +570,7 @@ dart_status dart_select_steps(const float* gathered, const int64_t* rank_step_of
 dart_status dart_loss_bwd(const dart_batch* b, const dart_meta* m, const dart_cfg* c, const dart_fwd_out* f,
                           const uint8_t* keep, const dart_norm* norm, void* dlogits, int32_t grad_dtype,
                           int64_t ldg, dart_stats* stats, void* ws, size_t ws_bytes, void* stream) {
+  NvtxRange nvtx_("dart_loss_bwd");
   const bool loss_only = dlogits == nullptr;   // loss + statistics only: no gradient sweep, logits unused
   dart_status st = batch_check(b, m, c, !loss_only);
   if (st != DART_OK) return st;
@@ -636,6 +650,7 @@ dart_status dart_loss_bwd(const dart_batch* b, const dart_meta* m, const dart_cf
 dart_status dart_loss_fused(const dart_batch* b, const dart_meta* m, const dart_cfg* c, const uint8_t* keep,
                             const dart_norm* norm, const dart_fwd_out* o, void* dlogits, int32_t grad_dtype,
                             int64_t ldg, dart_stats* stats, void* ws, size_t ws_bytes, void* stream) {
+  NvtxRange nvtx_("dart_loss_fused");
   dart_status st = batch_check(b, m, c);
   if (st != DART_OK) return st;
   if (c->ratio_level != DART_RATIO_TOKEN || exact_kl(c)) return DART_ERR_UNSUPPORTED;
@@ -740,6 +755,7 @@ dart_status dart_loss_fused(const dart_batch* b, const dart_meta* m, const dart_
 dart_status dart_loss_pass(const dart_batch* b, const dart_meta* m, const dart_cfg* c, const dart_fwd_out* f,
                            uint8_t* keep, float* tau, dart_norm* norm, void* dlogits, int32_t grad_dtype,
                            int64_t ldg, dart_stats* stats, void* ws, size_t ws_bytes, void* stream) {
+  NvtxRange nvtx_("dart_loss_pass");
   dart_status st = batch_check(b, m, c);
   if (st != DART_OK) return st;
   // single rank: the shard must be the whole batch
