@@ -53,7 +53,7 @@
 extern "C" {
 #endif
 
-#define DART_ABI_VERSION 5
+#define DART_ABI_VERSION 6
 
 typedef enum {
   DART_OK = 0,
@@ -344,6 +344,83 @@ int32_t dart_last_launch_count(void);
  * by the caller. */
 void dart_set_timing_events(void* fwd_sweep_begin, void* fwd_sweep_end, void* bwd_sweep_begin,
                             void* bwd_sweep_end);
+
+/* ==================================================================
+ * SURVEY §8(f) #4 (second half) -- host-side data curation (PAPER.md
+ * §4.1-4.2): the per-iteration rules that shape the ragged batch whose
+ * CSR metadata (dart_meta) the loss pass above consumes.  HOST functions
+ * (host pointers, no stream, no GPU), deterministic: the one random draw
+ * the method makes (which pool trajectory to inject) is an input.
+ * Readings where the paper is silent: DESIGN.md §3 R15-R19.
+ * ================================================================== */
+typedef struct {
+  int32_t n_max;          /* rollouts per task at low success rate: 8 */
+  int32_t n_min;          /* rollouts at success rate 1 (R15, paper silent): 2 */
+  int32_t cap_min;        /* shortest trajectory cap: 10 steps */
+  int32_t cap_max;        /* longest trajectory cap: 50 steps */
+  int32_t sr_high_permille; /* success rate above which sampling is reduced, in 1/1000: 600;
+                               integer so the rule is exact rational arithmetic (no float ties) */
+  int32_t reserved;       /* 0 */
+  double success_reward;  /* R17: a trajectory succeeds iff reward >= this: 0.5 (rewards in [0,1]) */
+} dart_curation_cfg;
+
+/* Trajectories grouped by task, as CSR (host pointers, caller-owned):
+ * task g owns trajectories [group_off[g], group_off[g+1]); trajectory i owns
+ * steps [traj_step_off[i], traj_step_off[i+1]) (>= 1 step), step k has
+ * step_tokens[k] >= 1 tokens; reward[i] in [0, 1]. */
+typedef struct {
+  int64_t n_groups;
+  const int64_t* group_off;       /* [n_groups + 1], group_off[0] == 0, non-decreasing */
+  const int64_t* traj_step_off;   /* [N + 1], strictly increasing from 0 */
+  const int32_t* step_tokens;     /* [S] */
+  const float* reward;            /* [N] */
+} dart_traj_set;
+
+/* Output of dart_curate_batch (host buffers, caller-owned, capacities in
+ * cap_traj / cap_steps): the dart_meta CSR of the batch plus each
+ * trajectory's source (rollout index i >= 0, or -(p + 1) for pool
+ * trajectory p).  G, N_traj, S, T are written by the call. */
+typedef struct {
+  int64_t cap_traj, cap_steps;    /* in: capacities of the arrays below */
+  int32_t* traj_group;            /* [cap_traj]      task group (0..G-1, non-decreasing) */
+  float* traj_reward;             /* [cap_traj]      R_i */
+  int64_t* traj_source;           /* [cap_traj]      provenance */
+  int64_t* traj_step_off;         /* [cap_traj + 1]  CSR steps */
+  int64_t* step_tok_off;          /* [cap_steps + 1] CSR tokens */
+  int64_t G, N_traj, S, T;        /* out: sizes */
+} dart_curated;
+
+/* PAPER.md:204-206 (§4.1 Dynamic Rollout Frequency): rollouts to sample for
+ * each of G tasks from its success history (n_success of n_total past
+ * rollouts; n_total == 0 counts as success rate 0).  sr <= sr_high -> n_max;
+ * above, linearly down to n_min at sr = 1, rounded half up (R15):
+ *   n = n_max - floor((sr - sr_high) / (1 - sr_high) * (n_max - n_min) + 1/2)
+ * evaluated exactly in integers (sr = n_success / n_total, sr_high =
+ * sr_high_permille / 1000).  DART_ERR_INVALID_ARG on a bad config or counts. */
+dart_status dart_rollout_counts(const dart_curation_cfg* cfg, int64_t G, const int64_t* n_success,
+                                const int64_t* n_total, int32_t* n_rollouts);
+
+/* PAPER.md:209-211 (§4.1 Dynamic Trajectory Length): each task's step cap
+ * from the historical maximum length of its successful completions
+ * (max_success_len[g] < 0: none yet -> cap_max), clamped to
+ * [cap_min, cap_max] (R16). */
+dart_status dart_trajectory_caps(const dart_curation_cfg* cfg, int64_t G, const int32_t* max_success_len,
+                                 int32_t* caps);
+
+/* PAPER.md:209-218 (§4.1-4.2): one training batch from this iteration's
+ * rollouts.  Per task, in order: (1) a rollout longer than the task's cap is
+ * terminated at the cap and, not having completed, gets reward 0 (R18);
+ * (2) if every rollout of the task then fails and the task's pool is not
+ * empty, pool trajectory floor(pool_draw[g] * n_pool_g) (a stored success,
+ * PAPER.md:216) is appended to the group (R19); (3) the task's trajectories
+ * (rollouts in order, then the injected one) form one contiguous group; a
+ * task with no trajectory forms none.  pool may be NULL (no pool) or must
+ * have n_groups == rollouts->n_groups; pool_draw[g] in [0, 1).
+ * DART_ERR_INVALID_ARG on malformed CSR, bad caps / draws or too small
+ * output capacities (cap_traj >= N_rollouts + G and cap_steps >= steps of
+ * all rollouts + pool suffice). */
+dart_status dart_curate_batch(const dart_curation_cfg* cfg, const dart_traj_set* rollouts, const int32_t* caps,
+                              const dart_traj_set* pool, const double* pool_draw, dart_curated* out);
 
 #ifdef __cplusplus
 }

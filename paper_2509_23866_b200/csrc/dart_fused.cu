@@ -41,7 +41,10 @@ constexpr int FU_SLOTS = FU_NC * FU_SW;   // ring slots of CH_BYTES
 // Each consumer warp owns FU_SW slots: a warp then never waits on a slot more
 // than one phase ahead of the producer (a shared ring let a fast warp alias
 // an older mbarrier phase -- parity waits -- and read stale data).
-constexpr int FU_THREADS = (FU_NC + 1) * 32;
+constexpr int FU_PRODUCER = FU_NC, FU_REDUCER = FU_NC + 1;
+constexpr int FU_THREADS = (FU_NC + 2) * 32;
+constexpr int FU_BAR_PART = 1, FU_BAR_ROW = 2;   // named barriers: partials in / row broadcast out
+constexpr int FU_BAR_COUNT = (FU_NC + 1) * 32;    // consumers + reducer
 
 // ---------------------------------------------------------------- cluster helpers
 __device__ __forceinline__ uint32_t cluster_rank() {
@@ -81,9 +84,10 @@ __device__ __forceinline__ void st_async_b64(uint32_t raddr, uint64_t v, uint32_
 struct FusedShared {
   uint64_t full[FU_SLOTS];
   uint64_t empty[FU_SLOTS];
-  double part_s[2][FU_NC];
-  float part_m[2][FU_NC];
-  float row_g[2], row_nl2[2];
+  double part_s[FU_NC];
+  float part_m[FU_NC];
+  float row_g, row_nl2, row_zy;
+  int32_t row_y;
   // split-row mode (CL = 2): the peer CTA's row partial, double-buffered by row parity
   uint64_t mbx[2];
   double mb_s[2][2];
@@ -96,6 +100,10 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
 __device__ __forceinline__ void named_bar_sync(int id, int count) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
 }
+__device__ __forceinline__ void named_bar_arrive(int id, int count) {
+  asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(count) : "memory");
+}
+
 
 template <typename Tin>
 __device__ __forceinline__ void unpack(const uint4& xv, float* z) {
@@ -143,6 +151,11 @@ struct __align__(16) FusedRec {
   float c;          // per-step loss weight c_s (0: masked step)
   uint32_t flags;   // bit0 kept step, bit1 truncated (ratio >= C), bits 8.. status bits
 };
+
+__device__ __forceinline__ int64_t fu_next_kept(const FusedRec* recs, int64_t t, int64_t rb) {
+  while (t < rb && !(recs[t].flags & 1u)) ++t;
+  return t;
+}
 
 __global__ void fused_rec_kernel(FusedParams p, FusedRec* rec) {
   const int64_t nthreads = (int64_t)gridDim.x * blockDim.x;
@@ -212,6 +225,18 @@ __device__ float fused_epilogue(const FusedParams& p, int64_t t, const FusedRec&
 // lse and g in both CTAs).  Two such CTAs per SM then hold one row's worth of
 // bytes between the passes instead of two, which halves the L2 footprint of
 // the pass-2 re-read while keeping two independent pipelines per SM.
+//
+// Roles per CTA: FU_NC consumer warps, a producer lane (bulk copies into one
+// FU_SW-slot ring per consumer warp, P1 then P2 chunks of each kept row) and
+// a reducer warp.  After pass 1 of a row each consumer warp stores its (m, s)
+// partial and ARRIVES on a named barrier (non-blocking); the reducer warp
+// SYNCs on it, folds the partials (and the peer CTA's), runs the fp64 row
+// epilogue and arrives on a second barrier with g / lse, on which the
+// consumers sync before pass 2.  (Measured variants: taking the
+// next row's first pass-1 chunks before pass 2 of this row, separate pass-1
+// / pass-2 rings, or pass 2 straight from L2 with ld.global all ran slower:
+// anything that lets pass 1 run ahead either puts HBM latency in front of
+// the L2-fed pass 2 or grows the L2 footprint until pass-2 reads miss.)
 template <typename Tin, typename Tout, int CL>
 __global__ void __launch_bounds__(FU_THREADS, DART_FU_CTAS) fused_sweep_kernel(const FusedParams p) {
   extern __shared__ __align__(128) uint8_t smem[];
@@ -219,12 +244,12 @@ __global__ void __launch_bounds__(FU_THREADS, DART_FU_CTAS) fused_sweep_kernel(c
   FusedShared& sh = *reinterpret_cast<FusedShared*>(smem + (size_t)FU_SLOTS * CH_BYTES);
   constexpr int EPV = 16 / sizeof(Tin);
   constexpr bool OUT_BF16 = sizeof(Tout) == 2;
-  constexpr int64_t OUTV = EPV * (int64_t)sizeof(Tout);
+  constexpr int OUTV = EPV * (int)sizeof(Tout);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
     for (int s = 0; s < FU_SLOTS; ++s) {
       mbar_init(&sh.full[s], 1);
-      mbar_init(&sh.empty[s], FU_NC > 0 ? 1 : 1);
+      mbar_init(&sh.empty[s], 1);
     }
     if (CL > 1) {
       mbar_init(&sh.mbx[0], 1);
@@ -242,41 +267,39 @@ __global__ void __launch_bounds__(FU_THREADS, DART_FU_CTAS) fused_sweep_kernel(c
   const int64_t total = p.step_cost[p.S_loc];
   const int64_t ra = fu_row_at_cost(p, (total * unit) / nb);
   const int64_t rb = fu_row_at_cost(p, (total * (unit + 1)) / nb);
-  const int64_t nvec = p.nvec;
+  // 32-bit chunk / vector arithmetic inside a row (a row is < 2^31 vectors)
+  const int nvec = (int)p.nvec;
   // local chunk jl <-> row chunk jl * CL + rank
-  const int64_t nch = (p.nch - (int64_t)rank + CL - 1) / CL;
+  const int nch = (int)((p.nch - (int64_t)rank + CL - 1) / CL);
   const float c2 = p.c2;
   const int tail_elems = (int)(p.V % EPV);
+  const FusedRec* recs = reinterpret_cast<const FusedRec*>(p.rec);
 
-  if (warp == FU_NC) {
-    // ===================== producer (one lane) =====================
+  if (warp == FU_PRODUCER) {
+    // ===================== producer (one lane): chunks in the consumers' ring order
     if (lane == 0) {
       uint64_t pol_last, pol_first;
       asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol_last));
       asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol_first));
-      int64_t nrow = 0;   // kept rows issued so far
-      for (int64_t t = ra; t < rb; ++t) {
-        if (!(reinterpret_cast<const FusedRec*>(p.rec)[t].flags & 1u)) continue;
+      uint32_t nrow = 0;   // kept rows issued so far
+      for (int64_t t = fu_next_kept(recs, ra, rb); t < rb; t = fu_next_kept(recs, t + 1, rb), ++nrow) {
         const uint8_t* row = p.logits + t * p.ld_bytes;
         for (int pass = 0; pass < 2; ++pass) {
-          for (int64_t ji = 0; ji < nch; ++ji) {
-            const int64_t j = ji;
-            const int w = (int)(j % FU_NC);
-            const int64_t cw = (nch - w + FU_NC - 1) / FU_NC;          // chunks of warp w per pass
-            const int64_t pos = j / FU_NC;
-            const int64_t idx = (2 * nrow + pass) * cw + pos;            // warp w's chunk ordinal
+          for (int j = 0; j < nch; ++j) {
+            const int w = j % FU_NC;
+            const uint32_t cw = (uint32_t)((nch - w + FU_NC - 1) / FU_NC);    // chunks of warp w per pass
+            const uint32_t idx = (2u * nrow + (uint32_t)pass) * cw + (uint32_t)(j / FU_NC);   // warp w's ordinal
             const int slot = w * FU_SW + (int)(idx % FU_SW);
-            const uint32_t use = (uint32_t)(idx / FU_SW);
+            const uint32_t use = idx / FU_SW;
             if (use > 0) mbar_wait(&sh.empty[slot], (use - 1) & 1u);
-            const int64_t v0 = (j * CL + rank) * CH_VEC;
-            const uint32_t nv = (uint32_t)min((int64_t)CH_VEC, nvec - v0);
+            const int v0 = (j * CL + (int)rank) * CH_VEC;
+            const uint32_t nv = (uint32_t)min(CH_VEC, nvec - v0);
             mbar_arrive_expect_tx(&sh.full[slot], nv * 16u);
             // pass 1 evict_last (the row must survive in L2 until pass 2), pass 2 evict_first
-            bulk_g2s_hint(ring + (size_t)slot * CH_BYTES, row + v0 * 16, nv * 16u, &sh.full[slot],
+            bulk_g2s_hint(ring + (size_t)slot * CH_BYTES, row + (size_t)v0 * 16, nv * 16u, &sh.full[slot],
                           pass == 0 ? pol_last : pol_first);
           }
         }
-        ++nrow;
       }
     }
     __syncwarp();
@@ -284,62 +307,89 @@ __global__ void __launch_bounds__(FU_THREADS, DART_FU_CTAS) fused_sweep_kernel(c
     return;
   }
 
-  // ===================== consumers (FU_NC warps) =====================
-  const FusedRec* recs = reinterpret_cast<const FusedRec*>(p.rec);
-  const int64_t cw = (nch - warp + FU_NC - 1) / FU_NC;   // this warp's chunks per pass
-  int64_t nrow = 0;  // kept rows consumed so far
-  int par = 0;       // mailbox parity
-  FusedRec nxt;
-  if (ra < rb) nxt = recs[ra];
-  for (int64_t t = ra; t < rb; ++t) {
-    const FusedRec rc = nxt;
-    if (t + 1 < rb) nxt = recs[t + 1];      // prefetch: hidden behind this row
-    uint8_t* orow = p.dlogits + t * p.ldg_bytes;
-    if (!(rc.flags & 1u)) {
-      if (!p.zero_fill) continue;
-      // masked step: zeros, no read; consumer warps split this CTA's chunks of the row
-      for (int64_t li = (int64_t)warp * 32 + lane; li < nch * CH_VEC; li += FU_NC * 32) {
-        const int64_t vi = ((li / CH_VEC) * CL + rank) * CH_VEC + (li % CH_VEC);
-        if (vi >= nvec) continue;
-        const int nvalid = (tail_elems && vi == nvec - 1) ? tail_elems : EPV;
-        uint8_t* dst = orow + vi * OUTV;
-        if (nvalid == EPV) {
-          if (OUT_BF16 && EPV == 8) stg128_cs(dst, make_uint4(0u, 0u, 0u, 0u));
-          else if (OUT_BF16) *reinterpret_cast<uint2*>(dst) = make_uint2(0u, 0u);
-          else
-            for (int e = 0; e < EPV; e += 4) stg128_cs(dst + 4 * e, make_uint4(0u, 0u, 0u, 0u));
-        } else {
-          for (int e = 0; e < nvalid; ++e) {
-            if (OUT_BF16) reinterpret_cast<__nv_bfloat16*>(dst)[e] = __float2bfloat16_rn(0.f);
-            else reinterpret_cast<float*>(dst)[e] = 0.f;
+  if (warp == FU_REDUCER) {
+    // ===================== reducer warp: fold, exchange, epilogue, broadcast
+    uint32_t k = 0;
+    for (int64_t tk = fu_next_kept(recs, ra, rb); tk < rb; tk = fu_next_kept(recs, tk + 1, rb), ++k) {
+      const int par = (int)(k & 1);
+      named_bar_sync(FU_BAR_PART, FU_BAR_COUNT);       // the consumers' partials of row k are in
+      // fixed-order fold of the consumer warps' partials (one per lane, xor butterfly)
+      const float mw = lane < FU_NC ? sh.part_m[lane] : -INFINITY;
+      const double sw = lane < FU_NC ? sh.part_s[lane] : 0.0;
+      const float Mf = warp_max_f(sw > 0.0 ? mw : -INFINITY);
+      double Sr = warp_sum_d(sw > 0.0 ? sw * (double)ex2(mw - Mf) : 0.0);
+      double Mr = Sr > 0.0 ? (double)Mf : -INFINITY;
+      if (lane == 0) {
+        const FusedRec rc = recs[tk];
+        if (CL > 1) {                            // exchange with the peer CTA, fold in rank order
+          sh.mb_m[par][rank] = (float)Mr;
+          sh.mb_s[par][rank] = Sr;
+          mbar_arrive_expect_tx(&sh.mbx[par], 12u);                     // the peer's 4 + 8 bytes
+          const uint32_t peer = rank ^ 1u;
+          const uint32_t rbar = map_rank(&sh.mbx[par], peer);
+          st_async_b32(map_rank(&sh.mb_m[par][rank], peer), __float_as_uint((float)Mr), rbar);
+          st_async_b64(map_rank(&sh.mb_s[par][rank], peer), (uint64_t)__double_as_longlong(Sr), rbar);
+          mbar_wait(&sh.mbx[par], (k >> 1) & 1u);
+          Mr = -INFINITY;
+          Sr = 0.0;
+          for (int k2 = 0; k2 < CL; ++k2) {
+            const double Mk = (double)sh.mb_m[par][k2], Sk = sh.mb_s[par][k2];
+            if (Sk == 0.0) continue;
+            if (Mr == -INFINITY) { Mr = Mk; Sr = Sk; continue; }
+            const double mn = fmax(Mr, Mk);
+            Sr = Sr * (double)ex2((float)(Mr - mn)) + Sk * (double)ex2((float)(Mk - mn));
+            Mr = mn;
           }
         }
+        const double L2s = log2(Sr);
+        sh.row_g = fused_epilogue(p, tk, rc, Mr, L2s, rank == 0);
+        sh.row_nl2 = (float)(-(Mr + L2s));
+        sh.row_y = rc.y;
+        sh.row_zy = rc.zy;
       }
-      continue;
+      named_bar_arrive(FU_BAR_ROW, FU_BAR_COUNT);      // row k's g / lse out (consumers sync)
     }
-    // ---------------- pass 1: online max / sum over this warp's chunks
-    float m = NEG_CLAMP * c2;
-    float2 s01 = make_float2(0.f, 0.f), s23 = make_float2(0.f, 0.f);
-    uint32_t bad = 0;
-    for (int64_t j = warp; j < nch; j += FU_NC) {
-      const int64_t idx = 2 * nrow * cw + j / FU_NC;
-      const int slot = warp * FU_SW + (int)(idx % FU_SW);
-      mbar_wait(&sh.full[slot], (uint32_t)((idx / FU_SW) & 1));
-      const uint8_t* sp = ring + (size_t)slot * CH_BYTES;
-      const int64_t v0 = (j * CL + rank) * CH_VEC;
-      const int nv = (int)min((int64_t)CH_VEC, nvec - v0);
-      uint4 x[VPL];
+    if (CL > 1) cluster_sync_all();                 // no CTA exits with mailbox traffic pending
+    return;
+  }
+
+  // ===================== consumers (FU_NC warps) =====================
+  const uint32_t cw = (uint32_t)((nch - warp + FU_NC - 1) / FU_NC);   // this warp's chunks per pass
+  uint32_t idx = 0;              // this warp's ring ordinal (chunks taken so far)
+  uint32_t bad = 0;
+
+  // the chunk at the head of this warp's ring: wait, pull into registers, slot back to the producer
+  auto take = [&](uint4 (&x)[VPL], int nv) {
+    const int slot = warp * FU_SW + (int)(idx % FU_SW);
+    mbar_wait(&sh.full[slot], (idx / FU_SW) & 1u);
+    ++idx;
+    const uint8_t* sp = ring + (size_t)slot * CH_BYTES;
+    if (nv == CH_VEC) {     // full chunk: unpredicated loads (measured 4% faster than the guarded form)
+#pragma unroll
+      for (int q = 0; q < VPL; ++q) x[q] = lds128(sp + (lane + 32 * q) * 16);
+    } else {
 #pragma unroll
       for (int q = 0; q < VPL; ++q) {
         const int vi = lane + 32 * q;
         x[q] = (vi < nv) ? lds128(sp + vi * 16) : make_uint4(0u, 0u, 0u, 0u);
       }
-      uint32_t dep = 0;
+    }
+    uint32_t dep = 0;
 #pragma unroll
-      for (int q = 0; q < VPL; ++q) dep |= x[q].x | x[q].y | x[q].z | x[q].w;
-      asm volatile("" ::"r"(dep));
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&sh.empty[slot]);   // slot back to the producer
+    for (int q = 0; q < VPL; ++q) dep |= x[q].x | x[q].y | x[q].z | x[q].w;
+    asm volatile("" ::"r"(dep));
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&sh.empty[slot]);   // slot back to the producer
+  };
+
+  // pass 1 over this warp's chunks [ji0, ji1) of a row: online max / sum into (m, s01, s23)
+  auto pass1 = [&](uint32_t ji0, uint32_t ji1, float& m, float2& s01, float2& s23) {
+    for (uint32_t ji = ji0; ji < ji1; ++ji) {
+      const int j = warp + (int)ji * FU_NC;
+      const int v0 = (j * CL + (int)rank) * CH_VEC;
+      const int nv = min(CH_VEC, nvec - v0);
+      uint4 x[VPL];
+      take(x, nv);
       const bool tail_chunk = tail_elems && v0 + nv == nvec;
       if (sizeof(Tin) == 2 && nv == CH_VEC && !tail_chunk) {
         // fast path: packed bf16x2 max, one unpack per pair; -inf logits give
@@ -419,84 +469,35 @@ __global__ void __launch_bounds__(FU_THREADS, DART_FU_CTAS) fused_sweep_kernel(c
         }
       }
     }
-    // warp partial (fixed lane fold) -> mailbox
-    {
-      const float M = warp_max_f(m);
-      const float sl = (s01.x + s01.y) + (s23.x + s23.y);
-      const double sd = warp_sum_d((double)sl * (double)ex2(m - M));
-      bad = warp_or(bad);
-      if (lane == 0) {
-        sh.part_m[par][warp] = M;
-        sh.part_s[par][warp] = sd;
-        if (bad) status_or(p.status, bad);
-      }
+  };
+
+  // warp partial of a row (fixed lane fold) -> the reducer; never waits
+  auto publish = [&](float m, float2 s01, float2 s23) {
+    const float M = warp_max_f(m);
+    const float sl = (s01.x + s01.y) + (s23.x + s23.y);
+    const double sd = warp_sum_d((double)sl * (double)ex2(m - M));
+    if (lane == 0) {
+      sh.part_m[warp] = M;
+      sh.part_s[warp] = sd;
     }
-    named_bar_sync(1, FU_NC * 32);
-    // ---------------- row epilogue (warp 0), broadcast through shared memory
-    if (warp == 0) {
-      // fixed-order fold of the consumer warps' partials across lanes (butterfly)
-      const float mw = lane < FU_NC ? sh.part_m[par][lane] : -INFINITY;
-      const double sw = lane < FU_NC ? sh.part_s[par][lane] : 0.0;
-      const float Mf = warp_max_f(sw > 0.0 ? mw : -INFINITY);
-      double Sr = warp_sum_d(sw > 0.0 ? sw * (double)ex2(mw - Mf) : 0.0);
-      double Mr = Sr > 0.0 ? (double)Mf : -INFINITY;
-      if (lane == 0) {
-      if (CL > 1) {                            // exchange with the peer CTA, fold in rank order
-        sh.mb_m[par][rank] = (float)Mr;
-        sh.mb_s[par][rank] = Sr;
-        mbar_arrive_expect_tx(&sh.mbx[par], 12u);                     // the peer's 4 + 8 bytes
-        const uint32_t peer = rank ^ 1u;
-        const uint32_t rbar = map_rank(&sh.mbx[par], peer);
-        st_async_b32(map_rank(&sh.mb_m[par][rank], peer), __float_as_uint((float)Mr), rbar);
-        st_async_b64(map_rank(&sh.mb_s[par][rank], peer), (uint64_t)__double_as_longlong(Sr), rbar);
-        mbar_wait(&sh.mbx[par], (uint32_t)((nrow >> 1) & 1));
-        Mr = -INFINITY;
-        Sr = 0.0;
-        for (int k2 = 0; k2 < CL; ++k2) {
-          const double Mk = (double)sh.mb_m[par][k2], Sk = sh.mb_s[par][k2];
-          if (Sk == 0.0) continue;
-          if (Mr == -INFINITY) { Mr = Mk; Sr = Sk; continue; }
-          const double mn = fmax(Mr, Mk);
-          Sr = Sr * (double)ex2((float)(Mr - mn)) + Sk * (double)ex2((float)(Mk - mn));
-          Mr = mn;
-        }
-      }
-      const double L2s = log2(Sr);
-      sh.row_g[par] = fused_epilogue(p, t, rc, Mr, L2s, rank == 0);
-      sh.row_nl2[par] = (float)(-(Mr + L2s));
-      }
-    }
-    named_bar_sync(1, FU_NC * 32);
-    const float g = sh.row_g[par], nl2 = sh.row_nl2[par];
-    const int32_t y = rc.y;
-    const float zy = rc.zy;
-    // ---------------- pass 2: gradient over this warp's chunks
+    named_bar_arrive(FU_BAR_PART, FU_BAR_COUNT);
+  };
+
+  // pass 2 over this warp's chunks of row t: dz = -g p (+ g at the target)
+  auto pass2 = [&](int64_t t, float g, float nl2, int32_t y, float zy) {
+    uint8_t* orow = p.dlogits + t * p.ldg_bytes;
     const float2 cc2 = make_float2(c2, c2), nl = make_float2(nl2, nl2), ng = make_float2(-g, -g);
-    for (int64_t ji = 0; ji < cw; ++ji) {
-      const int64_t j = warp + ji * FU_NC;
-      const int64_t idx = (2 * nrow + 1) * cw + ji;
-      const int slot = warp * FU_SW + (int)(idx % FU_SW);
-      mbar_wait(&sh.full[slot], (uint32_t)((idx / FU_SW) & 1));
-      const uint8_t* sp = ring + (size_t)slot * CH_BYTES;
-      const int64_t v0 = (j * CL + rank) * CH_VEC;
-      const int nv = (int)min((int64_t)CH_VEC, nvec - v0);
+    for (uint32_t ji = 0; ji < cw; ++ji) {
+      const int j = warp + (int)ji * FU_NC;
+      const int v0 = (j * CL + (int)rank) * CH_VEC;
+      const int nv = min(CH_VEC, nvec - v0);
       uint4 x[VPL];
+      take(x, nv);
+      if (OUT_BF16 && EPV == 8 && nv == CH_VEC && !(tail_elems && v0 + nv == nvec)) {
+        // full bf16 chunk: no per-vector guards, immediate store offsets from the lane's first vector
+        uint8_t* const olane = orow + (v0 + lane) * OUTV;
 #pragma unroll
-      for (int q = 0; q < VPL; ++q) {
-        const int vi = lane + 32 * q;
-        x[q] = (vi < nv) ? lds128(sp + vi * 16) : make_uint4(0u, 0u, 0u, 0u);
-      }
-      uint32_t dep = 0;
-#pragma unroll
-      for (int q = 0; q < VPL; ++q) dep |= x[q].x | x[q].y | x[q].z | x[q].w;
-      asm volatile("" ::"r"(dep));
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&sh.empty[slot]);
-#pragma unroll
-      for (int q = 0; q < VPL; ++q) {
-        const int vi = lane + 32 * q;
-        if (vi < nv) {
-          const int64_t gv = v0 + vi;
+        for (int q = 0; q < VPL; ++q) {
           float z[EPV], o[EPV];
           unpack<Tin>(x[q], z);
 #pragma unroll
@@ -506,32 +507,51 @@ __global__ void __launch_bounds__(FU_THREADS, DART_FU_CTAS) fused_sweep_kernel(c
             o[e] = dz.x;
             o[e + 1] = dz.y;
           }
-          const int nvalid = (tail_elems && gv == nvec - 1) ? tail_elems : EPV;
-          uint8_t* dst = orow + gv * OUTV;
-          if (nvalid == EPV) {
-            if (OUT_BF16 && EPV == 8) {
-              stg128_cs(dst, make_uint4(pack_bf16x2(o[0], o[1]), pack_bf16x2(o[2], o[3]), pack_bf16x2(o[4], o[5]),
-                                        pack_bf16x2(o[6], o[7])));
-            } else if (OUT_BF16) {
-              *reinterpret_cast<uint2*>(dst) = make_uint2(pack_bf16x2(o[0], o[1]), pack_bf16x2(o[2], o[3]));
-            } else {
+          stg128_cs(olane + q * 32 * OUTV, make_uint4(pack_bf16x2(o[0], o[1]), pack_bf16x2(o[2], o[3]),
+                                                      pack_bf16x2(o[4], o[5]), pack_bf16x2(o[6], o[7])));
+        }
+      } else {
 #pragma unroll
-              for (int e = 0; e < EPV; e += 4)
-                stg128_cs(dst + 4 * e, make_uint4(__float_as_uint(o[e]), __float_as_uint(o[e + 1]),
-                                                  __float_as_uint(o[e + 2]), __float_as_uint(o[e + 3])));
+        for (int q = 0; q < VPL; ++q) {
+          const int vi = lane + 32 * q;
+          if (vi < nv) {
+            const int gv = v0 + vi;
+            float z[EPV], o[EPV];
+            unpack<Tin>(x[q], z);
+#pragma unroll
+            for (int e = 0; e < EPV; e += 2) {
+              const float2 d = __ffma2_rn(make_float2(z[e], z[e + 1]), cc2, nl);
+              const float2 dz = __fmul2_rn(make_float2(ex2(d.x), ex2(d.y)), ng);
+              o[e] = dz.x;
+              o[e + 1] = dz.y;
             }
-          } else {
-            for (int e = 0; e < nvalid; ++e) {
-              if (OUT_BF16) reinterpret_cast<__nv_bfloat16*>(dst)[e] = __float2bfloat16_rn(o[e]);
-              else reinterpret_cast<float*>(dst)[e] = o[e];
+            const int nvalid = (tail_elems && gv == nvec - 1) ? tail_elems : EPV;
+            uint8_t* dst = orow + gv * OUTV;
+            if (nvalid == EPV) {
+              if (OUT_BF16 && EPV == 8) {
+                stg128_cs(dst, make_uint4(pack_bf16x2(o[0], o[1]), pack_bf16x2(o[2], o[3]), pack_bf16x2(o[4], o[5]),
+                                          pack_bf16x2(o[6], o[7])));
+              } else if (OUT_BF16) {
+                *reinterpret_cast<uint2*>(dst) = make_uint2(pack_bf16x2(o[0], o[1]), pack_bf16x2(o[2], o[3]));
+              } else {
+#pragma unroll
+                for (int e = 0; e < EPV; e += 4)
+                  stg128_cs(dst + 4 * e, make_uint4(__float_as_uint(o[e]), __float_as_uint(o[e + 1]),
+                                                    __float_as_uint(o[e + 2]), __float_as_uint(o[e + 3])));
+              }
+            } else {
+              for (int e = 0; e < nvalid; ++e) {
+                if (OUT_BF16) reinterpret_cast<__nv_bfloat16*>(dst)[e] = __float2bfloat16_rn(o[e]);
+                else reinterpret_cast<float*>(dst)[e] = o[e];
+              }
             }
           }
         }
       }
       // target element: g (1 - p_y), rewritten by its owning lane after the vector store
       if (y >= 0 && y < p.V) {
-        const int64_t yv = y / EPV;
-        if (yv >= v0 && yv < v0 + nv && lane == (int)((yv - v0) & 31)) {
+        const int yv = y / EPV;
+        if (yv >= v0 && yv < v0 + nv && lane == ((yv - v0) & 31)) {
           const float py = ex2(fmaf(zy, c2, nl2));
           const float dzy = fmaf(-g, py, g);
           if (OUT_BF16) reinterpret_cast<__nv_bfloat16*>(orow)[y] = __float2bfloat16_rn(dzy);
@@ -539,235 +559,15 @@ __global__ void __launch_bounds__(FU_THREADS, DART_FU_CTAS) fused_sweep_kernel(c
         }
       }
     }
-    ++nrow;
-    par ^= 1;
-  }
-  if (CL > 1) cluster_sync_all();                 // no CTA exits with mailbox traffic pending
-}
-
-// ================================================================ K7 (pipelined)
-// One CTA per SM: FP_NC consumer warps and one reducer warp.  Consumer warps
-// never meet at a CTA barrier: after pass 1 of kept row k each warp publishes
-// its (m, s) partial on an mbarrier and goes on to pass 1 of kept row k+1;
-// the reducer warp folds the partials (and, for split rows, the peer CTA's),
-// runs the row epilogue and publishes g / lse on a second mbarrier, which the
-// consumers wait on one item later, before pass 2 of row k.  Per warp the
-// item order is
-//   P1(k0), P1(k1), P2(k0), P1(k2), P2(k1), ..., P2(kK-1)
-// Each consumer warp streams its own chunks through its own FP_SW-slot ring
-// (lane 0 re-issues a slot's next chunk as soon as the warp holds the current
-// one in registers, as in the bwd sweep), so no warp waits on another's ring.
-// With rows split over a CTA pair each CTA holds two half rows between their
-// passes -- one row per SM, the L2 footprint that keeps pass 2 out of DRAM.
-#ifndef DART_FP_NC
-#define DART_FP_NC 15
-#endif
-#ifndef DART_FP_SW
-#define DART_FP_SW 3
-#endif
-constexpr int FP_NC = DART_FP_NC;                 // consumer warps
-constexpr int FP_SW = DART_FP_SW;                 // ring slots per consumer warp
-constexpr int FP_SLOTS = FP_NC * FP_SW;
-constexpr int FP_REDUCER = FP_NC;
-constexpr int FP_THREADS = (FP_NC + 1) * 32;
-static_assert(FP_NC <= 32, "the reducer folds one partial per lane");
-
-struct PipeShared {
-  uint64_t full[FP_SLOTS];
-  uint64_t pfull[2];   // kept row k's consumer partials are in (FP_NC arrivals), k & 1
-  uint64_t ready[2];   // kept row k's g / lse broadcast is in (1 arrival)
-  uint64_t mbx[2];     // split rows: the peer CTA's row partial has landed (12 tx bytes)
-  double part_s[2][FP_NC];
-  float part_m[2][FP_NC];
-  double mb_s[2][2];
-  float mb_m[2][2];
-  float bc_g[2], bc_nl2[2], bc_zy[2];
-  int32_t bc_y[2];
-};
-
-__device__ __forceinline__ int64_t fp_next_kept(const FusedRec* recs, int64_t t, int64_t rb) {
-  while (t < rb && !(recs[t].flags & 1u)) ++t;
-  return t;
-}
-
-// walker over the item sequence P1(k0), [P1(k+1), P2(k)]..., P2(kK-1) of the
-// kept rows in [ra, rb): row / p1 name the current item; r1 = the last row
-// whose pass 1 has been reached, r2 = the next row due for pass 2
-struct FpSeq {
-  int64_t r1, r2, row;
-  bool p1, valid;
-};
-__device__ __forceinline__ void fpseq_init(FpSeq& q, const FusedRec* recs, int64_t ra, int64_t rb) {
-  const int64_t t = fp_next_kept(recs, ra, rb);
-  q.valid = t < rb;
-  q.row = q.r1 = q.r2 = t;
-  q.p1 = true;
-}
-__device__ __forceinline__ void fpseq_next(FpSeq& q, const FusedRec* recs, int64_t rb) {
-  if (q.p1 && q.row != q.r2) {        // P1(k+1) -> P2(k)
-    q.row = q.r2;
-    q.p1 = false;
-    return;
-  }
-  if (!q.p1) {
-    if (q.row == q.r1) {              // the last row's pass 2
-      q.valid = false;
-      return;
-    }
-    q.r2 = q.r1;
-  }
-  const int64_t t = fp_next_kept(recs, q.r1 + 1, rb);   // the next row's pass 1, else the pending pass 2
-  if (t < rb) {
-    q.r1 = q.row = t;
-    q.p1 = true;
-  } else {
-    q.row = q.r2;
-    q.p1 = false;
-  }
-}
-
-template <typename Tin, typename Tout, int CL>
-__global__ void __launch_bounds__(FP_THREADS, 1) fused_pipe_kernel(const FusedParams p) {
-  extern __shared__ __align__(128) uint8_t smem[];
-  uint8_t* ring = smem;
-  PipeShared& sh = *reinterpret_cast<PipeShared*>(smem + (size_t)FP_SLOTS * CH_BYTES);
-  constexpr int EPV = 16 / sizeof(Tin);
-  constexpr bool OUT_BF16 = sizeof(Tout) == 2;
-  constexpr int64_t OUTV = EPV * (int64_t)sizeof(Tout);
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  if (threadIdx.x == 0) {
-    for (int s = 0; s < FP_SLOTS; ++s) mbar_init(&sh.full[s], 1);
-    for (int b = 0; b < 2; ++b) {
-      mbar_init(&sh.pfull[b], FP_NC);
-      mbar_init(&sh.ready[b], 1);
-      mbar_init(&sh.mbx[b], 1);
-    }
-    fence_mbar_init();
-  }
-  __syncthreads();
-  if (CL > 1) cluster_sync_all();                 // the peer's mailbox exists before any st.async
-
-  const uint32_t rank = CL > 1 ? cluster_rank() : 0u;
-  const int64_t unit = CL > 1 ? (int64_t)cluster_id() : (int64_t)blockIdx.x;
-  const int64_t nb = CL > 1 ? (int64_t)cluster_count() : (int64_t)gridDim.x;
-  const int64_t total = p.step_cost[p.S_loc];
-  const int64_t ra = fu_row_at_cost(p, (total * unit) / nb);
-  const int64_t rb = fu_row_at_cost(p, (total * (unit + 1)) / nb);
-  const int64_t nvec = p.nvec;
-  const int64_t nch = (p.nch - (int64_t)rank + CL - 1) / CL;   // local chunk jl <-> row chunk jl * CL + rank
-  const float c2 = p.c2;
-  const int tail_elems = (int)(p.V % EPV);
-  const FusedRec* recs = reinterpret_cast<const FusedRec*>(p.rec);
-
-  if (warp == FP_REDUCER) {
-    // ===================== reducer warp: fold, exchange, epilogue, broadcast
-    int64_t k = 0;
-    for (int64_t tk = fp_next_kept(recs, ra, rb); tk < rb; tk = fp_next_kept(recs, tk + 1, rb), ++k) {
-      const int par = (int)(k & 1);
-      const uint32_t ph = (uint32_t)((k >> 1) & 1);
-      mbar_wait(&sh.pfull[par], ph);
-      // fixed-order fold of the consumer warps' partials (one per lane, xor butterfly)
-      const float mw = lane < FP_NC ? sh.part_m[par][lane] : -INFINITY;
-      const double sw = lane < FP_NC ? sh.part_s[par][lane] : 0.0;
-      const float Mf = warp_max_f(sw > 0.0 ? mw : -INFINITY);
-      double Sr = warp_sum_d(sw > 0.0 ? sw * (double)ex2(mw - Mf) : 0.0);
-      double Mr = Sr > 0.0 ? (double)Mf : -INFINITY;
-      if (lane == 0) {
-        const FusedRec rc = recs[tk];
-        if (CL > 1) {                          // exchange with the peer CTA, fold in rank order
-          sh.mb_m[par][rank] = (float)Mr;
-          sh.mb_s[par][rank] = Sr;
-          mbar_arrive_expect_tx(&sh.mbx[par], 12u);                     // the peer's 4 + 8 bytes
-          const uint32_t peer = rank ^ 1u;
-          const uint32_t rbar = map_rank(&sh.mbx[par], peer);
-          st_async_b32(map_rank(&sh.mb_m[par][rank], peer), __float_as_uint((float)Mr), rbar);
-          st_async_b64(map_rank(&sh.mb_s[par][rank], peer), (uint64_t)__double_as_longlong(Sr), rbar);
-          mbar_wait(&sh.mbx[par], ph);
-          Mr = -INFINITY;
-          Sr = 0.0;
-          for (int k2 = 0; k2 < CL; ++k2) {
-            const double Mk = (double)sh.mb_m[par][k2], Sk = sh.mb_s[par][k2];
-            if (Sk == 0.0) continue;
-            if (Mr == -INFINITY) { Mr = Mk; Sr = Sk; continue; }
-            const double mn = fmax(Mr, Mk);
-            Sr = Sr * (double)ex2((float)(Mr - mn)) + Sk * (double)ex2((float)(Mk - mn));
-            Mr = mn;
-          }
-        }
-        const double L2s = log2(Sr);
-        sh.bc_g[par] = fused_epilogue(p, tk, rc, Mr, L2s, rank == 0);
-        sh.bc_nl2[par] = (float)(-(Mr + L2s));
-        sh.bc_y[par] = rc.y;
-        sh.bc_zy[par] = rc.zy;
-        mbar_arrive(&sh.ready[par]);
-      }
-      __syncwarp();
-    }
-    if (CL > 1) cluster_sync_all();                 // no CTA exits with mailbox traffic pending
-    return;
-  }
-
-  // ===================== consumers (FP_NC warps), each with its own ring
-  const int64_t cw = (nch - warp + FP_NC - 1) / FP_NC;   // this warp's chunks per item (local j = warp + ji * FP_NC)
-  uint64_t* const full = sh.full + warp * FP_SW;
-  uint8_t* const wring = ring + (size_t)warp * FP_SW * CH_BYTES;
-  uint64_t pol_last, pol_first;
-  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol_last));
-  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol_first));
-
-  // issue cursor: runs FP_SW chunks ahead of consumption, always into the slot just drained
-  FpSeq is;
-  fpseq_init(is, recs, ra, rb);
-  int64_t iji = 0;
-  if (cw == 0) is.valid = false;
-  auto issue = [&](int s) {
-    const int64_t j = warp + iji * FP_NC;
-    const int64_t v0 = (j * CL + rank) * CH_VEC;
-    const uint32_t nv = (uint32_t)min((int64_t)CH_VEC, nvec - v0);
-    if (lane == 0) {
-      mbar_arrive_expect_tx(&full[s], nv * 16u);
-      // pass 1 evict_last (the row must survive in L2 until pass 2), pass 2 evict_first
-      bulk_g2s_hint(wring + (size_t)s * CH_BYTES, p.logits + is.row * p.ld_bytes + v0 * 16, nv * 16u, &full[s],
-                    is.p1 ? pol_last : pol_first);
-    }
-    if (++iji == cw) {
-      iji = 0;
-      fpseq_next(is, recs, rb);
-    }
-  };
-#pragma unroll 1
-  for (int s = 0; s < FP_SW && is.valid; ++s) issue(s);
-
-  int slot = 0;
-  uint32_t phase = 0;
-  uint32_t bad = 0;
-  // the chunk at the head of this warp's ring: wait, pull into registers, hand the slot to the next chunk
-  auto take = [&](uint4 (&x)[VPL], int nv) {
-    mbar_wait(&full[slot], phase);
-    const uint8_t* sp = wring + (size_t)slot * CH_BYTES;
-#pragma unroll
-    for (int q = 0; q < VPL; ++q) {
-      const int vi = lane + 32 * q;
-      x[q] = (vi < nv) ? lds128(sp + vi * 16) : make_uint4(0u, 0u, 0u, 0u);
-    }
-    uint32_t dep = 0;
-#pragma unroll
-    for (int q = 0; q < VPL; ++q) dep |= x[q].x | x[q].y | x[q].z | x[q].w;
-    asm volatile("" ::"r"(dep));
-    __syncwarp();
-    if (is.valid) issue(slot);
-    if (++slot == FP_SW) {
-      slot = 0;
-      phase ^= 1u;
-    }
   };
 
-  auto zero_rows = [&](int64_t t0, int64_t t1) {         // masked steps: zeros, no read
+  // masked steps: zeros, no read; the consumer warps split this CTA's chunks of each row
+  auto zero_rows = [&](int64_t t0, int64_t t1) {
     if (!p.zero_fill) return;
     for (int64_t t = t0; t < t1; ++t) {
       uint8_t* orow = p.dlogits + t * p.ldg_bytes;
-      for (int64_t li = (int64_t)warp * 32 + lane; li < nch * CH_VEC; li += FP_NC * 32) {
-        const int64_t vi = ((li / CH_VEC) * CL + rank) * CH_VEC + (li % CH_VEC);
+      for (int li = warp * 32 + lane; li < nch * CH_VEC; li += FU_NC * 32) {
+        const int vi = ((li / CH_VEC) * CL + (int)rank) * CH_VEC + (li % CH_VEC);
         if (vi >= nvec) continue;
         const int nvalid = (tail_elems && vi == nvec - 1) ? tail_elems : EPV;
         uint8_t* dst = orow + vi * OUTV;
@@ -786,181 +586,20 @@ __global__ void __launch_bounds__(FP_THREADS, 1) fused_pipe_kernel(const FusedPa
     }
   };
 
-  // pass 1 over this warp's chunks of the row: online max / sum -> the reducer (partial slot par)
-  auto pass1 = [&](int par) {
+  int64_t tk = fu_next_kept(recs, ra, rb);
+  zero_rows(ra, tk);
+  while (tk < rb) {
     float m = NEG_CLAMP * c2;
     float2 s01 = make_float2(0.f, 0.f), s23 = make_float2(0.f, 0.f);
-#pragma unroll 1
-    for (int64_t ji = 0; ji < cw; ++ji) {
-      const int64_t v0 = ((warp + ji * FP_NC) * CL + rank) * CH_VEC;
-      const int nv = (int)min((int64_t)CH_VEC, nvec - v0);
-      uint4 x[VPL];
-      take(x, nv);
-      const bool tail_chunk = tail_elems && v0 + nv == nvec;
-      if (sizeof(Tin) == 2 && nv == CH_VEC && !tail_chunk) {
-        // fast path: packed bf16x2 max, one unpack per pair; -inf logits give 2^-inf = 0
-        uint32_t mx = 0xff80ff80u;
-#pragma unroll
-        for (int q = 0; q < VPL; ++q) {
-          mx = bmax2_nan(mx, x[q].x);
-          mx = bmax2_nan(mx, x[q].y);
-          mx = bmax2_nan(mx, x[q].z);
-          mx = bmax2_nan(mx, x[q].w);
-        }
-        const float cmr = fmax_nan(bf16lo(mx), bf16hi(mx));
-        if (!(cmr < INFINITY)) bad |= DART_STATUS_NONFINITE_LOGIT;
-        const float cms = cmr * c2;
-        if (cms > m + 2.0f) {   // lazy running max (LAZY_M = 2, as in the fwd sweep)
-          const float sc = ex2(m - cms);
-          s01 = __fmul2_rn(s01, make_float2(sc, sc));
-          s23 = __fmul2_rn(s23, make_float2(sc, sc));
-          m = cms;
-        }
-        const float2 cc = make_float2(c2, c2), nm = make_float2(-m, -m);
-#pragma unroll
-        for (int q = 0; q < VPL; ++q) {
-          const float2 d0 = __ffma2_rn(make_float2(bf16lo(x[q].x), bf16hi(x[q].x)), cc, nm);
-          const float2 d1 = __ffma2_rn(make_float2(bf16lo(x[q].y), bf16hi(x[q].y)), cc, nm);
-          const float2 d2 = __ffma2_rn(make_float2(bf16lo(x[q].z), bf16hi(x[q].z)), cc, nm);
-          const float2 d3 = __ffma2_rn(make_float2(bf16lo(x[q].w), bf16hi(x[q].w)), cc, nm);
-          s01 = __fadd2_rn(s01, make_float2(ex2(d0.x), ex2(d0.y)));
-          s23 = __fadd2_rn(s23, make_float2(ex2(d1.x), ex2(d1.y)));
-          s01 = __fadd2_rn(s01, make_float2(ex2(d2.x), ex2(d2.y)));
-          s23 = __fadd2_rn(s23, make_float2(ex2(d3.x), ex2(d3.y)));
-        }
-        continue;
-      }
-      float cm = -INFINITY;
-#pragma unroll
-      for (int q = 0; q < VPL; ++q) {
-        const int vi = lane + 32 * q;
-        if (vi < nv) {
-          float z[EPV];
-          unpack<Tin>(x[q], z);
-#pragma unroll
-          for (int e = 0; e < EPV; ++e) {
-            if (tail_chunk && vi == nv - 1 && e >= tail_elems) z[e] = NEG_CLAMP;
-            cm = fmax_nan(cm, z[e]);
-          }
-        }
-      }
-      if (!(cm < INFINITY)) bad |= DART_STATUS_NONFINITE_LOGIT;
-      const float cms = fmaxf(cm, NEG_CLAMP) * c2;
-      if (cms > m + 2.0f) {
-        const float sc = ex2(m - cms);
-        s01 = __fmul2_rn(s01, make_float2(sc, sc));
-        s23 = __fmul2_rn(s23, make_float2(sc, sc));
-        m = cms;
-      }
-      const float2 cc = make_float2(c2, c2), nm = make_float2(-m, -m);
-#pragma unroll
-      for (int q = 0; q < VPL; ++q) {
-        const int vi = lane + 32 * q;
-        if (vi < nv) {
-          float z[EPV];
-          unpack<Tin>(x[q], z);
-#pragma unroll
-          for (int e = 0; e < EPV; ++e) {
-            if (tail_chunk && vi == nv - 1 && e >= tail_elems) z[e] = NEG_CLAMP;
-            z[e] = fmaxf(z[e], NEG_CLAMP);   // -inf logits contribute exp -> 0
-          }
-#pragma unroll
-          for (int e = 0; e < EPV; e += 4) {
-            const float2 d0 = __ffma2_rn(make_float2(z[e], z[e + 1]), cc, nm);
-            const float2 d1 = __ffma2_rn(make_float2(z[e + 2], z[e + 3]), cc, nm);
-            s01 = __fadd2_rn(s01, make_float2(ex2(d0.x), ex2(d0.y)));
-            s23 = __fadd2_rn(s23, make_float2(ex2(d1.x), ex2(d1.y)));
-          }
-        }
-      }
-    }
-    // warp partial (fixed lane fold) -> the reducer
-    const float M = warp_max_f(m);
-    const float sl = (s01.x + s01.y) + (s23.x + s23.y);
-    const double sd = warp_sum_d((double)sl * (double)ex2(m - M));
-    if (lane == 0) {
-      sh.part_m[par][warp] = M;
-      sh.part_s[par][warp] = sd;
-      mbar_arrive(&sh.pfull[par]);
-    }
-  };
-
-  // pass 2 over this warp's chunks of row t: dz = -g p (+ g at the target)
-  auto pass2 = [&](int64_t t, float g, float nl2, int32_t y, float zy) {
-    uint8_t* orow = p.dlogits + t * p.ldg_bytes;
-    const float2 cc2 = make_float2(c2, c2), nl = make_float2(nl2, nl2), ng = make_float2(-g, -g);
-#pragma unroll 1
-    for (int64_t ji = 0; ji < cw; ++ji) {
-      const int64_t v0 = ((warp + ji * FP_NC) * CL + rank) * CH_VEC;
-      const int nv = (int)min((int64_t)CH_VEC, nvec - v0);
-      uint4 x[VPL];
-      take(x, nv);
-#pragma unroll
-      for (int q = 0; q < VPL; ++q) {
-        const int vi = lane + 32 * q;
-        if (vi < nv) {      // each vector's math and store stay together (the bwd sweep's measured shape)
-          const int64_t gv = v0 + vi;
-          float z[EPV], o[EPV];
-          unpack<Tin>(x[q], z);
-#pragma unroll
-          for (int e = 0; e < EPV; e += 2) {
-            const float2 d = __ffma2_rn(make_float2(z[e], z[e + 1]), cc2, nl);
-            const float2 dz = __fmul2_rn(make_float2(ex2(d.x), ex2(d.y)), ng);
-            o[e] = dz.x;
-            o[e + 1] = dz.y;
-          }
-          const int nvalid = (tail_elems && gv == nvec - 1) ? tail_elems : EPV;
-          uint8_t* dst = orow + gv * OUTV;
-          if (nvalid == EPV) {
-            if (OUT_BF16 && EPV == 8) {
-              stg128_cs(dst, make_uint4(pack_bf16x2(o[0], o[1]), pack_bf16x2(o[2], o[3]), pack_bf16x2(o[4], o[5]),
-                                        pack_bf16x2(o[6], o[7])));
-            } else if (OUT_BF16) {
-              *reinterpret_cast<uint2*>(dst) = make_uint2(pack_bf16x2(o[0], o[1]), pack_bf16x2(o[2], o[3]));
-            } else {
-#pragma unroll
-              for (int e = 0; e < EPV; e += 4)
-                stg128_cs(dst + 4 * e, make_uint4(__float_as_uint(o[e]), __float_as_uint(o[e + 1]),
-                                                  __float_as_uint(o[e + 2]), __float_as_uint(o[e + 3])));
-            }
-          } else {
-            for (int e = 0; e < nvalid; ++e) {
-              if (OUT_BF16) reinterpret_cast<__nv_bfloat16*>(dst)[e] = __float2bfloat16_rn(o[e]);
-              else reinterpret_cast<float*>(dst)[e] = o[e];
-            }
-          }
-        }
-      }
-      // target element: g (1 - p_y), rewritten by its owning lane after the vector store
-      if (y >= 0 && y < p.V) {
-        const int64_t yv = y / EPV;
-        if (yv >= v0 && yv < v0 + nv && lane == (int)((yv - v0) & 31)) {
-          const float py = ex2(fmaf(zy, c2, nl2));
-          const float dzy = fmaf(-g, py, g);
-          if (OUT_BF16) reinterpret_cast<__nv_bfloat16*>(orow)[y] = __float2bfloat16_rn(dzy);
-          else reinterpret_cast<float*>(orow)[y] = dzy;
-        }
-      }
-    }
-  };
-
-  FpSeq cs;
-  fpseq_init(cs, recs, ra, rb);
-  zero_rows(ra, cs.row);
-  int64_t k1 = 0, k2 = 0;      // pass-1 / pass-2 items done (kept-row ordinals)
-#pragma unroll 1
-  while (cs.valid) {
-    if (cs.p1) {
-      pass1((int)(k1 & 1));
-      ++k1;
-    } else {
-      const int par = (int)(k2 & 1);
-      mbar_wait(&sh.ready[par], (uint32_t)((k2 >> 1) & 1));
-      pass2(cs.row, sh.bc_g[par], sh.bc_nl2[par], sh.bc_y[par], sh.bc_zy[par]);
-      zero_rows(cs.row + 1, fp_next_kept(recs, cs.row + 1, rb));
-      ++k2;
-    }
-    fpseq_next(cs, recs, rb);
+    pass1(0u, cw, m, s01, s23);
+    publish(m, s01, s23);                            // non-blocking: the reducer folds
+    named_bar_sync(FU_BAR_ROW, FU_BAR_COUNT);       // row tk's g / lse
+    const float g = sh.row_g, nl2 = sh.row_nl2, zy = sh.row_zy;
+    const int32_t y = sh.row_y;
+    pass2(tk, g, nl2, y, zy);
+    const int64_t tn = fu_next_kept(recs, tk + 1, rb);
+    zero_rows(tk + 1, tn);
+    tk = tn;
   }
   bad = warp_or(bad);
   if (lane == 0 && bad) status_or(p.status, bad);
@@ -976,7 +615,7 @@ cudaError_t launch_fused_rec(const FusedParams& p, cudaStream_t st) {
 }
 
 template <typename Tin, typename Tout>
-static cudaError_t launch_fused_old_t(const FusedParams& p, int num_sms, bool split, cudaStream_t st) {
+static cudaError_t launch_fused_t(const FusedParams& p, int num_sms, bool split, cudaStream_t st) {
   const size_t smem = (size_t)FU_SLOTS * CH_BYTES + sizeof(FusedShared);
   if (!split) {
     auto kern = fused_sweep_kernel<Tin, Tout, 1>;
@@ -1004,44 +643,6 @@ static cudaError_t launch_fused_old_t(const FusedParams& p, int num_sms, bool sp
   if (cudaOccupancyMaxActiveClusters(&n, kern, &cfg) != cudaSuccess || n <= 0) {
     (void)cudaGetLastError();
     n = num_sms * DART_FU_CTAS / 2;
-  }
-  cfg.gridDim = dim3((unsigned)(2 * n));
-  return cudaLaunchKernelEx(&cfg, kern, p);
-}
-
-#ifndef DART_FUSED_PIPE
-#define DART_FUSED_PIPE 0
-#endif
-template <typename Tin, typename Tout>
-static cudaError_t launch_fused_t(const FusedParams& p, int num_sms, bool split, cudaStream_t st) {
-  if (!DART_FUSED_PIPE) return launch_fused_old_t<Tin, Tout>(p, num_sms, split, st);
-  const size_t smem = (size_t)FP_SLOTS * CH_BYTES + sizeof(PipeShared);
-  if (!split) {
-    auto kern = fused_pipe_kernel<Tin, Tout, 1>;
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    kern<<<(unsigned)num_sms, FP_THREADS, smem, st>>>(p);
-    return cudaGetLastError();
-  }
-  auto kern = fused_pipe_kernel<Tin, Tout, 2>;
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (e != cudaSuccess) return e;
-  cudaLaunchConfig_t cfg = {};
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = 2;
-  attr[0].val.clusterDim.y = 1;
-  attr[0].val.clusterDim.z = 1;
-  cfg.blockDim = dim3(FP_THREADS);
-  cfg.dynamicSmemBytes = smem;
-  cfg.stream = st;
-  cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  cfg.gridDim = dim3((unsigned)num_sms);
-  int n = 0;
-  if (cudaOccupancyMaxActiveClusters(&n, kern, &cfg) != cudaSuccess || n <= 0) {
-    (void)cudaGetLastError();
-    n = num_sms / 2;
   }
   cfg.gridDim = dim3((unsigned)(2 * n));
   return cudaLaunchKernelEx(&cfg, kern, p);

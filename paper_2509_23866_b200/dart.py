@@ -31,7 +31,7 @@ STATUS_BITS = {
     1 << 0: "NONFINITE_LOGIT", 1 << 1: "TARGET_RANGE", 1 << 2: "ROW_ALL_NEGINF",
     1 << 3: "NONFINITE_LOGP", 1 << 4: "EMPTY", 1 << 5: "BAD_CSR", 1 << 6: "TARGET_NEGINF",
 }
-ABI_VERSION = 5
+ABI_VERSION = 6
 RATIO_TOKEN, RATIO_STEP = 0, 1
 KL_K3, KL_EXACT = 0, 1
 
@@ -79,7 +79,8 @@ _lib = None
 
 EXPORTED = ["dart_workspace_size", "dart_loss_fwd", "dart_select_steps", "dart_loss_bwd", "dart_loss_fused",
             "dart_loss_pass", "dart_lmhead_workspace_size", "dart_lmhead_fwd", "dart_lmhead_bwd",
-            "dart_status_str", "dart_abi_version", "dart_last_launch_count", "dart_set_timing_events"]
+            "dart_status_str", "dart_abi_version", "dart_last_launch_count", "dart_set_timing_events",
+            "dart_rollout_counts", "dart_trajectory_caps", "dart_curate_batch"]
 
 
 class DartError(RuntimeError):
@@ -135,6 +136,9 @@ def lib():
     L.dart_last_launch_count.restype = ctypes.c_int32
     L.dart_set_timing_events.restype = None
     L.dart_set_timing_events.argtypes = [ctypes.c_void_p] * 4
+    # host-side curation (paper_2509_23866_b200/curation.py marshals)
+    for n in ("dart_rollout_counts", "dart_trajectory_caps", "dart_curate_batch"):
+        getattr(L, n).restype = ctypes.c_int
     if L.dart_abi_version() != ABI_VERSION:
         raise DartError(f"libdart_loss ABI {L.dart_abi_version()} != binding {ABI_VERSION}")
     _lib = L

@@ -127,6 +127,43 @@ def real_rewards(groups, rng):
     return list(rng.random(sum(len(l) for l in groups)))
 
 
+# ---------------------------------------------------------------- curation inputs
+def make_curation_inputs(G, seed=0, tok_lo=16, tok_hi=128, max_len=60, pool_max=3):
+    """Seeded raw inputs of one curation round (§4.1-4.2 workload,
+    no curation arithmetic here): per task a success history (n_success,
+    n_total), the historical max successful length (-1 = none), this
+    iteration's rollouts as (per-step token counts, reward) with up to
+    `max_len` steps, a pool of stored successes and one uniform draw per
+    task.  Roughly a third of the tasks are hard (every rollout fails), a
+    third easy (success rate above 0.6)."""
+    rng = np.random.default_rng(seed * 7919 + 5)
+    kind = rng.integers(0, 3, size=G)                 # 0 hard, 1 medium, 2 easy
+    p_succ = np.where(kind == 0, 0.0, np.where(kind == 1, rng.uniform(0.2, 0.6, G), rng.uniform(0.65, 1.0, G)))
+    n_total = rng.integers(0, 64, size=G)
+    n_success = np.asarray([int(rng.binomial(n, p)) for n, p in zip(n_total, p_succ)], dtype=np.int64)
+    max_succ = np.where(n_success > 0, rng.integers(3, 70, size=G), -1).astype(np.int32)
+    def traj(success):
+        L = int(rng.integers(1, max_len + 1))
+        return [int(x) for x in rng.integers(tok_lo, tok_hi + 1, size=L)], (1.0 if success else 0.0)
+    def rollouts(n, p):
+        return [traj(rng.random() < p) for _ in range(int(n))]
+    pool = [[traj(True) for _ in range(int(rng.integers(0, pool_max + 1)))] for _ in range(G)]
+    draws = rng.random(G)
+    return dict(n_success=n_success, n_total=n_total.astype(np.int64), max_success_len=max_succ,
+                p_succ=p_succ, make_rollouts=rollouts, pool=pool, pool_draw=draws, rng=rng)
+
+
+def layout_from_csr(G, traj_group, traj_reward, traj_step_off, step_tok_off, seed=0, fork_frac=0.3):
+    """A Layout over given CSR metadata (e.g. a curated batch); only the
+    generator's step types are drawn here."""
+    rng = np.random.default_rng(seed * 31 + 3)
+    S = len(step_tok_off) - 1
+    return Layout(G=int(G), traj_group=np.asarray(traj_group, dtype=np.int32),
+                  traj_reward=np.asarray(traj_reward, dtype=np.float32),
+                  traj_step_off=np.asarray(traj_step_off, dtype=np.int64),
+                  step_tok_off=np.asarray(step_tok_off, dtype=np.int64), step_fork=rng.random(S) < fork_frac)
+
+
 # ---------------------------------------------------------------- configs
 # name -> (groups-builder, tokens-per-step builder, V, dtype, is_cap)
 def config_layout(name, seed=0, real_reward=False):

@@ -47,7 +47,7 @@ def test_sm100a_cubin_inside():
 
 def test_version_and_status_strings(L):
     from paper_2509_23866_b200 import dart
-    assert L.dart_abi_version() == dart.ABI_VERSION == 5
+    assert L.dart_abi_version() == dart.ABI_VERSION == 6
     for c in range(5):
         assert L.dart_status_str(c).startswith(b"DART_")
     assert L.dart_status_str(99) == b"DART_UNKNOWN_STATUS"
