@@ -1029,7 +1029,7 @@ def lmhead_cpu_baseline(args, lb, cfg, rows=64):
     else:
         work()
     dt = time.time() - t0
-    return {"value": rows / dt, "unit": "tokens/s", "cores": 1, "kind": "oracle",
+    return {"value": rows / dt, "unit": "tokens/s", "cores": 1, "cpu_model": cpu_model(), "kind": "oracle",
             "sample": f"{rows} tokens: float64 h W^T (d={h.shape[1]}, V={W.shape[0]}) + per-token log-softmax / "
                       f"entropy, NumPy with BLAS limited to 1 thread", "seconds": dt}
 
@@ -1125,6 +1125,8 @@ def oracle_sample(batch, n_traj=None, max_tokens=1024, group=0):
              logp_rollout=batch.logp_rollout[rows_t].cpu().numpy().astype(np.float64),
              logp_ref=batch.logp_ref[rows_t].cpu().numpy().astype(np.float64),
              logits=batch.logits[rows_t].float().cpu().numpy())
+    if batch.ref_logits is not None:        # exact-KL workload: the reference policy's logits too
+        d["ref_logits"] = batch.ref_logits[rows_t].float().cpu().numpy()
     return d, len(rows), len(lens), len(sto2) - 1
 
 
