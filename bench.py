@@ -1246,9 +1246,10 @@ def run_reference(args):
     from paper_2509_23866_b200 import dart, synth
     layout_r, V, dtype, _ = synth.config_layout(args.config, seed=args.seed)
     # generate only the sample's rows on the CPU (identical recipe)
+    exact = args.kl == "exact"
     batch = synth.make_batch(args.config, seed=args.seed * 1000, device="cpu", layout=_first_traj_layout(layout_r),
-                             V=V, dtype=dtype)
-    cfg = dart.Config(entropy_q=args.q, beta_kl=args.beta)
+                             V=V, dtype=dtype, with_ref=exact)
+    cfg = dart.Config(entropy_q=args.q, beta_kl=args.beta, kl_mode=dart.KL_EXACT if exact else dart.KL_K3)
     d, ntok1, ntraj, nstep = oracle_sample(batch, max_tokens=args.cpu_tokens)
     procs = oracle_procs(ntok1 * V * 4) if args.cpu_procs <= 0 else args.cpu_procs
     pool = OraclePool([d] * procs, cfg.as_f32(), procs)      # the same sample on every core

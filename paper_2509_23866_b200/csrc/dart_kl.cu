@@ -217,20 +217,11 @@ fwd_kl_kernel(const FwdParams p) {
       mbar_wait(&bars[slot], phase);
       const uint8_t* sp = ring + (size_t)slot * CH_BYTES;
       uint4 xz[KVPL], xr[KVPL];
-      const bool full = nv == KV && !(tail_elems && v0 + nv == nvec);
-      if (full) {             // full chunk: unpredicated loads, nothing to sanitize
 #pragma unroll
-        for (int q = 0; q < KVPL; ++q) {
-          xz[q] = lds128(sp + (lane + 32 * q) * 16);
-          xr[q] = lds128(sp + KV * 16 + (lane + 32 * q) * 16);
-        }
-      } else {
-#pragma unroll
-        for (int q = 0; q < KVPL; ++q) {
-          const int vi = lane + 32 * q;
-          xz[q] = (vi < nv) ? lds128(sp + vi * 16) : make_uint4(0u, 0u, 0u, 0u);
-          xr[q] = (vi < nv) ? lds128(sp + KV * 16 + vi * 16) : make_uint4(0u, 0u, 0u, 0u);
-        }
+      for (int q = 0; q < KVPL; ++q) {
+        const int vi = lane + 32 * q;
+        xz[q] = (vi < nv) ? lds128(sp + vi * 16) : make_uint4(0u, 0u, 0u, 0u);
+        xr[q] = (vi < nv) ? lds128(sp + KV * 16 + vi * 16) : make_uint4(0u, 0u, 0u, 0u);
       }
       uint32_t dep = 0;
 #pragma unroll
@@ -240,16 +231,14 @@ fwd_kl_kernel(const FwdParams p) {
       if (prow < p.T_loc) issue(slot);
       if (++slot == STAGES) { slot = 0; phase ^= 1u; }
       // sanitize: vectors past nv and logits past V become NEG_CLAMP (exp -> 0)
-      if (!full) {
 #pragma unroll
-        for (int q = 0; q < KVPL; ++q) {
-          const int vi = lane + 32 * q;
-          if (vi >= nv) {
-            xz[q] = xr[q] = neg_clamp_vec<Tin>();
-          } else if (tail_elems && v0 + vi == nvec - 1) {
-            mask_tail<Tin>(xz[q], tail_elems);
-            mask_tail<Tin>(xr[q], tail_elems);
-          }
+      for (int q = 0; q < KVPL; ++q) {
+        const int vi = lane + 32 * q;
+        if (vi >= nv) {
+          xz[q] = xr[q] = neg_clamp_vec<Tin>();
+        } else if (tail_elems && v0 + vi == nvec - 1) {
+          mask_tail<Tin>(xz[q], tail_elems);
+          mask_tail<Tin>(xr[q], tail_elems);
         }
       }
       float cm, cmr;

@@ -87,6 +87,16 @@ def test_fused_odd_vocab_and_norm_modes():
                     dtype=torch.bfloat16, pad_ld=1008)
 
 
+def test_fused_split_rows_odd_vocab():
+    """Rows split over the CTA pair (>= 2 chunks per row) with a vocabulary
+    tail inside the last vector: V = 4099 bf16 (3 chunks: CTA 0 takes 2, CTA 1
+    one; most consumer warps own no chunk and publish empty partials)."""
+    layout, _, _, _ = synth.config_layout("small_multi", seed=2)
+    _fused_case("small_multi", dart.Config(), seed=2, layout=layout, V=4099, dtype=torch.bfloat16, pad_ld=4104)
+    _fused_case("small_multi", dart.Config(beta_kl=0.0), seed=3, layout=layout, V=40003, dtype=torch.bfloat16,
+                pad_ld=40008)
+
+
 def test_fused_matches_two_pass_gradient_closely():
     """Same mask and inputs: the fused call and fwd+bwd differ only by the
     lse reduction order (bf16 gradients within 1 ulp)."""
