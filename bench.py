@@ -567,7 +567,8 @@ def run_dart(args):
     # ---- e2e through the public API with host buffers (pinned), rank-local
     e2e = None
     if not args.no_e2e:
-        e2e = run_e2e(args, dl, batch, stream, world, inputs)
+        ok, why = e2e_host_memory_ok(inputs, world)
+        e2e = run_e2e(args, dl, batch, stream, world, inputs) if ok else {"skipped": why}
 
     # ---- CPU oracle baseline (rank 0, N == 1 only)
     cpu = None
@@ -1032,6 +1033,30 @@ def lmhead_cpu_baseline(args, lb, cfg, rows=64):
     return {"value": rows / dt, "unit": "tokens/s", "cores": 1, "cpu_model": cpu_model(), "kind": "oracle",
             "sample": f"{rows} tokens: float64 h W^T (d={h.shape[1]}, V={W.shape[0]}) + per-token log-softmax / "
                       f"entropy, NumPy with BLAS limited to 1 thread", "seconds": dt}
+
+
+def e2e_host_memory_ok(inputs, world):
+    """The e2e leg pins every rank's step inputs in host memory (18.7 GB per
+    rank at the single config).  Run it only if all ranks of this host fit in
+    70% of the available host memory -- the same decision on every rank (a
+    MIN all-reduce), so no rank waits in a collective another one skipped."""
+    need = sum(t.numel() * t.element_size() for t in inputs)
+    local = int(os.environ.get("LOCAL_WORLD_SIZE", str(world)))
+    try:
+        import psutil
+        avail = psutil.virtual_memory().available
+    except Exception:
+        avail = None
+    ok = avail is None or need * local <= 0.7 * avail
+    if world > 1:
+        import torch.distributed as dist
+        from paper_2509_23866_b200 import dist as D
+        t = torch.tensor([1 if ok else 0], dtype=torch.int32, device=inputs[0].device)
+        D.all_reduce(t, op=dist.ReduceOp.MIN)
+        ok = bool(t.item())
+    why = None if ok else (f"host memory: {local} ranks x {need / 1e9:.1f} GB pinned inputs > 70% of "
+                           f"{(avail or 0) / 1e9:.0f} GB available")
+    return ok, why
 
 
 def run_e2e(args, dl, batch, stream, world, inputs):

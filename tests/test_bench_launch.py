@@ -60,3 +60,21 @@ def test_weak_layouts_per_rank_blocks():
     assert np.array_equal(lays[0].step_tok_off, L0.step_tok_off)
     assert not np.array_equal(lays[0].traj_reward, lays[1].traj_reward[:len(lays[0].traj_reward)]) \
         or len(lays[0].traj_reward) != len(lays[1].traj_reward)
+
+
+def test_e2e_host_memory_guard():
+    """The e2e leg is skipped (not run into an OOM) when the ranks' pinned
+    inputs would not fit in host memory; small inputs always run."""
+    import importlib.util
+    import torch
+    spec = importlib.util.spec_from_file_location("bench_mod", os.path.join(ROOT, "bench.py"))
+    bench = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(bench)
+    ok, why = bench.e2e_host_memory_ok([torch.zeros(1024)], 1)
+    assert ok and why is None
+    os.environ["LOCAL_WORLD_SIZE"] = str(10 ** 9)     # pretend a billion ranks share this host
+    try:
+        ok, why = bench.e2e_host_memory_ok([torch.zeros(1 << 20)], 1)
+    finally:
+        del os.environ["LOCAL_WORLD_SIZE"]
+    assert not ok and "host memory" in why
