@@ -608,7 +608,7 @@ dart_status dart_loss_bwd(const dart_batch* b, const dart_meta* m, const dart_cf
   DART_TRY(launch_bwd_prep(pp, s));
 
   if (b->T_loc > 0 && !loss_only) {
-    RowRecParams rp;
+    RowRecParams rp = {};
     rp.T_loc = b->T_loc; rp.V = b->V; rp.ld_bytes = b->ld * (int64_t)es;
     rp.is_bf16 = b->logits_dtype == DART_BF16;
     rp.logits = static_cast<const uint8_t*>(b->logits);
