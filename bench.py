@@ -1248,16 +1248,21 @@ def cpu_baseline(args, batch, cfg):
     procs = oracle_procs(per * batch.V * 4) if args.cpu_procs <= 0 else args.cpu_procs
     samples, ntok = oracle_samples(batch, per, procs)
     pool = OraclePool(samples, cfg.as_f32(), procs)
+    # bounded CPU work of about args.cpu_seconds: the concurrent samples are
+    # re-run until that much wall time has passed (at most 8 rounds)
+    dt, rounds = 0.0, 0
     try:
-        dt = pool.run()
+        while rounds < 8 and (rounds == 0 or dt < args.cpu_seconds):
+            dt += pool.run()
+            rounds += 1
     finally:
         pool.close()
-    return {"value": ntok / dt, "unit": "logit-tokens/s", "cores": procs, "cpu_model": cpu_model(),
+    return {"value": ntok * rounds / dt, "unit": "logit-tokens/s", "cores": procs, "cpu_model": cpu_model(),
             "host_cores": os.cpu_count(), "kind": "oracle",
             "sample": f"{procs} independent samples run concurrently, one per process, each <= {per} tokens "
-                      f"of whole steps of one task group (groups cycled; {ntok} tokens in all, V={batch.V}); "
-                      f"full fwd+select+bwd incl. dlogits, float64 NumPy, one thread per process",
-            "seconds": dt}
+                      f"of whole steps of one task group (groups cycled; {ntok} tokens per round, V={batch.V}), "
+                      f"{rounds} rounds; full fwd+select+bwd incl. dlogits, float64 NumPy, one thread per process",
+            "seconds": dt, "rounds": rounds}
 
 
 def run_reference(args):
@@ -1334,6 +1339,7 @@ def main(argv=None):
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-tokens", type=int, default=1024, help="oracle sample tokens per worker process")
+    ap.add_argument("--cpu-seconds", type=float, default=10.0, help="cpu_baseline: minimum oracle wall time")
     ap.add_argument("--cpu-procs", type=int, default=0, help="oracle worker processes (0: host cores, memory-bounded)")
     ap.add_argument("--stream-rows", type=int, default=0,
                     help="chunk-stream the batch with chunks of at most this many rows (configs > HBM)")
