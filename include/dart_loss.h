@@ -396,7 +396,8 @@ typedef struct {
  * above, linearly down to n_min at sr = 1, rounded half up (R15):
  *   n = n_max - floor((sr - sr_high) / (1 - sr_high) * (n_max - n_min) + 1/2)
  * evaluated exactly in integers (sr = n_success / n_total, sr_high =
- * sr_high_permille / 1000).  DART_ERR_INVALID_ARG on a bad config or counts. */
+ * sr_high_permille / 1000).  DART_ERR_INVALID_ARG on a bad config or counts
+ * (negative, n_success > n_total, or n_total > 2^40). */
 dart_status dart_rollout_counts(const dart_curation_cfg* cfg, int64_t G, const int64_t* n_success,
                                 const int64_t* n_total, int32_t* n_rollouts);
 

@@ -45,7 +45,9 @@ dart_status dart_rollout_counts(const dart_curation_cfg* c, int64_t G, const int
                                 const int64_t* n_total, int32_t* n_rollouts) {
   if (!cfg_ok(c) || G < 0 || (G > 0 && (!n_success || !n_total || !n_rollouts))) return DART_ERR_INVALID_ARG;
   for (int64_t g = 0; g < G; ++g) {
-    if (n_total[g] < 0 || n_success[g] < 0 || n_success[g] > n_total[g]) return DART_ERR_INVALID_ARG;
+    // counts up to 2^40 keep the exact integer rule below inside int64
+    if (n_total[g] < 0 || n_success[g] < 0 || n_success[g] > n_total[g] || n_total[g] > ((int64_t)1 << 40))
+      return DART_ERR_INVALID_ARG;
     // exact: sr > h  <=>  1000 ns > h nt ;  drop = floor((1000 ns - h nt) D / ((1000 - h) nt) + 1/2)
     const int64_t ns = n_success[g], nt = n_total[g], h = c->sr_high_permille, D = c->n_max - c->n_min;
     int32_t n = c->n_max;
