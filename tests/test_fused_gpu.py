@@ -139,3 +139,29 @@ def test_fused_single_config_full_size_vs_oracle():
     rep = full_oracle_compare(dl, b, cfg, mask_given=True, keep=keep)
     print("fused full-size parity:", rep)
     assert rep["checked_rows"] == int(dl.stats_dict()["n_kept_tok"])
+
+
+def test_fused_zero_fill_off_leaves_masked_rows():
+    """zero_fill_masked = 0: the fused call writes the kept rows only; rows of
+    masked steps keep whatever the buffer held (here a NaN sentinel), kept
+    rows equal the dense call's bit for bit."""
+    b = synth.make_batch("small_multi", seed=4, V=3001, dtype=torch.bfloat16, pad_ld=3008)
+    cfg = dart.Config(entropy_q=0.5)
+    old = run_gpu(b, cfg, grad_dtype=torch.bfloat16)
+    dev = torch.device("cuda")
+    lg = b.logits_store.to(dev)[:, :b.V]
+    args = (lg, b.target.to(dev), b.logp_old.to(dev), b.logp_rollout.to(dev), b.logp_ref.to(dev))
+    dense = dart.DartLoss(b.layout, dart.whole_shard(b.layout), b.V, cfg, dev, ld=lg.stride(0))
+    dense.fused(*args, keep=old.keep, norm=old.norm)
+    sparse = dart.DartLoss(b.layout, dart.whole_shard(b.layout), b.V, dart.Config(entropy_q=0.5, zero_fill_masked=0),
+                           dev, ld=lg.stride(0))
+    sparse.dlogits_store.fill_(float("nan"))
+    sparse.fused(*args, keep=old.keep, norm=old.norm)
+    torch.cuda.synchronize()
+    sparse.check_status()
+    kept = torch.repeat_interleave(old.keep[:b.layout.S] != 0,
+                                   torch.as_tensor(np.diff(b.layout.step_tok_off), device=dev))
+    assert bool(kept.any()) and bool((~kept).any())
+    assert torch.equal(sparse.dlogits[kept], dense.dlogits[kept])
+    assert bool(torch.isnan(sparse.dlogits[~kept].float()).all())
+    assert sparse.stats_dict()["loss"] == dense.stats_dict()["loss"]
