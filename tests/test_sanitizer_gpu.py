@@ -1,6 +1,9 @@
 """compute-sanitizer memcheck + racecheck over a small pass (bulk-copy rings,
 mbarriers, split-row mode, ragged vocab tails).  Full four-tool runs:
-tools/gpu_sanitize.sh, logs in profiles/r01_sanitize_*.log."""
+tools/gpu_sanitize.sh, logs in profiles/r0*_sanitize_*.log.  Some GPU pools
+refuse the sanitizer (their compute-sanitizer is a stub that exits non-zero
+with a "closed on this pool" notice); the test then skips, and the
+guard-band checks of tests/test_bounds_gpu.py stand in for memcheck."""
 import os
 import shutil
 import subprocess
@@ -20,5 +23,7 @@ def test_compute_sanitizer_clean(tool):
     r = subprocess.run([cs, "--tool", tool, "--error-exitcode", "9", sys.executable,
                         os.path.join(ROOT, "tools", "sanitize_driver.py"), "tiny", "odd", "midsplit"],
                        cwd=ROOT, capture_output=True, text=True, timeout=600)
+    if r.returncode != 0 and "closed on this pool" in (r.stdout + r.stderr):
+        pytest.skip("compute-sanitizer refused by this GPU pool (tests/test_bounds_gpu.py covers writes)")
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
     assert "0 errors" in r.stdout or "0 hazards" in r.stdout
