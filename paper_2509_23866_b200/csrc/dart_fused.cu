@@ -32,6 +32,10 @@ namespace dart {
 #ifndef DART_FU_CTAS
 #define DART_FU_CTAS 2
 #endif
+#ifndef DART_FU_CL
+#define DART_FU_CL 2   // CTAs a kept row is split over (a thread-block cluster)
+#endif
+constexpr int FU_CL_MAX = 4;
 // two CTAs per SM (each 8 consumer warps + 1 producer, 96 KB ring): while one
 // CTA sits in its row barrier / epilogue / L2-fed pass 2, the other streams
 // its next row from HBM
@@ -88,10 +92,10 @@ struct FusedShared {
   float part_m[FU_NC];
   float row_g, row_nl2, row_zy;
   int32_t row_y;
-  // split-row mode (CL = 2): the peer CTA's row partial, double-buffered by row parity
+  // split-row mode (CL > 1): every cluster CTA's row partial, double-buffered by row parity
   uint64_t mbx[2];
-  double mb_s[2][2];
-  float mb_m[2][2];
+  double mb_s[2][FU_CL_MAX];
+  float mb_m[2][FU_CL_MAX];
 };
 
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
@@ -282,8 +286,9 @@ __global__ void __launch_bounds__(FU_THREADS, DART_FU_CTAS) fused_sweep_kernel(c
       asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol_last));
       asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol_first));
       uint32_t nrow = 0;   // kept rows issued so far
-      for (int64_t t = fu_next_kept(recs, ra, rb); t < rb; t = fu_next_kept(recs, t + 1, rb), ++nrow) {
+      for (int64_t t = fu_next_kept(recs, ra, rb), tn; t < rb; t = tn, ++nrow) {
         const uint8_t* row = p.logits + t * p.ld_bytes;
+        const uint32_t fl1 = t + 1 < rb ? recs[t + 1].flags : 1u;   // next row's flags, consumed after this row
         for (int pass = 0; pass < 2; ++pass) {
           for (int j = 0; j < nch; ++j) {
             const int w = j % FU_NC;
@@ -300,6 +305,7 @@ __global__ void __launch_bounds__(FU_THREADS, DART_FU_CTAS) fused_sweep_kernel(c
                           pass == 0 ? pol_last : pol_first);
           }
         }
+        tn = (t + 1 >= rb || (fl1 & 1u)) ? t + 1 : fu_next_kept(recs, t + 2, rb);
       }
     }
     __syncwarp();
@@ -312,6 +318,7 @@ __global__ void __launch_bounds__(FU_THREADS, DART_FU_CTAS) fused_sweep_kernel(c
     uint32_t k = 0;
     for (int64_t tk = fu_next_kept(recs, ra, rb); tk < rb; tk = fu_next_kept(recs, tk + 1, rb), ++k) {
       const int par = (int)(k & 1);
+      const FusedRec rc = recs[tk];                    // issued before the wait: off the row's critical path
       named_bar_sync(FU_BAR_PART, FU_BAR_COUNT);       // the consumers' partials of row k are in
       // fixed-order fold of the consumer warps' partials (one per lane, xor butterfly)
       const float mw = lane < FU_NC ? sh.part_m[lane] : -INFINITY;
@@ -320,15 +327,17 @@ __global__ void __launch_bounds__(FU_THREADS, DART_FU_CTAS) fused_sweep_kernel(c
       double Sr = warp_sum_d(sw > 0.0 ? sw * (double)ex2(mw - Mf) : 0.0);
       double Mr = Sr > 0.0 ? (double)Mf : -INFINITY;
       if (lane == 0) {
-        const FusedRec rc = recs[tk];
         if (CL > 1) {                            // exchange with the peer CTA, fold in rank order
           sh.mb_m[par][rank] = (float)Mr;
           sh.mb_s[par][rank] = Sr;
-          mbar_arrive_expect_tx(&sh.mbx[par], 12u);                     // the peer's 4 + 8 bytes
-          const uint32_t peer = rank ^ 1u;
-          const uint32_t rbar = map_rank(&sh.mbx[par], peer);
-          st_async_b32(map_rank(&sh.mb_m[par][rank], peer), __float_as_uint((float)Mr), rbar);
-          st_async_b64(map_rank(&sh.mb_s[par][rank], peer), (uint64_t)__double_as_longlong(Sr), rbar);
+          mbar_arrive_expect_tx(&sh.mbx[par], 12u * (CL - 1));          // 4 + 8 bytes from every peer
+#pragma unroll
+          for (int d = 1; d < CL; ++d) {
+            const uint32_t peer = (rank + (uint32_t)d) % (uint32_t)CL;
+            const uint32_t rbar = map_rank(&sh.mbx[par], peer);
+            st_async_b32(map_rank(&sh.mb_m[par][rank], peer), __float_as_uint((float)Mr), rbar);
+            st_async_b64(map_rank(&sh.mb_s[par][rank], peer), (uint64_t)__double_as_longlong(Sr), rbar);
+          }
           mbar_wait(&sh.mbx[par], (k >> 1) & 1u);
           Mr = -INFINITY;
           Sr = 0.0;
@@ -596,8 +605,9 @@ __global__ void __launch_bounds__(FU_THREADS, DART_FU_CTAS) fused_sweep_kernel(c
     named_bar_sync(FU_BAR_ROW, FU_BAR_COUNT);       // row tk's g / lse
     const float g = sh.row_g, nl2 = sh.row_nl2, zy = sh.row_zy;
     const int32_t y = sh.row_y;
+    const uint32_t fl1 = tk + 1 < rb ? recs[tk + 1].flags : 1u;    // prefetched; consumed after pass 2
     pass2(tk, g, nl2, y, zy);
-    const int64_t tn = fu_next_kept(recs, tk + 1, rb);
+    const int64_t tn = (tk + 1 >= rb || (fl1 & 1u)) ? tk + 1 : fu_next_kept(recs, tk + 2, rb);
     zero_rows(tk + 1, tn);
     tk = tn;
   }
@@ -614,6 +624,9 @@ cudaError_t launch_fused_rec(const FusedParams& p, cudaStream_t st) {
   return cudaGetLastError();
 }
 
+template <typename Tin, typename Tout, int CL>
+static cudaError_t launch_fused_cl(const FusedParams& p, int num_sms, size_t smem, cudaStream_t st);
+
 template <typename Tin, typename Tout>
 static cudaError_t launch_fused_t(const FusedParams& p, int num_sms, bool split, cudaStream_t st) {
   const size_t smem = (size_t)FU_SLOTS * CH_BYTES + sizeof(FusedShared);
@@ -624,13 +637,21 @@ static cudaError_t launch_fused_t(const FusedParams& p, int num_sms, bool split,
     kern<<<(unsigned)(num_sms * DART_FU_CTAS), FU_THREADS, smem, st>>>(p);
     return cudaGetLastError();
   }
-  auto kern = fused_sweep_kernel<Tin, Tout, 2>;
+  return launch_fused_cl<Tin, Tout, DART_FU_CL>(p, num_sms, smem, st);
+}
+
+template <typename Tin, typename Tout, int CL>
+static cudaError_t launch_fused_cl(const FusedParams& p, int num_sms, size_t smem, cudaStream_t st) {
+  if constexpr (CL > 2) {     // rows of fewer chunks than cluster CTAs: pairs
+    if (p.nch < CL) return launch_fused_cl<Tin, Tout, 2>(p, num_sms, smem, st);
+  }
+  auto kern = fused_sweep_kernel<Tin, Tout, CL>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   cudaLaunchConfig_t cfg = {};
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = 2;
+  attr[0].val.clusterDim.x = CL;
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
   cfg.blockDim = dim3(FU_THREADS);
@@ -642,9 +663,9 @@ static cudaError_t launch_fused_t(const FusedParams& p, int num_sms, bool split,
   int n = 0;
   if (cudaOccupancyMaxActiveClusters(&n, kern, &cfg) != cudaSuccess || n <= 0) {
     (void)cudaGetLastError();
-    n = num_sms * DART_FU_CTAS / 2;
+    n = num_sms * DART_FU_CTAS / CL;
   }
-  cfg.gridDim = dim3((unsigned)(2 * n));
+  cfg.gridDim = dim3((unsigned)(CL * n));
   return cudaLaunchKernelEx(&cfg, kern, p);
 }
 
