@@ -114,6 +114,10 @@ typedef enum {
 #define DART_STATUS_BAD_CSR         (1u << 5) /* decreasing offsets, traj_group decreasing or out of
                                                  [0,G), or the local shard not aligned to steps */
 #define DART_STATUS_TARGET_NEGINF   (1u << 6) /* the target's logit is -inf (log-prob -inf) */
+#define DART_STATUS_NONFINITE_LOSS  (1u << 7) /* a token's loss term or its derivative is not finite in
+                                                 the fp32 outputs (ell / dell), e.g. the k3 term
+                                                 e^d - d - 1 at d = logp_ref - logp > 88.7 or an
+                                                 importance ratio exp(logp - logp_old) beyond fp32 */
 
 /* Hyper-parameters (host struct).  Paper values: PAPER.md:575-578. */
 typedef struct {

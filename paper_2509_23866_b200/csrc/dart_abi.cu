@@ -348,6 +348,7 @@ dart_status dart_loss_fwd(const dart_batch* b, const dart_meta* m, const dart_cf
     sp.keep = nullptr;
     sp.logp = o->logp; sp.logp_old = b->logp_old; sp.logp_roll = b->logp_rollout; sp.logp_ref = b->logp_ref;
     sp.eps_low = c->eps_low; sp.eps_high = c->eps_high; sp.is_cap = c->is_cap; sp.beta = c->beta_kl;
+    sp.status = o->status;
     sp.step_entropy = o->step_entropy; sp.step_ell = o->step_ell;
     sp.step_stats = at<double>(ws, L.step_stats);
     DART_TRY(launch_step_reduce(sp, s));
@@ -442,6 +443,7 @@ dart_status dart_lmhead_fwd(const dart_lmhead* h, const dart_batch* b, const dar
     sp.keep = nullptr;
     sp.logp = o->logp; sp.logp_old = b->logp_old; sp.logp_roll = b->logp_rollout; sp.logp_ref = b->logp_ref;
     sp.eps_low = c->eps_low; sp.eps_high = c->eps_high; sp.is_cap = c->is_cap; sp.beta = c->beta_kl;
+    sp.status = o->status;
     sp.step_entropy = o->step_entropy; sp.step_ell = o->step_ell;
     sp.step_stats = at<double>(ws, L.step_stats);
     DART_TRY(launch_step_reduce(sp, s));
@@ -745,6 +747,7 @@ dart_status dart_loss_fused(const dart_batch* b, const dart_meta* m, const dart_
     sp.ratio_level = DART_RATIO_TOKEN;
     sp.logp = o->logp; sp.logp_old = b->logp_old; sp.logp_roll = b->logp_rollout; sp.logp_ref = b->logp_ref;
     sp.eps_low = c->eps_low; sp.eps_high = c->eps_high; sp.is_cap = c->is_cap; sp.beta = c->beta_kl;
+    sp.status = o->status;
     DART_TRY(launch_step_reduce(sp, s));
     pp.no_stats = 0;
     DART_TRY(launch_bwd_prep(pp, s));   // loss partial + statistics from the step sums

@@ -211,6 +211,7 @@ __device__ float fused_epilogue(const FusedParams& p, int64_t t, const FusedRec&
   const float beta = (float)p.beta;
   const float ell = -rc.w * sur + beta * kl;
   const float dell = -rc.w * (act ? A * r : 0.f) + beta * dkl;
+  if (!isfinite(ell) || !isfinite(dell)) bits |= DART_STATUS_NONFINITE_LOSS;
   if (!write) return rc.c * dell * (float)p.invT;
   p.lse[t] = (float)(lse2 * LN2_D);
   p.logp[t] = logp;

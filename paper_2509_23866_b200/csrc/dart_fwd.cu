@@ -381,6 +381,7 @@ __device__ void row_epilogue_z(const FwdParams& p, int64_t row, Part R, uint32_t
   }
   const double ell = -w * sur + p.beta * kl;                   // L = -J_HE per token
   const double dell = -w * (act ? A * r : 0.0) + p.beta * dkl;
+  if (!isfinite((float)ell) || !isfinite((float)dell)) bits |= DART_STATUS_NONFINITE_LOSS;
   if (lane == 0) {
     p.lse[row] = (float)lse;
     p.logp[row] = (float)logp;
@@ -666,14 +667,18 @@ __global__ void step_reduce_kernel(StepReduceParams p) {
       const double ell_s = -wt * sur + p.beta * skl;
       const double dsur = -wt * (act ? A * r : 0.0);
       const uint8_t flags = (uint8_t)((act ? 0u : 1u) | (trunc ? 2u : 0u));
+      bool bad = !isfinite(ell_s);
       for (int64_t t = t0 + lane; t < t1; t += 32) {
         double dkl = 0.0;
         if (p.beta != 0.0 && !p.exact_kl) dkl = 1.0 - exp((double)p.logp_ref[t] - (double)p.logp[t]);
-        p.dell[t] = (float)(dsur + p.beta * dkl);
+        const float dl = (float)(dsur + p.beta * dkl);
+        bad |= !isfinite(dl);
+        p.dell[t] = dl;
         p.ell[t] = (float)(ell_s / (double)n);
         p.aux_w[t] = (float)wt;
         p.aux_flags[t] = flags;
       }
+      if (__any_sync(0xffffffffu, bad) && lane == 0) status_or(p.status, DART_STATUS_NONFINITE_LOSS);
       sE = ell_s;
       sw = wt * (double)n;
       sclip = act ? 0.0 : (double)n;

@@ -99,6 +99,7 @@ struct StepReduceParams {
   int exact_kl;         // DART_KL_EXACT: the KL gradient is per element, not through logp
   const float *logp, *logp_old, *logp_roll, *logp_ref;
   double eps_low, eps_high, is_cap, beta;
+  uint32_t* status;     // DART_STATUS_NONFINITE_LOSS of the step-level terms
 };
 
 struct SelectParams {

@@ -142,6 +142,7 @@ __device__ void kl_row_epilogue(const FwdParams& p, int64_t row, double M, doubl
   const bool act = (A > 0.0) ? (r <= hi_c) : ((A < 0.0) ? (r >= lo_c) : true);
   const double ell = -w * sur + p.beta * kl;
   const double dell = -w * (act ? A * r : 0.0);   // the KL gradient is per element (bwd)
+  if (!isfinite((float)ell) || !isfinite((float)dell)) bits |= DART_STATUS_NONFINITE_LOSS;
   if (lane == 0) {
     p.lse[row] = (float)(lse2 * LN2_D);
     p.logp[row] = (float)logp;

@@ -30,6 +30,7 @@ SEL_FLOOR, SEL_CEIL, SEL_LINEAR, SEL_OFF = range(4)
 STATUS_BITS = {
     1 << 0: "NONFINITE_LOGIT", 1 << 1: "TARGET_RANGE", 1 << 2: "ROW_ALL_NEGINF",
     1 << 3: "NONFINITE_LOGP", 1 << 4: "EMPTY", 1 << 5: "BAD_CSR", 1 << 6: "TARGET_NEGINF",
+    1 << 7: "NONFINITE_LOSS",
 }
 ABI_VERSION = 6
 RATIO_TOKEN, RATIO_STEP = 0, 1

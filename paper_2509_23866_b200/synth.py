@@ -221,9 +221,11 @@ def _approx_target_logp(z, y, inv_temperature):
 
 def make_batch(name, seed=0, device="cpu", real_reward=False, chunk_rows=2048,
                inv_temperature=1.0, zero_delta=False, layout=None, V=None, dtype=None,
-               pad_ld: Optional[int] = None, with_ref=False, ref_sigma=0.3):
+               pad_ld: Optional[int] = None, with_ref=False, ref_sigma=0.3, logit_scale=1.0):
     """Builds a Batch for config `name` on `device` (seeded; identical bits for
-    the same (name, seed, device type))."""
+    the same (name, seed, device type)).  logit_scale multiplies the drawn
+    logits before rounding (sharper or flatter rows for parity sweeps); the
+    targets and the recorded log-probabilities follow the scaled logits."""
     if layout is None:
         layout, V0, dt0, _ = config_layout(name, seed, real_reward)
         V = V or V0
@@ -255,6 +257,8 @@ def make_batch(name, seed=0, device="cpu", real_reward=False, chunk_rows=2048,
         z = torch.randn((n, V), generator=gen, device=dev, dtype=torch.float32)
         z.mul_(sig_t[r0:r1, None])
         z[torch.arange(n, device=dev), vs_t[r0:r1]] += b_t[r0:r1]
+        if logit_scale != 1.0:
+            z.mul_(logit_scale)
         zq = z.to(dtype)
         logits[r0:r1] = zq
         u = torch.rand((n, V), generator=gen, device=dev, dtype=torch.float32).clamp_(1e-20, 1.0)

@@ -18,6 +18,28 @@ RTOL_TOK = 1e-5      # per-token ell / dell
 ATOL_TOK = 2e-6
 P_REL = 4e-6         # fp32 error of p_v relative to p_v (lse2 rounding + ex2.approx + fma)
 SEL_BAND = 1e-6      # north_star: the mask is bit-exact except steps within 1e-6 of tau (oracle values)
+LOG2E = 1.0 / math.log(2.0)
+
+
+def p_rel_row(z_row, lse_t, inv_temperature):
+    """Relative fp32 error bound of p_v = 2^(c2 z_v - lse2) per element
+    (DESIGN.md §4): P_REL plus the rounding of the exponent's two large
+    terms -- -lse2 stored as fp32 and c2 z_v with c2 = invT log2(e) in fp32,
+    each 2^-24 relative -- times ln 2.  For bf16 rows of magnitude ~30 the
+    added term is ~3e-6; for 8x sharper rows (|z| ~ 240) ~3e-5."""
+    zc = np.abs(np.where(np.isfinite(z_row), z_row, 0.0)) * (inv_temperature * LOG2E)
+    return P_REL + math.log(2.0) * 2.0 ** -24 * (abs(lse_t) * LOG2E + zc)
+
+
+def zero_g_row_ok(dz_row, c_tok, dell, inv_temperature, out_dtype):
+    """A kept row whose oracle g = c dell invT is exactly 0 (e.g. A = 0 and
+    logp_ref = logp in float64): the GPU's g is within dg = |c| invT
+    (RTOL_TOK |dell| + ATOL_TOK) of 0, so |dz_v| = |g_gpu| |delta - p| <= dg
+    (+ the output rounding).  Masked rows (c = 0) must be exactly zero."""
+    if c_tok == 0.0:
+        return bool(np.all(dz_row == 0))
+    dg = abs(c_tok * inv_temperature) * (RTOL_TOK * abs(dell) + ATOL_TOK)
+    return bool(np.all(np.abs(dz_row) <= dg * (1.0 + 2.0 ** -7) + 1e-38))
 
 
 def run_gpu(batch, cfg, grad_dtype=None, device="cuda", logits=None, runs=1):
@@ -44,14 +66,14 @@ def bf16_ulp(x):
     return 2.0 ** (np.floor(np.log2(ax)) - 7)
 
 
-def grad_tol(dz_ref, p_ref, g, dg, out_dtype):
+def grad_tol(dz_ref, p_ref, g, dg, out_dtype, p_rel=P_REL):
     """Error model of dz_v = g (delta_vy - p_v) in fp32 then rounded:
     |dz_gpu - dz_ref| <= 1 ulp of the output format
                        + dg |dz_ref / g|      (dg = bound on |g_gpu - g|: c*invT*(RTOL_TOK|dell| + ATOL_TOK))
-                       + |g| P_REL p_v        (fp32 error of p_v)
+                       + |g| p_rel p_v        (fp32 error of p_v; p_rel_row())
                        + FTZ floor."""
     ulp = bf16_ulp(dz_ref) if out_dtype == torch.bfloat16 else np.maximum(np.abs(dz_ref), 2.0 ** -126) * 2.0 ** -23
-    return ulp + dg * np.abs(dz_ref) / abs(g) + (abs(g) + dg) * P_REL * p_ref + abs(g) * 2.0 ** -125 + 1e-38
+    return ulp + dg * np.abs(dz_ref) / abs(g) + (abs(g) + dg) * p_rel * p_ref + abs(g) * 2.0 ** -125 + 1e-38
 
 
 def oracle_select_on(dl, batch, cfgf):
@@ -133,8 +155,11 @@ def compare(dl, batch, cfg, rows=None, check_all_tokens=True, oracle_rows_only=F
         rs = ref["stats"]
         for k in ("n_tok", "n_kept_tok", "n_kept_step"):
             assert st[k] == rs[k], k
-        for k in ("sum_w", "sum_adv", "sum_adv2", "sum_H", "sum_kl"):
+        for k in ("sum_w", "sum_adv", "sum_adv2", "sum_kl"):
             assert abs(st[k] - rs[k]) <= 1e-5 * (abs(rs[k]) + 1.0), (k, st[k], rs[k])
+        # sum of token entropies: each within RTOL_ENT |H| + ATOL_ENT (H >= 0, so sum |H| = sum H)
+        assert abs(st["sum_H"] - rs["sum_H"]) <= RTOL_ENT * abs(rs["sum_H"]) + ATOL_ENT * rs["n_tok"], \
+            ("sum_H", st["sum_H"], rs["sum_H"])
         assert abs(st["sum_clip"] - rs["sum_clip"]) <= int(near.sum())
         assert abs(st["sum_trunc"] - rs["sum_trunc"]) <= 1
 
@@ -147,13 +172,15 @@ def compare(dl, batch, cfg, rows=None, check_all_tokens=True, oracle_rows_only=F
         g = ref["c_tok"][t] * ref["dell"][t] * cfgf["inv_temperature"]
         dref = ref["dz"][t]
         if g == 0.0:
-            assert np.all(dz[t] == 0), f"row {t} must be zero"
+            assert zero_g_row_ok(dz[t], ref["c_tok"][t], ref["dell"][t], cfgf["inv_temperature"], dl.grad_dtype), \
+                f"row {t}: oracle g = 0"
             continue
         # p_ref for the error model: recover from dz_ref = g (onehot - p)
         p_ref = -dref / g
         p_ref[ob["target"][t]] = 1.0 - dref[ob["target"][t]] / g
         dg = abs(ref["c_tok"][t] * cfgf["inv_temperature"]) * (RTOL_TOK * abs(ref["dell"][t]) + ATOL_TOK)
-        tol = grad_tol(dref, np.abs(p_ref), g, dg, dl.grad_dtype)
+        tol = grad_tol(dref, np.abs(p_ref), g, dg, dl.grad_dtype,
+                       p_rel=p_rel_row(ob["logits"][t], ref["lse"][t], cfgf["inv_temperature"]))
         err = np.abs(dz[t] - dref)
         bad = np.nonzero(err > tol)[0]
         assert bad.size == 0, (t, bad[:5], dz[t][bad[:5]], dref[bad[:5]], g)

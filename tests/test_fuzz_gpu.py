@@ -1,0 +1,95 @@
+"""Randomised parity sweep: seeded random batches and configurations through
+the C ABI, each checked element by element against the float64 oracle with
+the parity bar of tests/gpu_helpers.compare() (main path) and of
+tests/test_fused_gpu._fused_case() (fused update, same mask).
+
+Each case draws its own layout (1-5 task groups of 1-6 rollouts, 1-6 steps
+per trajectory, 1-48 tokens per step, real or Bernoulli rewards -- so
+single-trajectory and all-equal groups, i.e. sigma_R = 0, occur), a
+vocabulary size from tiny to larger than one bulk chunk with a ragged tail,
+logits / gradient dtypes, a padded row pitch, and the hyper-parameters the
+ABI exposes (q, selection rule, normalisation mode, beta, IS cap C, inverse
+temperature, adv_eps, clip bounds, token- or step-level ratio); a quarter
+of the main-path cases draw their logits 8x sharper (|z| up to ~240:
+near-one-hot rows, the fp32 exponent-magnitude term of the dz error model)
+and some have -inf entries (p = 0, no 0 * inf in the entropy).  Inputs
+follow the DESIGN.md §5 recipe (synth.make_batch); the draws themselves
+hold no method arithmetic."""
+import numpy as np
+import pytest
+import torch
+
+from paper_2509_23866_b200 import dart, synth
+from tests.gpu_helpers import compare, run_gpu
+from tests.test_fused_gpu import _fused_case
+
+pytestmark = pytest.mark.gpu
+
+N_CASES = 96
+VOCABS = [1, 7, 33, 100, 513, 1000, 2047, 4099, 8200, 30001]
+
+
+def draw_case(seed):
+    rng = np.random.default_rng(1000 + seed)
+    V = int(rng.choice(VOCABS))
+    big = V > 2047                           # keep T x V small enough for the float64 oracle
+    G = int(rng.integers(1, 4 if big else 6))
+    groups = [list(rng.integers(1, 5 if big else 7, size=int(rng.integers(1, 7)))) for _ in range(G)]
+    traj_group = np.concatenate([[g] * len(l) for g, l in enumerate(groups)]).astype(np.int32)
+    steps = np.concatenate(groups).astype(np.int64)
+    traj_step_off = np.concatenate([[0], np.cumsum(steps)]).astype(np.int64)
+    S = int(traj_step_off[-1])
+    ntok = rng.integers(1, 13 if big else 49, size=S)
+    step_tok_off = np.concatenate([[0], np.cumsum(ntok)]).astype(np.int64)
+    if rng.random() < 0.5:
+        reward = rng.random(len(traj_group))
+    else:                                   # Bernoulli per group, some groups all-equal
+        reward = np.concatenate([(rng.random(len(l)) < rng.uniform(0.1, 0.9)).astype(np.float64)
+                                 for l in groups])
+    layout = synth.layout_from_csr(G, traj_group, reward.astype(np.float32), traj_step_off, step_tok_off, seed=seed)
+    dtype = torch.bfloat16 if (V >= 4096 or rng.random() < 0.5) else torch.float32
+    per = 8 if dtype == torch.bfloat16 else 4
+    pad_ld = -(-V // per) * per + (per * int(rng.integers(0, 3)))
+    grad_dtype = torch.float32 if (dtype == torch.float32 or rng.random() < 0.3) else torch.bfloat16
+    ratio_level = dart.RATIO_STEP if rng.random() < 0.25 else dart.RATIO_TOKEN
+    q = float(rng.choice([0.0, 0.2, 0.5, 0.9]))
+    cfg = dart.Config(
+        eps_low=float(rng.choice([0.2, 0.1])), eps_high=float(rng.choice([0.28, 0.2])),
+        is_cap=float(rng.choice([1.0, 2.0, 0.5])), beta_kl=float(rng.choice([0.0, 0.1])),
+        entropy_q=q, inv_temperature=float(rng.choice([1.0, 0.7, 1.3])),
+        adv_eps=float(rng.choice([0.0, 0.0, 1e-6])), norm_mode=int(rng.integers(0, 5)),
+        select_rule=int(rng.choice([dart.SEL_FLOOR, dart.SEL_FLOOR, dart.SEL_CEIL, dart.SEL_LINEAR, dart.SEL_OFF])),
+        ratio_level=ratio_level)
+    return layout, V, dtype, pad_ld, grad_dtype, cfg
+
+
+def _make(seed):
+    layout, V, dtype, pad_ld, grad_dtype, cfg = draw_case(seed)
+    rng = np.random.default_rng(7 + seed)
+    scale = 8.0 if rng.random() < 0.25 else 1.0     # sharp rows: |z| up to ~240, lse2 up to ~350
+    b = synth.make_batch("fuzz", seed=seed, layout=layout, V=V, dtype=dtype, pad_ld=pad_ld,
+                         inv_temperature=cfg.inv_temperature, logit_scale=scale)
+    if V > 1 and rng.random() < 0.3:   # -inf logits (masked vocabulary entries) in a third of the rows
+        rows = np.nonzero(rng.random(layout.T) < 0.33)[0]
+        for t in rows:
+            cols = rng.choice(V, size=max(1, V // 10), replace=False)
+            cols = cols[cols != int(b.target[t])]
+            b.logits[t, torch.as_tensor(cols, dtype=torch.long)] = float("-inf")
+    return b, grad_dtype, cfg
+
+
+@pytest.mark.parametrize("seed", range(N_CASES))
+def test_fuzz_main_path_vs_oracle(seed):
+    b, grad_dtype, cfg = _make(seed)
+    dl = run_gpu(b, cfg, grad_dtype=grad_dtype)
+    dl.check_status()
+    compare(dl, b, cfg)
+
+
+@pytest.mark.parametrize("seed", range(0, N_CASES, 2))
+def test_fuzz_fused_vs_oracle(seed):
+    layout, V, dtype, pad_ld, grad_dtype, cfg = draw_case(seed)
+    if cfg.ratio_level != dart.RATIO_TOKEN:
+        cfg.ratio_level = dart.RATIO_TOKEN      # the fused update is the token-level form (ABI: UNSUPPORTED otherwise)
+    _fused_case("fuzz", cfg, seed=seed, grad_dtype=grad_dtype, layout=layout, V=V, dtype=dtype, pad_ld=pad_ld,
+                inv_temperature=cfg.inv_temperature)

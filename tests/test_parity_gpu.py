@@ -116,7 +116,8 @@ def test_neg_inf_logits_and_one_hot_rows():
 
 
 @pytest.mark.parametrize("what,bit", [("nan", 1 << 0), ("posinf", 1 << 0), ("target", 1 << 1),
-                                      ("allneginf", 1 << 2), ("logp", 1 << 3), ("target_neginf", 1 << 6)])
+                                      ("allneginf", 1 << 2), ("logp", 1 << 3), ("target_neginf", 1 << 6),
+                                      ("kl_overflow", 1 << 7), ("ratio_overflow", 1 << 7)])
 def test_status_bits(what, bit):
     b = synth.make_batch("tiny", seed=0)
     if what == "nan":
@@ -131,6 +132,11 @@ def test_status_bits(what, bit):
         b.logp_old[2] = float("nan")
     elif what == "target_neginf":
         b.logits[6, b.target[6]] = float("-inf")
+    elif what == "kl_overflow":     # k3: e^d with d = logp_ref - logp > 88.7 is beyond fp32
+        b.logits[5, b.target[5]] -= 150.0
+    elif what == "ratio_overflow":  # r = exp(logp - logp_old) beyond fp32: -w r A = +inf where A < 0
+        b.logp_old.fill_(-200.0)
+        b.logp_rollout.fill_(-200.0)
     dl = run_gpu(b, dart.Config(is_cap=2.0))
     v = int(dl.status.item())
     assert v & bit, hex(v)
