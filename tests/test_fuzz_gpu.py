@@ -93,3 +93,46 @@ def test_fuzz_fused_vs_oracle(seed):
         cfg.ratio_level = dart.RATIO_TOKEN      # the fused update is the token-level form (ABI: UNSUPPORTED otherwise)
     _fused_case("fuzz", cfg, seed=seed, grad_dtype=grad_dtype, layout=layout, V=V, dtype=dtype, pad_ld=pad_ld,
                 inv_temperature=cfg.inv_temperature)
+
+
+@pytest.mark.parametrize("seed", range(1, N_CASES, 6))
+def test_fuzz_virtual_ranks_vs_oracle(seed):
+    """The same random batches sharded over W = 2..5 trajectory ranges (some
+    possibly empty), the all-gather emulated by concatenation: bitwise equal
+    to the unsharded pass and, assembled, the oracle's parity bar."""
+    from paper_2509_23866_b200 import dist as D
+    from tests.gpu_helpers import Assembled, snapshot
+    b, grad_dtype, cfg = _make(seed)
+    W = 2 + seed % 4
+    ref = run_gpu(b, cfg, grad_dtype=grad_dtype)
+    ref.check_status()
+    shards = D.shard_layout(b.layout, W)
+    dev = torch.device("cuda")
+    ld = b.logits_store.stride(0)
+    dls = []
+    for sh in shards:
+        dl = dart.DartLoss(b.layout, sh, b.V, cfg, dev, logits_dtype=b.logits.dtype, grad_dtype=ref.grad_dtype,
+                           group=False, world_shards=shards, ld=ld, ldg=ref.ldg)
+        sl = slice(sh.tok_begin, sh.tok_end)
+        dl.forward(b.logits_store[sl].to(dev)[:, :b.V], b.target[sl].to(dev).contiguous(),
+                   b.logp_old[sl].to(dev).contiguous(), b.logp_rollout[sl].to(dev).contiguous(),
+                   b.logp_ref[sl].to(dev).contiguous())
+        dls.append(dl)
+    S_pad = dls[0].S_pad
+    gathered = torch.zeros(W * S_pad, dtype=torch.float32, device=dev)
+    for r, (dl, sh) in enumerate(zip(dls, shards)):
+        gathered[r * S_pad: r * S_pad + sh.S_loc] = dl.step_H[:sh.S_loc]
+    for dl in dls:
+        dl.set_gathered(gathered)
+        dl.select()
+        dl.backward()
+    torch.cuda.synchronize()
+    for dl, sh in zip(dls, shards):
+        dl.check_status()
+        sl = slice(sh.tok_begin, sh.tok_end)
+        assert torch.equal(dl.keep[:b.layout.S], ref.keep[:b.layout.S])
+        assert dl.norm_dict() == ref.norm_dict()
+        for a, c in ((dl.lse, ref.lse[sl]), (dl.H, ref.H[sl]), (dl.ell, ref.ell[sl]), (dl.dell, ref.dell[sl])):
+            assert torch.equal(a, c)
+        assert torch.equal(dl.dlogits, ref.dlogits[sl])
+    compare(Assembled([snapshot(dl) for dl in dls], b.layout, grad_dtype=ref.grad_dtype, stats_reduced=False), b, cfg)
