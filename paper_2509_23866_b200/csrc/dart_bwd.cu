@@ -364,7 +364,7 @@ bwd_sweep_kernel(const BwdParams p) {
       uint32_t dep = 0;
 #pragma unroll
       for (int k = 0; k < BVPL; ++k) dep |= x[k].x | x[k].y | x[k].z | x[k].w;
-      asm volatile("" ::"r"(dep));
+      hold_until_loaded(dep);
       __syncwarp();
       if (pc.valid) bwd_issue<Tin, WARPS, STAGES>(pc, p, bars, ring, slot, lane, pol);
       if (++slot == STAGES) { slot = 0; phase ^= 1u; }

@@ -113,6 +113,17 @@ __device__ __forceinline__ uint4 lds128(const void* p) {
   return v;
 }
 
+// A ring slot may be handed back (to the producer, or to this warp's own next
+// bulk copy) only once every 16-byte vector loaded from it has arrived in
+// registers.  `dep` ORs all loaded words; storing it to a scratch word makes
+// that a real register dependency (ptxas deletes an empty asm consumer, after
+// which nothing orders the LDS ahead of the next bulk copy into the slot --
+// observed as a rare stale chunk once other stores congested the MIO queue).
+__device__ __forceinline__ void hold_until_loaded(uint32_t dep) {
+  __shared__ uint32_t dep_sink;
+  asm volatile("st.shared.b32 [%0], %1;" ::"r"(smem_u32(&dep_sink)), "r"(dep) : "memory");
+}
+
 __device__ __forceinline__ void stg128_cs(void* p, uint4 v) {
   asm volatile("st.global.cs.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w)
                : "memory");

@@ -35,6 +35,10 @@ namespace dart {
 #ifndef DART_FU_CL
 #define DART_FU_CL 2   // CTAs a kept row is split over (a thread-block cluster)
 #endif
+#ifndef DART_FU_ZB
+#define DART_FU_ZB 16  // >0: masked-row zero stores deferred into the row-barrier windows, this many
+                       // 16-byte stores per lane per window (0: written inline between kept rows)
+#endif
 constexpr int FU_CL_MAX = 4;
 // two CTAs per SM (each 8 consumer warps + 1 producer, 96 KB ring): while one
 // CTA sits in its row barrier / epilogue / L2-fed pass 2, the other streams
@@ -387,7 +391,7 @@ __global__ void __launch_bounds__(FU_THREADS, DART_FU_CTAS) fused_sweep_kernel(c
     uint32_t dep = 0;
 #pragma unroll
     for (int q = 0; q < VPL; ++q) dep |= x[q].x | x[q].y | x[q].z | x[q].w;
-    asm volatile("" ::"r"(dep));
+    hold_until_loaded(dep);
     __syncwarp();
     if (lane == 0) mbar_arrive(&sh.empty[slot]);   // slot back to the producer
   };
@@ -596,22 +600,76 @@ __global__ void __launch_bounds__(FU_THREADS, DART_FU_CTAS) fused_sweep_kernel(c
     }
   };
 
+#if DART_FU_ZB > 0
+  // deferred zero-fill: a per-warp cursor over the masked rows below `zlim`
+  // (rows in order, this warp's vectors li = warp*32 + lane + k*FU_NC*32 of each)
+  int64_t zt = ra;
+  int zli = warp * 32 + lane;
+  bool zt_masked = zt < rb && !(recs[zt].flags & 1u);
+  const int zrow_vecs = nch * CH_VEC;
+  auto zero_some = [&](int64_t zlim, int budget) {
+    if (!p.zero_fill) return;
+    while (zt < zlim) {
+      if (!zt_masked) {
+        ++zt;
+        zt_masked = zt < rb && !(recs[zt].flags & 1u);
+        continue;
+      }
+      if (budget <= 0) return;
+      uint8_t* orow = p.dlogits + zt * p.ldg_bytes;
+      for (; zli < zrow_vecs && budget > 0; zli += FU_NC * 32, --budget) {
+        const int vi = ((zli / CH_VEC) * CL + (int)rank) * CH_VEC + (zli % CH_VEC);
+        if (vi >= nvec) continue;
+        const int nvalid = (tail_elems && vi == nvec - 1) ? tail_elems : EPV;
+        uint8_t* dst = orow + vi * OUTV;
+        if (nvalid == EPV) {
+          if (OUT_BF16 && EPV == 8) stg128_cs(dst, make_uint4(0u, 0u, 0u, 0u));
+          else if (OUT_BF16) *reinterpret_cast<uint2*>(dst) = make_uint2(0u, 0u);
+          else
+            for (int e = 0; e < EPV; e += 4) stg128_cs(dst + 4 * e, make_uint4(0u, 0u, 0u, 0u));
+        } else {
+          for (int e = 0; e < nvalid; ++e) {
+            if (OUT_BF16) reinterpret_cast<__nv_bfloat16*>(dst)[e] = __float2bfloat16_rn(0.f);
+            else reinterpret_cast<float*>(dst)[e] = 0.f;
+          }
+        }
+      }
+      if (zli >= zrow_vecs) {
+        zli = warp * 32 + lane;
+        ++zt;
+        zt_masked = zt < rb && !(recs[zt].flags & 1u);
+      }
+    }
+  };
+#endif
+
   int64_t tk = fu_next_kept(recs, ra, rb);
+#if DART_FU_ZB == 0
   zero_rows(ra, tk);
+#endif
   while (tk < rb) {
     float m = NEG_CLAMP * c2;
     float2 s01 = make_float2(0.f, 0.f), s23 = make_float2(0.f, 0.f);
     pass1(0u, cw, m, s01, s23);
     publish(m, s01, s23);                            // non-blocking: the reducer folds
+#if DART_FU_ZB > 0
+    zero_some(tk, DART_FU_ZB);                      // masked rows below this one, while the row reduces
+    __syncwarp();                                   // reconverge: bar.sync is warp-aligned
+#endif
     named_bar_sync(FU_BAR_ROW, FU_BAR_COUNT);       // row tk's g / lse
     const float g = sh.row_g, nl2 = sh.row_nl2, zy = sh.row_zy;
     const int32_t y = sh.row_y;
     const uint32_t fl1 = tk + 1 < rb ? recs[tk + 1].flags : 1u;    // prefetched; consumed after pass 2
     pass2(tk, g, nl2, y, zy);
     const int64_t tn = (tk + 1 >= rb || (fl1 & 1u)) ? tk + 1 : fu_next_kept(recs, tk + 2, rb);
+#if DART_FU_ZB == 0
     zero_rows(tk + 1, tn);
+#endif
     tk = tn;
   }
+#if DART_FU_ZB > 0
+  zero_some(rb, 1 << 30);                           // what is left (after the last kept row)
+#endif
   bad = warp_or(bad);
   if (lane == 0 && bad) status_or(p.status, bad);
   if (CL > 1) cluster_sync_all();

@@ -428,7 +428,7 @@ __device__ __forceinline__ void release_refill(const uint4 (&x)[FVPL], uint64_t*
   uint32_t dep = 0;
 #pragma unroll
   for (int kk = 0; kk < FVPL; ++kk) dep |= x[kk].x | x[kk].y | x[kk].z | x[kk].w;
-  asm volatile("" ::"r"(dep));
+  hold_until_loaded(dep);
   __syncwarp();
   // (no fence.proxy.async needed: this is a read-then-async-write hazard and
   // every read has completed -- its value is in a register -- before the issue)

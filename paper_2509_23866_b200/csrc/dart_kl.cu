@@ -227,7 +227,7 @@ fwd_kl_kernel(const FwdParams p) {
       uint32_t dep = 0;
 #pragma unroll
       for (int q = 0; q < KVPL; ++q) dep |= xz[q].x | xz[q].y | xz[q].z | xz[q].w | xr[q].x | xr[q].y | xr[q].z | xr[q].w;
-      asm volatile("" ::"r"(dep));
+      hold_until_loaded(dep);
       __syncwarp();
       if (prow < p.T_loc) issue(slot);
       if (++slot == STAGES) { slot = 0; phase ^= 1u; }
@@ -463,7 +463,7 @@ bwd_kl_kernel(const BwdParams p) {
       uint32_t dep = 0;
 #pragma unroll
       for (int q = 0; q < KVPL; ++q) dep |= xz[q].x | xz[q].y | xz[q].z | xz[q].w | xr[q].x | xr[q].y | xr[q].z | xr[q].w;
-      asm volatile("" ::"r"(dep));
+      hold_until_loaded(dep);
       __syncwarp();
       if (pc.valid) issue(slot);
       if (++slot == STAGES) { slot = 0; phase ^= 1u; }

@@ -215,7 +215,7 @@ class Assembled:
     already (equal on every rank) or local partials (summed here)."""
 
     def __init__(self, parts, layout, grad_dtype=torch.bfloat16, stats_reduced=True):
-        parts = sorted(parts, key=lambda p: p["tok"][0])
+        parts = sorted(parts, key=lambda p: (p["tok"][0], p["tok"][1]))   # empty shards before their successor
         t = 0
         for p in parts:
             assert p["tok"][0] == t, "shards must tile the batch"
