@@ -361,10 +361,7 @@ bwd_sweep_kernel(const BwdParams p) {
         const int vi = lane + 32 * k;
         x[k] = (vi < nv) ? lds128(sp + vi * 16) : make_uint4(0u, 0u, 0u, 0u);
       }
-      uint32_t dep = 0;
-#pragma unroll
-      for (int k = 0; k < BVPL; ++k) dep |= x[k].x | x[k].y | x[k].z | x[k].w;
-      hold_until_loaded(dep);
+      fence_reads_before_refill();
       __syncwarp();
       if (pc.valid) bwd_issue<Tin, WARPS, STAGES>(pc, p, bars, ring, slot, lane, pol);
       if (++slot == STAGES) { slot = 0; phase ^= 1u; }

@@ -113,15 +113,19 @@ __device__ __forceinline__ uint4 lds128(const void* p) {
   return v;
 }
 
-// A ring slot may be handed back (to the producer, or to this warp's own next
-// bulk copy) only once every 16-byte vector loaded from it has arrived in
-// registers.  `dep` ORs all loaded words; storing it to a scratch word makes
-// that a real register dependency (ptxas deletes an empty asm consumer, after
-// which nothing orders the LDS ahead of the next bulk copy into the slot --
-// observed as a rare stale chunk once other stores congested the MIO queue).
-__device__ __forceinline__ void hold_until_loaded(uint32_t dep) {
-  __shared__ uint32_t dep_sink;
-  asm volatile("st.shared.b32 [%0], %1;" ::"r"(smem_u32(&dep_sink)), "r"(dep) : "memory");
+// A ring slot is handed back (to the producer warp, or to this warp's own next
+// bulk copy) right after the shared loads that read it.  Those loads are
+// generic-proxy reads and the refill is an async-proxy (bulk copy) write, so
+// the hand-back is preceded by fence.proxy.async: it orders this thread's
+// earlier shared accesses before the async proxy's later ones.  (An empty-asm
+// "use" of the loaded words does not: ptxas deletes it, and without an
+// ordering the refill raced the loads -- seen as rare run-to-run lse jitter
+// of the fused update once extra stores congested the MIO queue.  A real
+// data dependency also closes it but stalls every chunk on the load latency,
+// 2-3% on the sweeps; the fence costs nothing measurable, A/B in
+// profiles/r02_ring_fence.md.)
+__device__ __forceinline__ void fence_reads_before_refill() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
 
 __device__ __forceinline__ void stg128_cs(void* p, uint4 v) {

@@ -388,10 +388,7 @@ __global__ void __launch_bounds__(FU_THREADS, DART_FU_CTAS) fused_sweep_kernel(c
         x[q] = (vi < nv) ? lds128(sp + vi * 16) : make_uint4(0u, 0u, 0u, 0u);
       }
     }
-    uint32_t dep = 0;
-#pragma unroll
-    for (int q = 0; q < VPL; ++q) dep |= x[q].x | x[q].y | x[q].z | x[q].w;
-    hold_until_loaded(dep);
+    fence_reads_before_refill();
     __syncwarp();
     if (lane == 0) mbar_arrive(&sh.empty[slot]);   // slot back to the producer
   };

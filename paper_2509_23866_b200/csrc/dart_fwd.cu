@@ -418,20 +418,16 @@ __device__ __forceinline__ void issue_next(Stream& ps, uint64_t* bars, uint8_t* 
   if (ps.v == ps.vend) stream_next_segment(ps, W, units, lg, nvec);
 }
 
-// Hand the slot back to the copy engine once every lane holds its vectors in
-// registers (the OR consumes each loaded word, so the LDS results have landed
-// before the async-proxy write is issued), and refill it STAGES chunks ahead.
+// Hand the slot back to the copy engine right after this chunk's shared loads
+// (fence_reads_before_refill orders them before the async-proxy refill) and
+// refill it STAGES chunks ahead.
 template <int STAGES>
 __device__ __forceinline__ void release_refill(const uint4 (&x)[FVPL], uint64_t* bars, uint8_t* ring, int slot,
                                                Stream& ps, const FwdParams& p, int64_t W, int64_t units, int lg,
                                                int64_t nvec, int lane, uint64_t pol) {
-  uint32_t dep = 0;
-#pragma unroll
-  for (int kk = 0; kk < FVPL; ++kk) dep |= x[kk].x | x[kk].y | x[kk].z | x[kk].w;
-  hold_until_loaded(dep);
+  (void)x;
+  fence_reads_before_refill();
   __syncwarp();
-  // (no fence.proxy.async needed: this is a read-then-async-write hazard and
-  // every read has completed -- its value is in a register -- before the issue)
   if (ps.valid) issue_next(ps, bars, ring, slot, p, W, units, lg, nvec, lane, pol);
 }
 

@@ -224,10 +224,7 @@ fwd_kl_kernel(const FwdParams p) {
         xz[q] = (vi < nv) ? lds128(sp + vi * 16) : make_uint4(0u, 0u, 0u, 0u);
         xr[q] = (vi < nv) ? lds128(sp + KV * 16 + vi * 16) : make_uint4(0u, 0u, 0u, 0u);
       }
-      uint32_t dep = 0;
-#pragma unroll
-      for (int q = 0; q < KVPL; ++q) dep |= xz[q].x | xz[q].y | xz[q].z | xz[q].w | xr[q].x | xr[q].y | xr[q].z | xr[q].w;
-      hold_until_loaded(dep);
+      fence_reads_before_refill();
       __syncwarp();
       if (prow < p.T_loc) issue(slot);
       if (++slot == STAGES) { slot = 0; phase ^= 1u; }
@@ -460,10 +457,7 @@ bwd_kl_kernel(const BwdParams p) {
         xz[q] = (vi < nv) ? lds128(sp + vi * 16) : make_uint4(0u, 0u, 0u, 0u);
         xr[q] = (vi < nv) ? lds128(sp + KV * 16 + vi * 16) : make_uint4(0u, 0u, 0u, 0u);
       }
-      uint32_t dep = 0;
-#pragma unroll
-      for (int q = 0; q < KVPL; ++q) dep |= xz[q].x | xz[q].y | xz[q].z | xz[q].w | xr[q].x | xr[q].y | xr[q].z | xr[q].w;
-      hold_until_loaded(dep);
+      fence_reads_before_refill();
       __syncwarp();
       if (pc.valid) issue(slot);
       if (++slot == STAGES) { slot = 0; phase ^= 1u; }
