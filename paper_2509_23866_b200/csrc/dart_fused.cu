@@ -32,14 +32,10 @@ namespace dart {
 #ifndef DART_FU_CTAS
 #define DART_FU_CTAS 2
 #endif
-#ifndef DART_FU_CL
-#define DART_FU_CL 2   // CTAs a kept row is split over (a thread-block cluster)
-#endif
-#ifndef DART_FU_ZB
-#define DART_FU_ZB 16  // >0: masked-row zero stores deferred into the row-barrier windows, this many
-                       // 16-byte stores per lane per window (0: written inline between kept rows)
-#endif
-constexpr int FU_CL_MAX = 4;
+// masked rows' zero stores per lane issued in each row-barrier window (16-byte
+// stores; 8..64 measured alike, 0 -- inline between kept rows -- 2% slower)
+constexpr int FU_ZB = 16;
+constexpr int FU_CL_MAX = 2;   // CTAs a kept row is split over (4-CTA clusters measured 16% slower)
 // two CTAs per SM (each 8 consumer warps + 1 producer, 96 KB ring): while one
 // CTA sits in its row barrier / epilogue / L2-fed pass 2, the other streams
 // its next row from HBM
@@ -572,34 +568,9 @@ __global__ void __launch_bounds__(FU_THREADS, DART_FU_CTAS) fused_sweep_kernel(c
     }
   };
 
-  // masked steps: zeros, no read; the consumer warps split this CTA's chunks of each row
-  auto zero_rows = [&](int64_t t0, int64_t t1) {
-    if (!p.zero_fill) return;
-    for (int64_t t = t0; t < t1; ++t) {
-      uint8_t* orow = p.dlogits + t * p.ldg_bytes;
-      for (int li = warp * 32 + lane; li < nch * CH_VEC; li += FU_NC * 32) {
-        const int vi = ((li / CH_VEC) * CL + (int)rank) * CH_VEC + (li % CH_VEC);
-        if (vi >= nvec) continue;
-        const int nvalid = (tail_elems && vi == nvec - 1) ? tail_elems : EPV;
-        uint8_t* dst = orow + vi * OUTV;
-        if (nvalid == EPV) {
-          if (OUT_BF16 && EPV == 8) stg128_cs(dst, make_uint4(0u, 0u, 0u, 0u));
-          else if (OUT_BF16) *reinterpret_cast<uint2*>(dst) = make_uint2(0u, 0u);
-          else
-            for (int e = 0; e < EPV; e += 4) stg128_cs(dst + 4 * e, make_uint4(0u, 0u, 0u, 0u));
-        } else {
-          for (int e = 0; e < nvalid; ++e) {
-            if (OUT_BF16) reinterpret_cast<__nv_bfloat16*>(dst)[e] = __float2bfloat16_rn(0.f);
-            else reinterpret_cast<float*>(dst)[e] = 0.f;
-          }
-        }
-      }
-    }
-  };
-
-#if DART_FU_ZB > 0
-  // deferred zero-fill: a per-warp cursor over the masked rows below `zlim`
-  // (rows in order, this warp's vectors li = warp*32 + lane + k*FU_NC*32 of each)
+  // masked rows: zeros, no read, deferred into the row-barrier windows -- a
+  // per-warp cursor over the masked rows below `zlim` (rows in order, this
+  // warp's vectors li = warp*32 + lane + k*FU_NC*32 of each)
   int64_t zt = ra;
   int zli = warp * 32 + lane;
   bool zt_masked = zt < rb && !(recs[zt].flags & 1u);
@@ -638,35 +609,24 @@ __global__ void __launch_bounds__(FU_THREADS, DART_FU_CTAS) fused_sweep_kernel(c
       }
     }
   };
-#endif
 
   int64_t tk = fu_next_kept(recs, ra, rb);
-#if DART_FU_ZB == 0
-  zero_rows(ra, tk);
-#endif
   while (tk < rb) {
     float m = NEG_CLAMP * c2;
     float2 s01 = make_float2(0.f, 0.f), s23 = make_float2(0.f, 0.f);
     pass1(0u, cw, m, s01, s23);
     publish(m, s01, s23);                            // non-blocking: the reducer folds
-#if DART_FU_ZB > 0
-    zero_some(tk, DART_FU_ZB);                      // masked rows below this one, while the row reduces
+    zero_some(tk, FU_ZB);                           // masked rows below this one, while the row reduces
     __syncwarp();                                   // reconverge: bar.sync is warp-aligned
-#endif
     named_bar_sync(FU_BAR_ROW, FU_BAR_COUNT);       // row tk's g / lse
     const float g = sh.row_g, nl2 = sh.row_nl2, zy = sh.row_zy;
     const int32_t y = sh.row_y;
     const uint32_t fl1 = tk + 1 < rb ? recs[tk + 1].flags : 1u;    // prefetched; consumed after pass 2
     pass2(tk, g, nl2, y, zy);
     const int64_t tn = (tk + 1 >= rb || (fl1 & 1u)) ? tk + 1 : fu_next_kept(recs, tk + 2, rb);
-#if DART_FU_ZB == 0
-    zero_rows(tk + 1, tn);
-#endif
     tk = tn;
   }
-#if DART_FU_ZB > 0
   zero_some(rb, 1 << 30);                           // what is left (after the last kept row)
-#endif
   bad = warp_or(bad);
   if (lane == 0 && bad) status_or(p.status, bad);
   if (CL > 1) cluster_sync_all();
@@ -693,14 +653,11 @@ static cudaError_t launch_fused_t(const FusedParams& p, int num_sms, bool split,
     kern<<<(unsigned)(num_sms * DART_FU_CTAS), FU_THREADS, smem, st>>>(p);
     return cudaGetLastError();
   }
-  return launch_fused_cl<Tin, Tout, DART_FU_CL>(p, num_sms, smem, st);
+  return launch_fused_cl<Tin, Tout, FU_CL_MAX>(p, num_sms, smem, st);
 }
 
 template <typename Tin, typename Tout, int CL>
 static cudaError_t launch_fused_cl(const FusedParams& p, int num_sms, size_t smem, cudaStream_t st) {
-  if constexpr (CL > 2) {     // rows of fewer chunks than cluster CTAs: pairs
-    if (p.nch < CL) return launch_fused_cl<Tin, Tout, 2>(p, num_sms, smem, st);
-  }
   auto kern = fused_sweep_kernel<Tin, Tout, CL>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
