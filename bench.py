@@ -516,12 +516,17 @@ def run_dart(args):
                     "GBps": 2 * src.numel() * src.element_size() / (cms * 1e-3) / 1e9, "clocks": cclk}
 
     ms = elapsed_ms / args.steps
+    rank_ms = None
     if world > 1:
         import torch.distributed as dist
         from paper_2509_23866_b200 import dist as D
-        t = torch.tensor([ms], dtype=torch.float64, device=dev)
+        t = torch.tensor([ms, -ms], dtype=torch.float64, device=dev)
         D.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
+        tm = torch.tensor([ms], dtype=torch.float64, device=dev)
+        D.all_reduce(tm)
+        rank_ms = {"max": float(t[0].item()), "min": -float(t[1].item()), "mean": float(tm.item()) / world,
+                   "what": "per-rank device time of the timed loop / steps (SURVEY §8(d): max/mean rank time)"}
+        ms = rank_ms["max"]
     T_tot = glayout.T
     value = T_tot / (ms * 1e-3)
 
@@ -612,6 +617,8 @@ def run_dart(args):
             "e2e": e2e,
             "cpu_baseline": cpu,
         }
+        if rank_ms is not None:
+            line["rank_ms"] = rank_ms
         if copy_ref is not None:
             copy_ref["step_frac_vs_copy"] = line["kernels"]["step_GBps"] / copy_ref["GBps"]
             line["copy_sustained"] = copy_ref
