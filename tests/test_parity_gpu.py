@@ -258,3 +258,28 @@ def test_step_level_ratio_mid():
     dl.check_status()
     rng = np.random.default_rng(3)
     compare(dl, b, cfg, rows=sorted(rng.choice(b.layout.T, 12, replace=False).tolist()))
+
+
+def test_deterministic_bitwise_full_size():
+    """The bench's pass (single config, T = 61440, V = 152064, its launch
+    configuration) is bitwise reproducible run to run: per-token values, step
+    entropies, mask, loss statistics and every dlogits row.  Guards the ring
+    hand-back ordering (profiles/r02_ring_fence.md) at the size and occupancy
+    where a refill racing the shared loads would show."""
+    b = synth.make_batch("single", seed=0, device="cuda")
+    cfg = dart.Config()
+    dev = torch.device("cuda")
+    dl = dart.DartLoss(b.layout, dart.whole_shard(b.layout), b.V, cfg, dev)
+    ref = None
+    for _ in range(4):
+        dl.run(b.logits, b.target, b.logp_old, b.logp_rollout, b.logp_ref)
+        torch.cuda.synchronize()
+        dl.check_status()
+        cur = [x.clone() for x in (dl.lse, dl.H, dl.ell, dl.dell, dl.step_H, dl.keep, dl.stats)]
+        cs = dl.dlogits.view(torch.int16).sum(dim=1, dtype=torch.int64)     # per-row checksum
+        if ref is None:
+            ref, ref_dz, ref_cs = cur, dl.dlogits.clone(), cs
+            continue
+        for a, c in zip(cur, ref):
+            assert torch.equal(a, c)
+        assert torch.equal(cs, ref_cs) and torch.equal(dl.dlogits, ref_dz)
