@@ -6,7 +6,7 @@ MERGE per-launch DRAM traffic into profiles/ncu_traffic.json (bench.py's
 
 Inputs (written on the box by tools/gpu_bench_prof.sh): gpurun_out/launches.csv
 (ncu gpu__time_duration launch list of bench.py) and gpurun_out/prof_<k>.ncu-rep
-(`ncu --set full` of one launch) for k in fwd, bwd, fused (those present)."""
+(`ncu --set full` of one launch) for k in fwd, bwd, fused, lmfwd, lmdz (those present)."""
 import collections
 import csv
 import json
@@ -19,7 +19,8 @@ G, P = "gpurun_out", "profiles"
 os.makedirs(P, exist_ok=True)
 tpath = f"{P}/ncu_traffic.json"
 traffic = json.load(open(tpath)) if os.path.exists(tpath) else {}
-KEYS = {"fwd": "fwd_sweep", "bwd": "bwd_sweep", "fused": "fused_sweep"}
+KEYS = {"fwd": "fwd_sweep", "bwd": "bwd_sweep", "fused": "fused_sweep",
+        "lmfwd": "lmhead_fwd", "lmdz": "lmhead_dz"}    # the last two: tools/gpu_prof_lmhead.sh
 rows_md = []
 for k, key in KEYS.items():
     rep = f"{G}/prof_{k}.ncu-rep"
