@@ -114,7 +114,10 @@ def advantages(traj_reward, traj_group, traj_step_off, G, adv_eps=0.0):
         if np.all(R_D == R_D[0]):
             # exact arithmetic gives sigma_R = 0 iff all rewards of D are equal;
             # float rounding of R_bar can leave ~1e-17 residue, so decide it exactly
+            # -- and R_bar is then R itself (the residue would otherwise become the
+            # advantage (R - R_bar) / adv_eps ~ 1e-11 under the adv_eps flag)
             sigma = 0.0
+            R_bar = R_D[0]
         if adv_eps > 0.0:                                     # flag, not the paper
             A[trajs] = (R[trajs] - R_bar) / (sigma + adv_eps)
             ok[g] = 1

@@ -203,10 +203,19 @@ __device__ float fused_epilogue(const FusedParams& p, int64_t t, const FusedRec&
   const bool act = (A > 0.f) ? (r <= hi_c) : ((A < 0.f) ? (r >= lo_c) : true);
   float kl = 0.f, dkl = 0.f;
   if (p.beta != 0.0) {
+    // k3 = e^d - d - 1 and 1 - e^d without fp32 cancellation at small |d|
+    // (logp_ref ~ logp: (e^d - d) - 1 in fp32 loses ~1e-7 absolute against a
+    // value of d^2 / 2): a Taylor series below |d| = 1/4 (truncation
+    // d^5 / 2520 relative), expm1 above.
     const float d = rc.lref - logp;
-    const float ed = expf(d);
-    kl = (ed - d) - 1.f;
-    dkl = 1.f - ed;
+    const float em1 = expm1f(d);
+    dkl = -em1;
+    if (fabsf(d) < 0.25f) {
+      const float d2 = d * d;
+      kl = d2 * (0.5f + d * (1.f / 6.f + d * (1.f / 24.f + d * (1.f / 120.f + d * (1.f / 720.f)))));
+    } else {
+      kl = em1 - d;
+    }
   }
   const float beta = (float)p.beta;
   const float ell = -rc.w * sur + beta * kl;

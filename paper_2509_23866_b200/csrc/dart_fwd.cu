@@ -42,7 +42,9 @@ __global__ void adv_kernel(AdvParams p) {
     }
     uint8_t ok = 0;
     if (sumL > 0) {
-      const double Rbar = sumLR / sumL;
+      // PAPER.md:134; all rewards equal: R itself (exact arithmetic -- the
+      // rounded quotient's residue would become A = residue / adv_eps)
+      const double Rbar = all_equal ? (double)R0 : sumLR / sumL;
       double var = 0.0;
       for (int64_t i = i0; i < i1; ++i) {
         const double L = (double)(p.traj_step_off[i + 1] - p.traj_step_off[i]);

@@ -31,6 +31,20 @@ def p_rel_row(z_row, lse_t, inv_temperature):
     return P_REL + math.log(2.0) * 2.0 ** -24 * (abs(lse_t) * LOG2E + zc)
 
 
+def loss_tol(ref):
+    """Loss bar: 1e-5 relative to sum |c_t ell_t| (L can be ~0)
+    plus the loss's sensitivity to the fp32 rounding of log pi(y):
+    sum_t |c_t dell_t| dlogp_t with dlogp_t = 2^-22 (|lse_t| + |logp_t|) (the
+    max and the target logit enter in fp32, each exact to 2^-24 relative of a
+    term of size <= |lse| + |logp|).  A loss made of tiny terms (A = 0 and
+    logp_ref ~ logp: ell = beta k3 ~ d^2 / 2) inherits that absolute error,
+    far above 1e-5 of its own size; for ordinary batches the term is ~1e-6
+    of the loss."""
+    dlogp = 2.0 ** -22 * (np.abs(ref["lse"]) + np.abs(ref["logp"])) + 1e-9
+    return (RTOL_ENT * float(np.sum(np.abs(ref["c_tok"] * ref["ell"])))
+            + float(np.sum(np.abs(ref["c_tok"] * ref["dell"]) * dlogp)) + 1e-12)
+
+
 def zero_g_row_ok(dz_row, c_tok, dell, inv_temperature, out_dtype):
     """A kept row whose oracle g = c dell invT is exactly 0 (e.g. A = 0 and
     logp_ref = logp in float64): the GPU's g is within dg = |c| invT
@@ -150,13 +164,16 @@ def compare(dl, batch, cfg, rows=None, check_all_tokens=True, oracle_rows_only=F
     assert nd["n_keep_tok"] == int(n[keep_gpu.astype(bool)].sum())
     st = dl.stats_dict()
     if check_all_tokens:
-        scale = float(np.sum(np.abs(ref["c_tok"] * ref["ell"]))) + 1e-300
-        assert abs(st["loss"] - ref["loss"]) <= RTOL_ENT * scale + 1e-12, (st["loss"], ref["loss"])
+        assert abs(st["loss"] - ref["loss"]) <= loss_tol(ref), (st["loss"], ref["loss"])
         rs = ref["stats"]
         for k in ("n_tok", "n_kept_tok", "n_kept_step"):
             assert st[k] == rs[k], k
-        for k in ("sum_w", "sum_adv", "sum_adv2", "sum_kl"):
+        for k in ("sum_w", "sum_adv2", "sum_kl"):
             assert abs(st[k] - rs[k]) <= 1e-5 * (abs(rs[k]) + 1.0), (k, st[k], rs[k])
+        # sum of A over kept tokens: every token of a trajectory carries the same fp32-rounded A,
+        # so the error adds coherently -- bound it by 1e-5 sum|A| <= 1e-5 sqrt(n sum A^2) (Cauchy-Schwarz)
+        sa_tol = 1e-5 * (math.sqrt(rs["n_kept_tok"] * rs["sum_adv2"]) + 1.0)
+        assert abs(st["sum_adv"] - rs["sum_adv"]) <= sa_tol, ("sum_adv", st["sum_adv"], rs["sum_adv"])
         # sum of token entropies: each within RTOL_ENT |H| + ATOL_ENT (H >= 0, so sum |H| = sum H)
         assert abs(st["sum_H"] - rs["sum_H"]) <= RTOL_ENT * abs(rs["sum_H"]) + ATOL_ENT * rs["n_tok"], \
             ("sum_H", st["sum_H"], rs["sum_H"])

@@ -125,6 +125,11 @@ def test_p4_advantages_spec_examples(golden):
     # the flag adv_eps > 0 keeps the group (verl-style)
     A, ok = _adv(e["traj_rewards"], e["traj_steps"], adv_eps=1e-6)
     assert ok[0] == 1 and np.all(A == 0)
+    # exact arithmetic: equal non-dyadic rewards over step counts whose float mean
+    # does not round back to R still give R_bar = R and A = 0 exactly (not residue / eps)
+    for r, steps in ((0.3, [3, 5, 7]), (0.1, [1, 2, 3, 4, 5, 6]), (0.7, [11])):
+        A, ok = _adv([r] * len(steps), steps, adv_eps=1e-6)
+        assert ok[0] == 1 and np.all(A == 0.0), (r, steps, A)
 
 
 def test_p4_advantage_invariants_random_groups():

@@ -1,0 +1,25 @@
+"""Extended randomised parity sweep (on the GPU box): the cases of
+tests/test_fuzz_gpu.py for seeds [a, b) -- main path, fused update (even
+seeds) and virtual ranks (every sixth) -- each against the float64 oracle.
+Usage: python tools/fuzz_more.py 96 600"""
+import sys
+import traceback
+sys.path.insert(0, ".")
+from tests import test_fuzz_gpu as F
+
+a, b = (int(x) for x in sys.argv[1:3])
+fails = []
+for seed in range(a, b):
+    tests = [("main", F.test_fuzz_main_path_vs_oracle)]
+    if seed % 2 == 0:
+        tests.append(("fused", F.test_fuzz_fused_vs_oracle))
+    if seed % 6 == 1:
+        tests.append(("vranks", F.test_fuzz_virtual_ranks_vs_oracle))
+    for name, fn in tests:
+        try:
+            fn(seed)
+        except Exception as e:   # noqa: BLE001  (report and continue)
+            fails.append((seed, name, repr(e)[:300]))
+            print("FAIL", seed, name, repr(e)[:300], flush=True)
+            traceback.print_exc(limit=3)
+print(f"seeds {a}..{b - 1}: {len(fails)} failures", flush=True)
