@@ -1,0 +1,92 @@
+"""Randomised parity sweep of the other paths (the companion of
+tests/test_fuzz_gpu.py, same case generator): the exact full-vocabulary KL
+(NEXT #4) against the oracle with test_kl_gpu's bar, the LM-head-fused
+forward (NEXT #3) against the oracle with test_lmhead_gpu's bar (exact-
+integer operands, so the GEMM is exact), and the chunk-streamed pass with
+random chunk sizes / pool depths, bitwise equal to the resident pass."""
+import numpy as np
+import pytest
+import torch
+
+from paper_2509_23866_b200 import dart, synth
+from paper_2509_23866_b200.stream import StreamedPass
+from tests.gpu_helpers import run_gpu
+from tests.test_fuzz_gpu import draw_case
+
+pytestmark = pytest.mark.gpu
+
+
+def _kl_case(seed):
+    layout, V, dtype, pad_ld, grad_dtype, cfg = draw_case(seed)
+    cfg.kl_mode = dart.KL_EXACT
+    cfg.beta_kl = 0.1 if cfg.beta_kl == 0 else cfg.beta_kl
+    V = max(V, 2)
+    dtype = torch.float32 if V % 4 == 0 and V < 4096 else torch.bfloat16
+    if dtype == torch.bfloat16 and V % 8:
+        V += 8 - V % 8                    # the exact-KL path takes unpadded rows here: 16-byte pitch
+    if dtype == torch.float32 and V % 4:
+        V += 4 - V % 4
+    b = synth.make_batch("fuzz", seed=seed, layout=layout, V=V, dtype=dtype, with_ref=True,
+                         inv_temperature=cfg.inv_temperature)
+    return b, cfg
+
+
+@pytest.mark.parametrize("seed", range(0, 48, 3))
+def test_fuzz_exact_kl_vs_oracle(seed):
+    from tests.test_kl_gpu import _check, _run
+    b, cfg = _kl_case(seed)
+    dl = _run(b, cfg)
+    _check(dl, b, cfg, rows=list(range(b.layout.T)))
+
+
+@pytest.mark.parametrize("seed", range(1, 48, 6))
+def test_fuzz_lmhead_forward_vs_oracle(seed):
+    from tests.test_lmhead_gpu import compare_lm, run_lm
+    rng = np.random.default_rng(5000 + seed)
+    layout, V, _, _, _, cfg = draw_case(seed)
+    V = int(rng.choice([3, 257, 513, 1000, 2049, 3000]))
+    d = int(rng.choice([16, 64, 136, 256]))
+    cfg.ratio_level = dart.RATIO_TOKEN
+    cfg.kl_mode = dart.KL_K3
+    lb = synth.make_lmhead("fuzz", d, seed=seed, V=V, layout=layout, exact=True,
+                           inv_temperature=cfg.inv_temperature)
+    dl, _ = run_lm(lb, cfg)
+    compare_lm(dl, lb, cfg, exact=True)
+
+
+@pytest.mark.parametrize("seed", range(2, 48, 6))
+def test_fuzz_streamed_equals_resident(seed):
+    rng = np.random.default_rng(7000 + seed)
+    layout, V, dtype, pad_ld, grad_dtype, cfg = draw_case(seed)
+    cfg.zero_fill_masked = 1
+    b = synth.make_batch("fuzz", seed=seed, layout=layout, V=V, dtype=dtype, inv_temperature=cfg.inv_temperature)
+    if b.logits.dtype == torch.bfloat16 and V % 8:
+        pytest.skip("streamed pool buffers use the unpadded row pitch")
+    if b.logits.dtype == torch.float32 and V % 4:
+        pytest.skip("streamed pool buffers use the unpadded row pitch")
+    ref = run_gpu(b, cfg)
+    dev = torch.device("cuda")
+    logits = b.logits.to(dev)
+    max_rows = int(rng.integers(max(1, layout.T // 7), layout.T + 2))
+    pool = int(rng.integers(1, 4))
+    sp = StreamedPass(b.layout, b.V, cfg, dev, max_rows=max_rows, pool=pool,
+                      logits_dtype=b.logits.dtype, grad_dtype=ref.grad_dtype)
+    got = torch.empty_like(ref.dlogits)
+
+    def fill(i, buf):
+        c = sp.chunks[i]
+        buf[:c.T_loc].copy_(logits[c.tok_begin:c.tok_end])
+
+    def consume(i, dz):
+        c = sp.chunks[i]
+        got[c.tok_begin:c.tok_end].copy_(dz)
+
+    sp.run(b.target.to(dev), b.logp_old.to(dev), b.logp_rollout.to(dev), b.logp_ref.to(dev), fill=fill,
+           consume=consume)
+    torch.cuda.synchronize()
+    sp.check_status()
+    assert torch.equal(sp.keep[:b.layout.S], ref.keep[:b.layout.S])
+    assert torch.equal(sp.norm, ref.norm)
+    assert torch.equal(got, ref.dlogits)
+    L = ref.stats_dict()["loss"]
+    assert abs(sp.stats_dict()["loss"] - L) <= 1e-12 * abs(L) + 1e-15

@@ -1,11 +1,14 @@
 """Extended randomised parity sweep (on the GPU box): the cases of
-tests/test_fuzz_gpu.py for seeds [a, b) -- main path, fused update (even
-seeds) and virtual ranks (every sixth) -- each against the float64 oracle.
+tests/test_fuzz_gpu.py / test_fuzz_paths_gpu.py for seeds [a, b) -- main
+path, fused update (even seeds), virtual ranks, exact KL, LM-head forward and
+the streamed pass (subsets of seeds) -- each against the float64 oracle or the
+resident pass.
 Usage: python tools/fuzz_more.py 96 600"""
 import sys
 import traceback
 sys.path.insert(0, ".")
 from tests import test_fuzz_gpu as F
+from tests import test_fuzz_paths_gpu as P
 
 a, b = (int(x) for x in sys.argv[1:3])
 fails = []
@@ -15,10 +18,18 @@ for seed in range(a, b):
         tests.append(("fused", F.test_fuzz_fused_vs_oracle))
     if seed % 6 == 1:
         tests.append(("vranks", F.test_fuzz_virtual_ranks_vs_oracle))
+    if seed % 3 == 0:
+        tests.append(("exact_kl", P.test_fuzz_exact_kl_vs_oracle))
+    if seed % 6 == 1:
+        tests.append(("lmhead", P.test_fuzz_lmhead_forward_vs_oracle))
+    if seed % 6 == 2:
+        tests.append(("stream", P.test_fuzz_streamed_equals_resident))
     for name, fn in tests:
         try:
             fn(seed)
         except Exception as e:   # noqa: BLE001  (report and continue)
+            if type(e).__name__ == "Skipped":
+                continue
             fails.append((seed, name, repr(e)[:300]))
             print("FAIL", seed, name, repr(e)[:300], flush=True)
             traceback.print_exc(limit=3)
