@@ -12,6 +12,13 @@ from tests.gpu_helpers import ATOL_ENT, ATOL_LOGP, ATOL_TOK, RTOL_ENT, RTOL_TOK,
 
 pytestmark = pytest.mark.gpu
 
+# Absolute accuracy of one token's exact KL on the GPU: KL_t = sum_v p (z' - z'_ref)
+# - (lse - lse_ref) comes from fp32-accumulated sums (flushed to fp64 every 8
+# chunks) of terms of size |z' - z'_ref| ~ |lse - lse_ref| + O(1), so it carries
+# ~1e-7 absolute error however small KL_t is; a bar relative to
+# KL_t alone fails on near-identical policies (KL ~ 1e-8 .. 1e-3 per token).
+KL_ATOL = 4e-7
+
 
 def _run(b, cfg, grad_dtype=None):
     dev = torch.device("cuda")
@@ -41,8 +48,11 @@ def _check(dl, b, cfg, rows):
     assert np.all(np.abs(ell[ok] - ref["ell"][ok]) <= RTOL_TOK * np.abs(ref["ell"][ok]) + ATOL_TOK)
     st = dl.stats_dict()
     scale = float(np.sum(np.abs(ref["c_tok"] * ref["ell"]))) + 1e-300
-    assert abs(st["loss"] - ref["loss"]) <= RTOL_ENT * scale + 1e-12
-    assert abs(st["sum_kl"] - ref["stats"]["sum_kl"]) <= 1e-5 * abs(ref["stats"]["sum_kl"]) + 1e-6
+    kl_slack = cfgf["beta_kl"] * KL_ATOL * float(np.sum(np.abs(ref["c_tok"])))
+    assert abs(st["loss"] - ref["loss"]) <= RTOL_ENT * scale + kl_slack + 1e-12, (st["loss"], ref["loss"])
+    n_kept = ref["stats"]["n_kept_tok"]
+    assert abs(st["sum_kl"] - ref["stats"]["sum_kl"]) <= 1e-5 * abs(ref["stats"]["sum_kl"]) + KL_ATOL * n_kept + 1e-9, \
+        (st["sum_kl"], ref["stats"]["sum_kl"])
     dz = dl.dlogits.float().cpu().numpy()
     invT = cfgf["inv_temperature"]
     for t in rows:

@@ -27,9 +27,11 @@ for seed in range(a, b):
     for name, fn in tests:
         try:
             fn(seed)
-        except Exception as e:   # noqa: BLE001  (report and continue)
+        except BaseException as e:   # noqa: BLE001  (report and continue; pytest.skip is a BaseException)
             if type(e).__name__ == "Skipped":
                 continue
+            if isinstance(e, KeyboardInterrupt):
+                raise
             fails.append((seed, name, repr(e)[:300]))
             print("FAIL", seed, name, repr(e)[:300], flush=True)
             traceback.print_exc(limit=3)
