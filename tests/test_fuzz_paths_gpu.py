@@ -90,3 +90,23 @@ def test_fuzz_streamed_equals_resident(seed):
     assert torch.equal(got, ref.dlogits)
     L = ref.stats_dict()["loss"]
     assert abs(sp.stats_dict()["loss"] - L) <= 1e-12 * abs(L) + 1e-15
+
+
+@pytest.mark.parametrize("seed", range(3, 48, 8))
+def test_fuzz_lmhead_update_vs_oracle(seed):
+    """The LM-head update pass (dz from the z-GEMM epilogue, cuBLAS dh / dW) on
+    random layouts, shapes, chunkings and hyper-parameters (clip bounds kept
+    wide, as in test_lmhead_update_gpu, so dW is comparable element-wise)."""
+    from tests.test_lmhead_update_gpu import check_update
+    rng = np.random.default_rng(9000 + seed)
+    layout, _, _, _, _, cfg = draw_case(seed)
+    V = int(rng.choice([776, 1032, 2048, 3000]))   # the update needs V % 8 == 0
+    d = int(rng.choice([64, 128, 200, 256]))
+    exact = bool(rng.random() < 0.5)
+    cfg.ratio_level = dart.RATIO_TOKEN
+    cfg.kl_mode = dart.KL_K3
+    cfg.eps_low = cfg.eps_high = 0.95
+    chunk_rows = None if rng.random() < 0.5 else int(rng.integers(max(1, layout.T // 5), layout.T + 1))
+    lb = synth.make_lmhead("fuzz", d, seed=seed, V=V, layout=layout, exact=exact,
+                           inv_temperature=cfg.inv_temperature)
+    check_update(lb, cfg, chunk_rows, exact)

@@ -19,7 +19,7 @@ import torch
 
 from oracle import dart_oracle as O
 from paper_2509_23866_b200 import dart, lmhead, synth
-from tests.gpu_helpers import ATOL_TOK, P_REL, RTOL_ENT, RTOL_TOK, bf16_ulp
+from tests.gpu_helpers import ATOL_LOGP, ATOL_TOK, P_REL, RTOL_ENT, RTOL_TOK, bf16_ulp
 
 pytestmark = pytest.mark.gpu
 
@@ -70,9 +70,15 @@ def test_lmhead_update_matches_oracle(d, V, chunk_rows, exact):
     # branch can flip under the logits' GEMM error and dW (a sum over all rows) is
     # comparable element by element; the paper's bounds are covered row-wise below
     cfg = dart.Config(entropy_q=0.3, eps_low=0.95, eps_high=0.95)
+    check_update(lb, cfg, chunk_rows, exact, expect_chunks=bool(chunk_rows))
+
+
+def check_update(lb, cfg, chunk_rows, exact, expect_chunks=False):
+    """The update pass on `lb` against the oracle (the error model above)."""
+    d, V = lb.hidden.shape[1], lb.batch.V
     old = old_pass(lb, cfg)
     up, dh, dW = run_update(lb, cfg, old.keep, old.norm, chunk_rows)
-    if chunk_rows:
+    if expect_chunks:              # (chunks are whole trajectories: a fuzz batch may have one)
         assert len(up.chunks) > 1
     cfgf = cfg.as_f32()
     invT = cfgf["inv_temperature"]
@@ -106,9 +112,20 @@ def test_lmhead_update_matches_oracle(d, V, chunk_rows, exact):
     dh_ref, dW_ref = O.lmhead_grads(dz, h, W)
     rel = (2.0 ** -8 + (RTOL_TOK + 4 * Ez) + 2 * Ez * invT + ATOL_TOK / np.maximum(np.abs(ref["dell"]), 1e-30))[:, None]
     a = np.zeros_like(dz)
-    for t in np.nonzero(ref["c_tok"] * ref["dell"])[0]:
-        a[t] = abs(ref["c_tok"][t] * ref["dell"][t]) * invT * (P_REL + 2 * Ez * invT) * \
-            O.log_softmax_row(ob["logits"][t], invT)[1]
+    beta = cfgf["beta_kl"]
+    for t in np.nonzero(ref["c_tok"])[0]:
+        p_t = O.log_softmax_row(ob["logits"][t], invT)[1]
+        a[t] = abs(ref["c_tok"][t] * ref["dell"][t]) * invT * (P_REL + 2 * Ez * invT) * p_t
+        # dell's sensitivity to the log-prob error: |d dell / d logp| = |-w A r act + beta e^d|
+        # times ATOL_LOGP + 4 Ez invT (the forward's lse and the dz kernel's recomputed z are two
+        # GEMMs, each within Ez) -- an absolute term that matters where dell itself is ~0
+        # (A = 0 and logp_ref = logp: the fuzz's degenerate rows, tests/test_fuzz_paths_gpu.py)
+        sens = abs(ref["w"][t] * ref["A_tok"][t] * ref["r"][t]) + beta * np.exp(ob["logp_ref"][t] - ref["logp"][t])
+        onehot = np.zeros_like(p_t)
+        onehot[int(ob["target"][t])] = 1.0
+        # ... times |delta - p| as the GPU sees it: p within (P_REL + 4 Ez invT) p (near-one-hot rows)
+        a[t] += abs(ref["c_tok"][t]) * invT * sens * (ATOL_LOGP + 4 * Ez * invT) * \
+            (np.abs(onehot - p_t) + (P_REL + 4 * Ez * invT) * p_t)
     tol_dh = (rel + V * U) * (np.abs(dz) @ np.abs(W)) + a @ np.abs(W) + 1e-30
     tol_dW = ((rel + T * U) * np.abs(dz) + a).T @ np.abs(h) + 1e-30
     e_dh = np.abs(dh.cpu().numpy() - dh_ref)

@@ -24,6 +24,8 @@ for seed in range(a, b):
         tests.append(("lmhead", P.test_fuzz_lmhead_forward_vs_oracle))
     if seed % 6 == 2:
         tests.append(("stream", P.test_fuzz_streamed_equals_resident))
+    if seed % 8 == 3:
+        tests.append(("lmupdate", P.test_fuzz_lmhead_update_vs_oracle))
     for name, fn in tests:
         try:
             fn(seed)
