@@ -18,6 +18,8 @@ for seed in range(a, b):
         tests.append(("fused", F.test_fuzz_fused_vs_oracle))
     if seed % 6 == 1:
         tests.append(("vranks", F.test_fuzz_virtual_ranks_vs_oracle))
+    if seed % 8 == 5:
+        tests.append(("zero_fill_off", F.test_fuzz_zero_fill_off))
     if seed % 3 == 0:
         tests.append(("exact_kl", P.test_fuzz_exact_kl_vs_oracle))
     if seed % 6 == 1:
