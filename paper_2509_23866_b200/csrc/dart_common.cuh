@@ -124,6 +124,14 @@ __device__ __forceinline__ uint4 lds128(const void* p) {
 // data dependency also closes it but stalls every chunk on the load latency,
 // 2-3% on the sweeps; the fence costs nothing measurable, A/B in
 // profiles/r02_ring_fence.md.)
+// Start value of a per-lane running maximum (log2 domain) when padding and
+// -inf logits are clamped to NEG_CLAMP: NEG_CLAMP * c2 rounded TOWARD ZERO.
+// A lane that only ever sees clamped values then gets
+// 2^fma(NEG_CLAMP, c2, -m0) = 2^(<= 0) instead of 2^(+half an ulp of ~1.4e30)
+// = inf (the round-to-nearest product can sit below the exact one), whose
+// product with the fold's zero weight was a NaN row.
+__device__ __forceinline__ float clamp_max0(float c2) { return __fmul_rz(NEG_CLAMP, c2); }
+
 __device__ __forceinline__ void fence_reads_before_refill() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }

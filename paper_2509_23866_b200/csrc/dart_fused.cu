@@ -192,7 +192,7 @@ __global__ void fused_rec_kernel(FusedParams p, FusedRec* rec) {
 __device__ float fused_epilogue(const FusedParams& p, int64_t t, const FusedRec& rc, double Mr, double L2s,
                                 bool write = true) {
   uint32_t bits = rc.flags >> 8;
-  if (Mr <= (double)(NEG_CLAMP * p.c2)) bits |= DART_STATUS_ROW_ALL_NEGINF;
+  if (Mr <= (double)clamp_max0(p.c2)) bits |= DART_STATUS_ROW_ALL_NEGINF;
   const double lse2 = Mr + L2s;
   const float logp = (float)(((double)rc.zy * (double)p.c2 - Mr - L2s) * LN2_D);
   const float r = expf(logp - rc.lo);
@@ -621,7 +621,7 @@ __global__ void __launch_bounds__(FU_THREADS, DART_FU_CTAS) fused_sweep_kernel(c
 
   int64_t tk = fu_next_kept(recs, ra, rb);
   while (tk < rb) {
-    float m = NEG_CLAMP * c2;
+    float m = clamp_max0(c2);                       // (see dart_common.cuh)
     float2 s01 = make_float2(0.f, 0.f), s23 = make_float2(0.f, 0.f);
     pass1(0u, cw, m, s01, s23);
     publish(m, s01, s23);                            // non-blocking: the reducer folds

@@ -37,8 +37,6 @@ __device__ __forceinline__ void unpack8(const uint4& xv, float* z) {
   }
 }
 
-__device__ __forceinline__ float kl_m0(float c2) { return __fmul_rz(NEG_CLAMP, c2); }
-
 template <typename Tin>
 __device__ __forceinline__ uint4 neg_clamp_vec() {
   if (sizeof(Tin) == 2) {
@@ -125,7 +123,7 @@ __device__ void kl_row_epilogue(const FwdParams& p, int64_t row, double M, doubl
   else zy = is_bf16 ? logit_at<__nv_bfloat16>(p.logits + row * p.ld_bytes, y) : logit_at<float>(p.logits + row * p.ld_bytes, y);
   if (!isfinite(lo) || !isfinite(lr)) bits |= DART_STATUS_NONFINITE_LOGP;
   if (zy == -INFINITY) bits |= DART_STATUS_TARGET_NEGINF;
-  if (M <= (double)kl_m0(p.c2)) bits |= DART_STATUS_ROW_ALL_NEGINF;
+  if (M <= (double)clamp_max0(p.c2)) bits |= DART_STATUS_ROW_ALL_NEGINF;
   const double L2s = log2(S), L2r = log2(Sr);
   const double lse2 = M + L2s, lse2r = Mr + L2r;
   double H = LN2_D * (L2s - U / S);
@@ -205,11 +203,9 @@ fwd_kl_kernel(const FwdParams p) {
   uint32_t phase = 0;
 #pragma unroll 1
   for (int64_t row = wid; row < p.T_loc; row += W) {
-    // running maxima start at NEG_CLAMP * c2 rounded toward zero: a lane that
-    // only ever sees NEG_CLAMP padding (rows of fewer than 32 vectors) then
-    // gets 2^(fma(NEG_CLAMP, c2, -m)) = 2^(<= 0), never 2^(+half an ulp of
-    // 1.4e30) = inf, whose product with the fold's zero factor was NaN
-    float m = kl_m0(c2), mr = kl_m0(c2);
+    // running maxima start at NEG_CLAMP * c2 rounded toward zero (dart_common.cuh):
+    // lanes that only see NEG_CLAMP padding (rows of fewer than 32 vectors)
+    float m = clamp_max0(c2), mr = clamp_max0(c2);
     float2 s[4], u[4], D[4], sr[4];
 #pragma unroll
     for (int j = 0; j < 4; ++j) s[j] = u[j] = D[j] = sr[j] = make_float2(0.f, 0.f);

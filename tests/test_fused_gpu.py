@@ -14,8 +14,8 @@ from tests.gpu_helpers import (ATOL_ENT, ATOL_LOGP, ATOL_TOK, P_REL, RTOL_ENT, R
 pytestmark = pytest.mark.gpu
 
 
-def _fused_case(name, cfg, seed=0, grad_dtype=None, rows=None, **kw):
-    b = synth.make_batch(name, seed=seed, **kw)
+def _fused_case(name, cfg, seed=0, grad_dtype=None, rows=None, batch=None, **kw):
+    b = batch if batch is not None else synth.make_batch(name, seed=seed, **kw)
     old = run_gpu(b, cfg, grad_dtype=grad_dtype)          # old-policy pass -> mask + norm
     old.check_status()
     keep = old.keep.clone()

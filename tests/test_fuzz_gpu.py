@@ -169,3 +169,13 @@ def test_fuzz_zero_fill_off(seed):
             #      elsewhere); here: kept rows written and finite
             assert torch.isfinite(dl.dlogits[kt].float()).all(), mode
         assert torch.isnan(dl.dlogits[~kt].float()).all(), mode
+
+
+@pytest.mark.parametrize("seed", range(1, N_CASES, 4))
+def test_fuzz_fused_hard_inputs_vs_oracle(seed):
+    """The fused update on the main-path sweep's inputs (8x sharper rows, -inf
+    entries, padded pitches) -- the inputs that exposed the running-max start
+    value bug (clamp_max0 in dart_common.cuh)."""
+    b, grad_dtype, cfg = _make(seed)
+    cfg.ratio_level = dart.RATIO_TOKEN
+    _fused_case("fuzz", cfg, seed=seed, grad_dtype=grad_dtype, batch=b)

@@ -16,6 +16,8 @@ for seed in range(a, b):
     tests = [("main", F.test_fuzz_main_path_vs_oracle)]
     if seed % 2 == 0:
         tests.append(("fused", F.test_fuzz_fused_vs_oracle))
+    else:
+        tests.append(("fused_hard", F.test_fuzz_fused_hard_inputs_vs_oracle))
     if seed % 6 == 1:
         tests.append(("vranks", F.test_fuzz_virtual_ranks_vs_oracle))
     if seed % 8 == 5:
