@@ -8,7 +8,7 @@ import torch
 
 from oracle import dart_oracle as O
 from paper_2509_23866_b200 import dart, synth
-from tests.gpu_helpers import ATOL_ENT, ATOL_LOGP, ATOL_TOK, RTOL_ENT, RTOL_TOK, bf16_ulp, oracle_select_on
+from tests.gpu_helpers import ATOL_ENT, ATOL_LOGP, ATOL_TOK, RTOL_ENT, RTOL_TOK, bf16_ulp, oracle_select_on, p_rel_row
 
 pytestmark = pytest.mark.gpu
 
@@ -32,7 +32,11 @@ def _run(b, cfg, grad_dtype=None):
     return dl
 
 
-def _check(dl, b, cfg, rows):
+def _check(dl, b, cfg, rows, grad_atol=0.0):
+    """grad_atol: an absolute floor for the dlogits comparison (the north_star's
+    2e-3 on bf16 gradients) -- used for the stress inputs of the path fuzz,
+    whose 8x sharper rows and masked vocabularies are outside the per-element
+    error model below; 0 keeps the model alone."""
     cfgf = cfg.as_f32()
     L = b.layout
     keep = dl.keep.cpu().numpy()[:L.S]
@@ -64,16 +68,24 @@ def _check(dl, b, cfg, rows):
             continue
         _, p = O.log_softmax_row(ob["logits"][t], invT)
         klt, lpq = O.kl_exact_row(ob["logits"][t], ob["ref_logits"][t], invT)
+        lpq = np.where(p > 0, np.nan_to_num(lpq, nan=0.0, posinf=0.0, neginf=0.0), 0.0)   # p = 0: no term
         dref = ref["dz"][t]
         # error model: 1 output ulp + dell's tolerance through |delta - p| + the fp32
-        # error of p and of (log p - log q) in the KL term
+        # error of p (p_rel_row: grows with the exponent's magnitude) and of
+        # (log p - log q) = (z' - z'_ref) - (lse - lse_ref), whose fp32 terms are
+        # each exact to 2^-24 of their size (rows of 8x sharper logits reach ~250)
         onehot = np.zeros_like(p)
         onehot[ob["target"][t]] = 1.0
         a = abs(c * invT)
+        zf = np.abs(np.where(np.isfinite(ob["logits"][t]), ob["logits"][t], 0.0)).max() * invT
+        zrf = np.abs(np.where(np.isfinite(ob["ref_logits"][t]), ob["ref_logits"][t], 0.0)).max() * invT
+        lpq_err = 2e-5 + 2.0 ** -21 * (zf + zrf)
+        prel = p_rel_row(ob["logits"][t], ref["lse"][t], invT)
         tol = (bf16_ulp(dref) if dl.grad_dtype == torch.bfloat16 else np.abs(dref) * 2.0 ** -22)
         tol = tol + a * (RTOL_TOK * abs(ref["dell"][t]) + ATOL_TOK) * np.abs(onehot - p)
-        tol = tol + a * 4e-6 * p * (abs(ref["dell"][t]) + cfgf["beta_kl"] * (np.abs(lpq) + klt + 1.0))
-        tol = tol + a * cfgf["beta_kl"] * p * 2e-5 * (1.0 + np.abs(lpq)) + 1e-38
+        tol = tol + a * prel * p * (abs(ref["dell"][t]) + cfgf["beta_kl"] * (np.abs(lpq) + klt + 1.0))
+        tol = tol + a * cfgf["beta_kl"] * p * lpq_err * (1.0 + np.abs(lpq)) + 1e-38
+        tol = np.maximum(tol, grad_atol)
         err = np.abs(dz[t] - dref)
         assert np.all(err <= tol), (t, np.argmax(err - tol), err.max())
 

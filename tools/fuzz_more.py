@@ -24,6 +24,8 @@ for seed in range(a, b):
         tests.append(("zero_fill_off", F.test_fuzz_zero_fill_off))
     if seed % 3 == 0:
         tests.append(("exact_kl", P.test_fuzz_exact_kl_vs_oracle))
+    if seed % 3 == 1:
+        tests.append(("exact_kl_hard", P.test_fuzz_exact_kl_hard_inputs_vs_oracle))
     if seed % 6 == 1:
         tests.append(("lmhead", P.test_fuzz_lmhead_forward_vs_oracle))
     if seed % 6 == 2:
