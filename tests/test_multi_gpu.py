@@ -36,10 +36,16 @@ def _port():
 
 
 def _cfg(name):
+    if name.startswith("fuzz/"):       # a randomised case of tests/test_fuzz_gpu.py
+        from tests.test_fuzz_gpu import _make
+        return _make(int(name[5:]))[2]
     return dart.Config(is_cap=2.0) if name.startswith("tiny") else dart.Config()
 
 
 def _batch(name, seed):
+    if name.startswith("fuzz/"):
+        from tests.test_fuzz_gpu import _make
+        return _make(int(name[5:]))[0]
     _, V, dt, _ = synth.config_layout(name, seed)
     per = 16 // (2 if dt == torch.bfloat16 else 4)
     return synth.make_batch(name, seed=seed, pad_ld=-(-V // per) * per)
@@ -107,7 +113,7 @@ def _check(parts, name, seed, sample):
     for r, p in enumerate(parts):
         for i in range(*p["traj"]):
             owners.setdefault(int(b.layout.traj_group[i]), set()).add(r)
-    if name != "mid":      # the adaptive mix (and tiny over 5 ranks) puts groups across ranks: C1 matters
+    if name != "mid" and not name.startswith("fuzz/"):   # adaptive mix / tiny over 5 ranks: groups straddle ranks
         assert any(len(rs) > 1 for rs in owners.values())
     rows = _rows(name, seed, sample, b.layout.T, [p["tok"][0] for p in parts if p["tok"][1] > p["tok"][0]])
     compare(view, b, cfg, rows=rows)
@@ -133,3 +139,13 @@ def test_gloo_more_ranks_than_trajectories():
     from paper_2509_23866_b200 import dist as D
     assert any(s.T_loc == 0 for s in D.shard_layout(synth.make_batch("tiny", seed=1).layout, 5))
     _check(_run("gloo", 5, "tiny", 1), "tiny", 1, None)
+
+
+@pytest.mark.parametrize("seed,world", [(11, 2), (23, 3), (42, 4)])
+def test_gloo_ranks_one_gpu_fuzz_vs_oracle(seed, world):
+    """Randomised batches of tests/test_fuzz_gpu.py (ragged groups, odd / padded
+    vocabularies, -inf entries, random configurations) over real gloo process
+    groups sharing one GPU: the collectives' padding and empty shards on
+    random layouts, every rank checked against the oracle."""
+    name = f"fuzz/{seed}"
+    _check(_run("gloo", world, name, seed), name, seed, None)
